@@ -1,0 +1,208 @@
+/*
+ * ctkv.h -- C ABI of the B200 (sm_100a) CTkvr hot path.
+ *
+ * Drop-in boundary for the reference package `centroidkv` 0.1.0, whose
+ * public hot-path API is Python (ck/__init__.py:10-35; ck = the package at
+ * /root/reference/pkg/src/centroidkv).  The reference has no FFI, so each
+ * entry point below names the Python function it replaces; the Python
+ * mirror in paper_2512_15550_b200/ binds these through ctypes
+ * (INTEGRATION.md shows the binding).
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer unless documented otherwise; calls
+ *    are asynchronous on the caller's stream (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream).
+ *  - Caller allocates everything, including a workspace whose size the
+ *    matching *_workspace_bytes() query returns.  No hidden allocation.
+ *  - Status is returned as int (CTKV_OK == 0); nothing throws across C.
+ *    Data-dependent conditions found on the device (empty recall, zero
+ *    norms, ids out of range) are reported through a caller-provided
+ *    int32 `flags` word (CTKV_FLAG_*), sticky (OR-ed).
+ *  - Tensor layouts follow the reference exactly: K/V [b,g,cap,d]
+ *    token-major per (b,g) (ck/store.py:41-44), centroids [b,h,C,d],
+ *    lists [b,g,C,rho] int32 with -1 = empty (ck/index.py:35-55),
+ *    fifo_head [b] int64.
+ *  - Scores that drive selections accumulate in float64; attention outputs
+ *    are float32 [b,h,d] with float64 row_max / denom
+ *    (ck/retrieval.py:50-58).
+ */
+#ifndef CTKV_H
+#define CTKV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CTKV_ABI_VERSION 1
+
+enum ctkv_dtype { CTKV_F32 = 0, CTKV_BF16 = 1 };
+
+enum ctkv_status {
+  CTKV_OK = 0,
+  CTKV_ESHAPE = 1,     /* -> ShapeError     (ck/errors.py:8-9)   */
+  CTKV_ECONFIG = 2,    /* -> ConfigError    (ck/errors.py:12-13) */
+  CTKV_EINDEX = 3,     /* -> IndexError     (ck/store.py:146-147) */
+  CTKV_ECUDA = 4,      /* -> RuntimeError                         */
+  CTKV_EWORKSPACE = 5  /* workspace too small -> RuntimeError      */
+};
+
+enum ctkv_flag {
+  CTKV_FLAG_DEGENERATE = 1,      /* zero-norm vector: DegenerateQueryWarning (ck/tensor_ops.py:202-206) */
+  CTKV_FLAG_EMPTY_RECALL = 2,    /* some (b,g) recalled nothing                */
+  CTKV_FLAG_NONEMPTY_RECALL = 4, /* some (b,g) recalled something; both set => the
+                                    reference's "mixed empty/nonempty" ConfigError
+                                    (ck/retrieval.py:326-327)                    */
+  CTKV_FLAG_ID_RANGE = 8,        /* token id outside [0,total): IndexError       */
+  CTKV_FLAG_CAPACITY = 16,       /* device buffer limit hit (see ctkv_status_string) */
+  CTKV_FLAG_DUP_IDS = 32,        /* duplicate ids in an attention set (ck/retrieval.py:261-262) */
+  CTKV_FLAG_BUILD_FALLBACK = 64, /* build rows re-done on the exact fallback path (info) */
+  CTKV_FLAG_NO_TOKENS = 128      /* nothing attendable: ConfigError (ck/retrieval.py:355) */
+};
+
+/* Dimensions shared by every call (ck/tensor_ops.py:25-55 HeadLayout plus
+ * the partition lengths of ck/store.py:34-39). */
+typedef struct ctkv_layout {
+  int32_t batch;        /* b  (the local shard's batch) */
+  int32_t query_heads;  /* h */
+  int32_t kv_heads;     /* g  (h % g == 0, h/g <= 16) */
+  int32_t head_dim;     /* d in {16,32,64,128,256} */
+  int64_t capacity;     /* token rows allocated per (b,g) in K and V */
+  int32_t dtype;        /* enum ctkv_dtype of K, V, queries and centroids */
+  int32_t init_len;     /* L_init */
+  int32_t local_len;    /* L_local */
+  int32_t reserved;
+} ctkv_layout;
+
+/* Device state of one QueryCentroidIndex (ck/index.py:35-55). */
+typedef struct ctkv_index {
+  void* centroids;      /* [b,h,C,d] dtype, raw (not normalised) queries */
+  int32_t* lists;       /* [b,g,C,rho] int32, -1 = empty */
+  int64_t* fifo_head;   /* [b] FIFO cursor (ck/index.py:55,121,133) */
+  int32_t* sync;        /* [1+b] int32 scratch, zero-initialised once, owned by the index */
+  int32_t capacity;     /* C */
+  int32_t rho;          /* list length */
+} ctkv_index;
+
+/* Device state of one KvStore (ck/store.py:23-44). */
+typedef struct ctkv_store {
+  void* keys;           /* [b,g,capacity,d] */
+  void* values;         /* [b,g,capacity,d] */
+  int64_t* total;       /* device scalar: tokens stored (ck/store.py:75-76) */
+} ctkv_store;
+
+/* One fused decode step (replaces ck/retrieval.py:304-378 decode_step,
+ * preceded by ck/store.py:114-129 append when k_new != NULL, exactly the
+ * order of ck/session.py:58-60 run_decode). */
+typedef struct ctkv_step_args {
+  const void* query;    /* [b,h,d] dtype */
+  const void* k_new;    /* [b,g,d] dtype or NULL (no append this step) */
+  const void* v_new;    /* [b,g,d] dtype or NULL */
+  int32_t c_prime;      /* C'  (1 <= C' <= C) */
+  int32_t rho_prime;    /* rho' */
+  int32_t use_dcu;      /* FIFO dynamic centroid update (ck/index.py:103-133) */
+  int32_t use_rerank;   /* 0: attend the whole recall set (ck/retrieval.py:334-337) */
+  /* outputs; every one but `out` may be NULL */
+  float* out;           /* [b,h,d] merged attention output */
+  double* row_max;      /* [b,h] merged running max */
+  double* denom;        /* [b,h] merged denominator */
+  int32_t* selected;    /* [b,g,C'] centroid slots, cosine-descending */
+  int32_t* recall_len;  /* [b,g] */
+  int32_t* sparse_ids;  /* [b,g,sparse_cap] score-descending (recall order when !use_rerank) */
+  int32_t* sparse_len;  /* [b,g] */
+  int32_t sparse_cap;   /* row stride of sparse_ids */
+  int32_t* flags;       /* sticky CTKV_FLAG_* word (device) or NULL */
+} ctkv_step_args;
+
+int ctkv_abi_version(void);
+const char* ctkv_status_string(int status);
+/* 1 if the current device is sm_100 and the kernels load; else 0. */
+int ctkv_device_ok(void);
+
+/* ---- storage (ck/store.py) -------------------------------------------- */
+
+/* KvStore.append (ck/store.py:114-129): write [b,g,d] rows at *total, ++*total. */
+int ctkv_append(const ctkv_layout* L, ctkv_store S, const void* k_new, const void* v_new,
+                void* stream);
+
+/* ---- prefill index build (ck/index.py:59-99, Alg. 1) --------------------- */
+
+enum ctkv_build_mode {
+  CTKV_BUILD_EXACT = 0,  /* SIMT float64-accumulating scores (fp32 parity config) */
+  CTKV_BUILD_FAST = 1    /* tensor-core bf16 scores, fp32 accumulation */
+};
+
+size_t ctkv_build_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32_t rho,
+                                  int64_t n_off, int32_t mode);
+/* QueryCentroidIndex.build: for each (b,g,c) write the top-rho token ids of
+ * keys[b,g,off_begin:off_begin+n_off] by GQA group-max of
+ * f32((centroids[b,h,c] . k) / sqrt(d)), ordered (score desc, id asc). */
+int ctkv_build_lists(const ctkv_layout* L, const void* centroids, const void* keys,
+                     int64_t off_begin, int64_t n_off, int32_t capacity, int32_t rho,
+                     int32_t mode, int32_t* lists, int32_t* flags, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
+/* ---- decode (ck/retrieval.py) --------------------------------------------- */
+
+size_t ctkv_decode_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32_t rho,
+                                   int32_t c_prime, int32_t rho_prime);
+
+/* decode_step (+ append): recall -> rerank -> sparse + static attention ->
+ * merge -> DCU, all on the device, no host synchronisation. */
+int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctkv_step_args* A,
+                     void* workspace, size_t workspace_bytes, void* stream);
+
+/* recall (ck/retrieval.py:132-168): selected [b,g,C'], recalled
+ * [b,g,C'*rho] first-occurrence order, recall_len [b,g].  Like the
+ * reference it needs no store: `id_bound` is an exclusive upper bound of
+ * the token ids held in the lists (the store's total at build time; DCU
+ * only ever re-lists recalled ids, so it never grows). */
+int ctkv_recall(const ctkv_layout* L, ctkv_index I, int64_t id_bound, const void* query,
+                int32_t c_prime, int32_t* selected, int32_t* recalled, int32_t* recall_len,
+                int32_t* flags, void* workspace, size_t workspace_bytes, void* stream);
+
+/* rerank scores + order (ck/retrieval.py:171-218): grouped [b,g,lmax] f64
+ * group-max logits of the recalled ids; order [b,g,lmax] = positions into
+ * `recalled` sorted (score desc, position asc). */
+int ctkv_rerank(const ctkv_layout* L, ctkv_store S, const void* query, const int32_t* recalled,
+                const int32_t* recall_len, int32_t lmax, double* grouped, int32_t* order,
+                int32_t* flags, void* workspace, size_t workspace_bytes, void* stream);
+
+/* attention partial over per-(b,g) id lists (ck/retrieval.py:221-264);
+ * ids [b,g,lmax] (or [lmax] when ids_shared), optionally united with the
+ * static partition (ck/store.py:94-96) -- the merge is exact. */
+size_t ctkv_attend_workspace_bytes(const ctkv_layout* L, int32_t lmax, int32_t with_static);
+int ctkv_attend(const ctkv_layout* L, ctkv_store S, const void* query, const int32_t* ids,
+                const int32_t* ids_len, int32_t lmax, int32_t ids_shared, int32_t with_static,
+                float* out, double* row_max, double* denom, int32_t* flags, void* workspace,
+                size_t workspace_bytes, void* stream);
+
+/* merge (ck/retrieval.py:275-284) of two partials over `rows` = b*h rows. */
+int ctkv_merge(int64_t rows, int32_t head_dim, const float* out_a, const double* max_a,
+               const double* den_a, const float* out_b, const double* max_b,
+               const double* den_b, float* out, double* row_max, double* denom, void* stream);
+
+/* fifo_update (ck/index.py:103-133): slot = fifo_head[b] % C gets the
+ * query and, per kv head, the top-min(rho, L) recalled ids by `grouped`. */
+int ctkv_fifo_update(const ctkv_layout* L, ctkv_index I, const void* query,
+                     const int32_t* recalled, const int32_t* recall_len, int32_t lmax,
+                     const double* grouped, void* workspace, size_t workspace_bytes,
+                     void* stream);
+
+/* dot_scores + group_max (ck/tensor_ops.py:72-118) as a device primitive:
+ * out [b,g,m,n] f32 (grouped=1) or [b,h,m,n] (grouped=0). */
+int ctkv_scores(const ctkv_layout* L, const void* q, int64_t m, const void* k, int64_t n,
+                int64_t k_row_stride, int32_t grouped, float* out, void* stream);
+
+/* top_k_rows (ck/tensor_ops.py:144-169) on the device: rows [r,n] f32 ->
+ * idx [r,k] int32 ordered (value desc, index asc). */
+size_t ctkv_topk_workspace_bytes(int64_t rows, int64_t n, int32_t k);
+int ctkv_topk_rows(const float* values, int64_t rows, int64_t n, int32_t k, int32_t* idx,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CTKV_H */

@@ -1,0 +1,393 @@
+// extern "C" entry points of libctkv.so (declared in include/ctkv.h).
+// Validation mirrors the reference's exception contract: shape problems
+// -> CTKV_ESHAPE (ShapeError), precondition violations -> CTKV_ECONFIG
+// (ConfigError, e.g. ck/retrieval.py:136-139), CUDA failures -> CTKV_ECUDA.
+#include <algorithm>
+#include <cstring>
+
+#include "ctkv.h"
+#include "ctkv_internal.h"
+
+using namespace ctkv;
+
+namespace {
+
+size_t a256(size_t x) { return (x + 255) & ~size_t(255); }
+
+bool dim_ok(int d) { return d == 16 || d == 32 || d == 64 || d == 128 || d == 256; }
+
+int check_layout(const ctkv_layout* L) {
+  if (!L) return CTKV_ESHAPE;
+  if (L->batch < 1 || L->query_heads < 1 || L->kv_heads < 1) return CTKV_ESHAPE;
+  if (L->query_heads % L->kv_heads) return CTKV_ESHAPE;
+  const int gs = L->query_heads / L->kv_heads;
+  if (gs > 16) return CTKV_ESHAPE;
+  if (!dim_ok(L->head_dim)) return CTKV_ESHAPE;
+  if (L->dtype != CTKV_F32 && L->dtype != CTKV_BF16) return CTKV_ESHAPE;
+  if (L->capacity < 0 || L->init_len < 0 || L->local_len < 0) return CTKV_ECONFIG;
+  return CTKV_OK;
+}
+
+int static_slots(const ctkv_layout* L) {
+  const int64_t n = (int64_t)L->init_len + L->local_len;
+  return (int)((n + kStaticSplitHost - 1) / kStaticSplitHost);
+}
+
+struct DecodeWs {
+  double* gcos;
+  double* pm;
+  double* pl;
+  float* po;
+  double* logits;
+  size_t bytes;
+};
+
+DecodeWs carve_decode(const ctkv_layout* L, int C, int lmax, int ns, void* base) {
+  const int U = L->batch * L->kv_heads;
+  const int gs = L->query_heads / L->kv_heads;
+  const int d = L->head_dim;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* p = base ? static_cast<char*>(base) + off : nullptr;
+    off += a256(b);
+    return p;
+  };
+  DecodeWs w;
+  w.gcos = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * std::max(C, 1)));
+  w.pm = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * std::max(ns, 1) * gs));
+  w.pl = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * std::max(ns, 1) * gs));
+  w.po = reinterpret_cast<float*>(take(sizeof(float) * (size_t)U * std::max(ns, 1) * gs * d));
+  w.logits = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * gs * std::max(lmax, 1)));
+  w.bytes = off;
+  return w;
+}
+
+void fill_layout(DecodeParams& p, const ctkv_layout* L) {
+  std::memset(&p, 0, sizeof(p));
+  p.b = L->batch;
+  p.h = L->query_heads;
+  p.g = L->kv_heads;
+  p.gs = p.h / p.g;
+  p.U = p.b * p.g;
+  p.cap = L->capacity;
+  p.init_len = L->init_len;
+  p.local_len = L->local_len;
+  p.bitmap_words = (int)((L->capacity + 31) / 32);
+}
+
+
+}  // namespace
+
+extern "C" {
+
+int ctkv_abi_version(void) { return CTKV_ABI_VERSION; }
+
+const char* ctkv_status_string(int s) {
+  switch (s) {
+    case CTKV_OK: return "ok";
+    case CTKV_ESHAPE: return "shape error (unsupported or inconsistent dimensions)";
+    case CTKV_ECONFIG: return "config error (precondition violated or device limit exceeded)";
+    case CTKV_EINDEX: return "token id out of range";
+    case CTKV_ECUDA: return "CUDA error";
+    case CTKV_EWORKSPACE: return "workspace too small";
+  }
+  return "unknown status";
+}
+
+int ctkv_device_ok(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return 0;
+  return prop.major == 10 && prop.minor == 0 ? 1 : 0;
+}
+
+int ctkv_append(const ctkv_layout* L, ctkv_store S, const void* k_new, const void* v_new,
+                void* stream) {
+  if (int rc = check_layout(L)) return rc;
+  if (!S.keys || !S.values || !S.total || !k_new || !v_new) return CTKV_ECONFIG;
+  return launch_append(L->dtype, S.keys, S.values, k_new, v_new, S.total,
+                       (int64_t)L->batch * L->kv_heads, L->capacity, L->head_dim,
+                       static_cast<cudaStream_t>(stream));
+}
+
+size_t ctkv_build_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32_t rho,
+                                  int64_t n_off, int32_t mode) {
+  if (check_layout(L)) return 0;
+  BuildParams p{};
+  p.b = L->batch;
+  p.h = L->query_heads;
+  p.g = L->kv_heads;
+  p.gs = p.h / p.g;
+  p.d = L->head_dim;
+  p.C = capacity;
+  p.rho = rho;
+  p.n_off = n_off;
+  p.mode = mode;
+  return build_workspace_bytes(p);
+}
+
+int ctkv_build_lists(const ctkv_layout* L, const void* centroids, const void* keys,
+                     int64_t off_begin, int64_t n_off, int32_t capacity, int32_t rho,
+                     int32_t mode, int32_t* lists, int32_t* flags, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  if (int rc = check_layout(L)) return rc;
+  if (capacity < 1 || rho < 0 || rho > n_off || n_off < 0 || off_begin < 0 ||
+      off_begin + n_off > L->capacity)
+    return CTKV_ECONFIG;
+  if (rho > 8192) return CTKV_ECONFIG;
+  const int gs = L->query_heads / L->kv_heads;
+  if (gs != 1 && gs != 2 && gs != 4 && gs != 8) return CTKV_ESHAPE;
+  BuildParams p{};
+  p.b = L->batch;
+  p.h = L->query_heads;
+  p.g = L->kv_heads;
+  p.gs = gs;
+  p.d = L->head_dim;
+  p.cap = L->capacity;
+  p.cent = centroids;
+  p.keys = keys;
+  p.off_begin = off_begin;
+  p.n_off = n_off;
+  p.C = capacity;
+  p.rho = rho;
+  p.lists = lists;
+  p.flags = flags;
+  p.mode = mode;
+  return launch_build(p, L->dtype, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t ctkv_decode_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32_t rho,
+                                   int32_t c_prime, int32_t) {
+  if (check_layout(L)) return 0;
+  return carve_decode(L, capacity, c_prime * rho, static_slots(L), nullptr).bytes;
+}
+
+int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctkv_step_args* A,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_layout(L)) return rc;
+  if (!A || !A->query || !A->out || !S.keys || !S.values || !S.total) return CTKV_ECONFIG;
+  if (I.capacity < 1) return CTKV_ECONFIG;                            // "recall: empty index"
+  if (A->c_prime < 1 || A->c_prime > I.capacity) return CTKV_ECONFIG;  // ck/retrieval.py:138
+  if (A->rho_prime < 1) return CTKV_ECONFIG;
+  if (I.rho < 0 || I.rho > 8 * 512) return CTKV_ECONFIG;
+  if ((A->k_new == nullptr) != (A->v_new == nullptr)) return CTKV_ECONFIG;
+  if (A->use_dcu && (!I.fifo_head || !I.sync)) return CTKV_ECONFIG;
+  if (A->k_new && !I.sync) return CTKV_ECONFIG;
+  const int ns = static_slots(L);
+  const int lmax = A->c_prime * I.rho;
+  DecodeWs w = carve_decode(L, I.capacity, lmax, ns, workspace);
+  if (w.bytes > workspace_bytes) return CTKV_EWORKSPACE;
+  DecodeParams p;
+  fill_layout(p, L);
+  p.keys = S.keys;
+  p.values = S.values;
+  p.total = S.total;
+  p.k_new = A->k_new;
+  p.v_new = A->v_new;
+  p.cent = I.centroids;
+  p.lists = I.lists;
+  p.fifo = I.fifo_head;
+  p.sync = I.sync;
+  p.C = I.capacity;
+  p.rho = I.rho;
+  p.q = A->query;
+  p.c_prime = A->c_prime;
+  p.rho_prime = A->rho_prime;
+  p.use_rerank = A->use_rerank;
+  p.stages = kStageSelect | kStageUnion | kStageScores | kStageSort | kStageAttend |
+             (A->use_dcu ? kStageDcu : 0) | (A->k_new ? kStageAppendTail : 0);
+  p.do_cos = 1;
+  p.cos_blocks_per_unit = (I.capacity + kCosChunkHost - 1) / kCosChunkHost;
+  p.ns = ns;
+  p.lmax = lmax;
+  p.gcos = w.gcos;
+  p.pm = w.pm;
+  p.pl = w.pl;
+  p.po = w.po;
+  p.logits = w.logits;
+  p.out = A->out;
+  p.row_max = A->row_max;
+  p.denom = A->denom;
+  p.selected = A->selected;
+  p.recall_len = A->recall_len;
+  p.sparse_ids = A->sparse_ids;
+  p.sparse_len = A->sparse_len;
+  p.sparse_cap = A->sparse_ids ? A->sparse_cap : 0;
+  p.flags = A->flags;
+  if (unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
+  if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;
+  return launch_unit(p, L->dtype, L->head_dim, st);
+}
+
+int ctkv_recall(const ctkv_layout* L, ctkv_index I, int64_t id_bound, const void* query,
+                int32_t c_prime, int32_t* selected, int32_t* recalled, int32_t* recall_len,
+                int32_t* flags, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_layout(L)) return rc;
+  if (I.capacity < 1) return CTKV_ECONFIG;
+  if (c_prime < 1 || c_prime > I.capacity) return CTKV_ECONFIG;
+  if (I.rho < 0 || I.rho > 8 * 512) return CTKV_ECONFIG;
+  const int lmax = c_prime * I.rho;
+  DecodeWs w = carve_decode(L, I.capacity, lmax, 0, workspace);
+  if (w.bytes > workspace_bytes) return CTKV_EWORKSPACE;
+  if (id_bound < 0) return CTKV_ECONFIG;
+  DecodeParams p;
+  fill_layout(p, L);
+  p.total = nullptr;
+  p.id_bound = id_bound;
+  p.bitmap_words = (int)((id_bound + 31) / 32);
+  p.cent = I.centroids;
+  p.lists = I.lists;
+  p.C = I.capacity;
+  p.rho = I.rho;
+  p.q = query;
+  p.c_prime = c_prime;
+  p.stages = kStageSelect | kStageUnion;
+  p.do_cos = 1;
+  p.cos_blocks_per_unit = (I.capacity + kCosChunkHost - 1) / kCosChunkHost;
+  p.ns = 0;
+  p.lmax = lmax;
+  p.gcos = w.gcos;
+  p.logits = w.logits;
+  p.selected = selected;
+  p.rec_out = recalled;
+  p.recall_len = recall_len;
+  p.flags = flags;
+  if (unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = launch_scan(p, L->dtype, L->head_dim, p.U * p.cos_blocks_per_unit, st)) return rc;
+  return launch_unit(p, L->dtype, L->head_dim, st);
+}
+
+int ctkv_rerank(const ctkv_layout* L, ctkv_store S, const void* query, const int32_t* recalled,
+                const int32_t* recall_len, int32_t lmax, double* grouped, int32_t* order,
+                int32_t* flags, void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_layout(L)) return rc;
+  if (lmax < 0 || !recalled || !recall_len) return CTKV_ECONFIG;
+  DecodeWs w = carve_decode(L, 0, lmax, 0, workspace);
+  if (w.bytes > workspace_bytes) return CTKV_EWORKSPACE;
+  DecodeParams p;
+  fill_layout(p, L);
+  p.keys = S.keys;
+  p.values = S.values;
+  p.total = S.total;
+  p.q = query;
+  p.C = 1;
+  p.stages = kStageScores | kStageSort;
+  p.lmax = lmax;
+  p.rec_in = recalled;
+  p.len_in = recall_len;
+  p.logits = w.logits;
+  p.grouped_out = grouped;
+  p.order_out = order;
+  p.flags = flags;
+  p.c_prime = 1;
+  if (unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
+  return launch_unit(p, L->dtype, L->head_dim, static_cast<cudaStream_t>(stream));
+}
+
+int ctkv_fifo_update(const ctkv_layout* L, ctkv_index I, const void* query,
+                     const int32_t* recalled, const int32_t* recall_len, int32_t lmax,
+                     const double* grouped, void* workspace, size_t workspace_bytes,
+                     void* stream) {
+  if (int rc = check_layout(L)) return rc;
+  if (I.capacity < 1 || !I.fifo_head || !I.sync || !recalled || !recall_len || !grouped)
+    return CTKV_ECONFIG;
+  DecodeWs w = carve_decode(L, 0, lmax, 0, workspace);
+  if (w.bytes > workspace_bytes) return CTKV_EWORKSPACE;
+  DecodeParams p;
+  fill_layout(p, L);
+  p.cent = I.centroids;
+  p.lists = I.lists;
+  p.fifo = I.fifo_head;
+  p.sync = I.sync;
+  p.C = I.capacity;
+  p.rho = I.rho;
+  p.q = query;
+  p.c_prime = 1;
+  p.dcu_force = 1;
+  p.stages = kStageSort | kStageDcu;
+  p.lmax = lmax;
+  p.rec_in = recalled;
+  p.len_in = recall_len;
+  p.grouped_in = grouped;
+  p.logits = w.logits;
+  p.total = nullptr;  // the DCU-only pass never reads the store
+  if (unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
+  return launch_unit(p, L->dtype, L->head_dim, static_cast<cudaStream_t>(stream));
+}
+
+size_t ctkv_attend_workspace_bytes(const ctkv_layout* L, int32_t lmax, int32_t with_static) {
+  if (check_layout(L)) return 0;
+  const int ns = (lmax + kAttnSplitHost - 1) / kAttnSplitHost + (with_static ? static_slots(L) : 0);
+  return carve_decode(L, 0, 0, ns, nullptr).bytes;
+}
+
+int ctkv_attend(const ctkv_layout* L, ctkv_store S, const void* query, const int32_t* ids,
+                const int32_t* ids_len, int32_t lmax, int32_t ids_shared, int32_t with_static,
+                float* out, double* row_max, double* denom, int32_t* flags, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  if (int rc = check_layout(L)) return rc;
+  if (!out || lmax < 0 || (lmax > 0 && (!ids || !ids_len))) return CTKV_ECONFIG;
+  const int list_splits = lmax > 0 ? (lmax + kAttnSplitHost - 1) / kAttnSplitHost : 0;
+  const int ns = list_splits + (with_static ? static_slots(L) : 0);
+  if (ns == 0) return CTKV_ECONFIG;
+  DecodeWs w = carve_decode(L, 0, 0, ns, workspace);
+  if (w.bytes > workspace_bytes) return CTKV_EWORKSPACE;
+  DecodeParams p;
+  fill_layout(p, L);
+  p.keys = S.keys;
+  p.values = S.values;
+  p.total = S.total;
+  p.q = query;
+  p.ns = ns;
+  p.list_splits = list_splits;
+  p.ids_shared = ids_shared;
+  p.lmax = lmax;
+  p.rec_in = ids;
+  p.len_in = ids_len;
+  p.pm = w.pm;
+  p.pl = w.pl;
+  p.po = w.po;
+  p.out = out;
+  p.row_max = row_max;
+  p.denom = denom;
+  p.flags = flags;
+  return launch_attn(p, L->dtype, L->head_dim, static_cast<cudaStream_t>(stream));
+}
+
+int ctkv_merge(int64_t rows, int32_t head_dim, const float* out_a, const double* max_a,
+               const double* den_a, const float* out_b, const double* max_b,
+               const double* den_b, float* out, double* row_max, double* denom, void* stream) {
+  if (rows < 0 || head_dim < 1) return CTKV_ESHAPE;
+  return launch_merge2(rows, head_dim, out_a, max_a, den_a, out_b, max_b, den_b, out, row_max,
+                       denom, static_cast<cudaStream_t>(stream));
+}
+
+int ctkv_scores(const ctkv_layout* L, const void* q, int64_t m, const void* k, int64_t n,
+                int64_t k_row_stride, int32_t grouped, float* out, void* stream) {
+  if (int rc = check_layout(L)) return rc;
+  const int gs = L->query_heads / L->kv_heads;
+  if (gs != 1 && gs != 2 && gs != 4 && gs != 8) return CTKV_ESHAPE;
+  if (m < 0 || n < 0) return CTKV_ESHAPE;
+  if (m == 0 || n == 0) return CTKV_OK;
+  return launch_scores(L->dtype, L->batch, L->query_heads, L->kv_heads, L->head_dim, q, m, k, n,
+                       k_row_stride, grouped, out, static_cast<cudaStream_t>(stream));
+}
+
+size_t ctkv_topk_workspace_bytes(int64_t rows, int64_t n, int32_t k) {
+  return topk_workspace_bytes(rows, n, k);
+}
+
+int ctkv_topk_rows(const float* values, int64_t rows, int64_t n, int32_t k, int32_t* idx,
+                   void* workspace, size_t workspace_bytes, void* stream) {
+  if (rows < 0 || n < 0 || k < 0) return CTKV_ESHAPE;
+  if (k > n) k = (int32_t)n;
+  if (k > 8192) return CTKV_ECONFIG;
+  return launch_topk_rows(values, rows, n, k, idx, workspace, workspace_bytes,
+                          static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

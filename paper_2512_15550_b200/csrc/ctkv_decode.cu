@@ -1,0 +1,920 @@
+// Decode-step kernels for the B200 CTkvr path (sm_100a).
+//
+// One decode step per layer is two kernels (plus nothing else: the KV
+// append is folded into the first one):
+//
+//   scan_kernel   -- every SM streams HBM: (a) per (b,g) unit, the cosine of
+//                    the gs query heads against all C centroids with the GQA
+//                    group max (Alg. 2 L1-2; ck/retrieval.py:144-145,
+//                    ck/tensor_ops.py:190-207); (b) split-K attention partials
+//                    over the static partition [0,L_init) U [ring_start,total)
+//                    (ck/retrieval.py:341-344).  Block 0 also appends the new
+//                    token's K/V (ck/store.py:114-129).
+//   unit_kernel   -- one CTA per (b,g) unit: top-C' slots (ties -> smaller
+//                    slot), first-occurrence union of their lists through a
+//                    shared-memory bitmap (ck/retrieval.py:151-162), gathered
+//                    f64 q.k rerank with group max (ck/retrieval.py:171-218),
+//                    (score desc, position asc) ordering, the FIFO DCU write
+//                    (ck/index.py:103-133), sparse attention reusing the
+//                    rerank logits (ck/retrieval.py:221-246), and the exact
+//                    merge with the static partials (ck/retrieval.py:275-284).
+//
+// The same unit_kernel, with stage bits switched off, backs the staged API
+// calls (recall / rerank / fifo_update) so every stage is parity-testable
+// on its own.  Generic id-list attention (sparse_attention API,
+// _partial_over_ids) is attn_split_kernel + attn_merge_kernel.
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+
+#include "ctkv.h"
+#include "ctkv_common.cuh"
+#include "ctkv_internal.h"
+
+namespace ctkv {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanWarps = kScanThreads / 32;
+constexpr int kCosChunk = 64;       // centroids per scan CTA (all gs heads)
+constexpr int kStaticSplit = 64;    // static tokens per scan CTA
+constexpr int kUnitThreads = 512;
+constexpr int kUnitWarps = kUnitThreads / 32;
+constexpr int kAttnChunk = 512;     // sparse tokens per weight chunk
+constexpr int kAttnSplit = 64;      // tokens per attn_split_kernel CTA
+
+template <typename T>
+__device__ __forceinline__ const T* kv_row(const T* base, const T* fresh, int64_t cap, int unit,
+                                           int64_t id, int64_t t_new, int D) {
+  // the token appended by this very step is read from the caller's buffer
+  // (the store copy is written concurrently by scan block 0)
+  if (fresh != nullptr && id == t_new) return fresh + (int64_t)unit * D;
+  return base + ((int64_t)unit * cap + id) * D;
+}
+
+// this lane's partial of q_hh . row in f64 (products of f32-representable
+// values are exact in f64; only the summation order differs from numpy)
+template <typename T, int D>
+__device__ __forceinline__ double lane_dot(const float* qs, int hh, const float* kv, int sub) {
+  using R = Row<T, D>;
+  double a = 0.0;
+#pragma unroll
+  for (int v = 0; v < R::VPL; ++v) {
+    const float4* qv = reinterpret_cast<const float4*>(qs + hh * D + R::elem(sub, v));
+#pragma unroll
+    for (int j = 0; j < R::EPV / 4; ++j) {
+      const float4 q4 = qv[j];
+      const float* x = kv + v * R::EPV + 4 * j;
+      a = fma((double)q4.x, (double)x[0], a);
+      a = fma((double)q4.y, (double)x[1], a);
+      a = fma((double)q4.z, (double)x[2], a);
+      a = fma((double)q4.w, (double)x[3], a);
+    }
+  }
+  return a;
+}
+
+// Per-warp weighted row sums: red_warp[hh][:] += sum_t w(hh,t) * row(t)[:]
+// for t in [0,n) strided over the block's warps.  Heads are processed four
+// at a time so the accumulators stay in registers for any group size.
+template <typename T, int D, typename RowFn, typename WFn>
+__device__ void accum_weighted_rows(int n, int gs, RowFn rowfn, WFn wfn, float* red_warp) {
+  using R = Row<T, D>;
+  const int nwarps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane % R::LPR, rw = lane / R::LPR;
+  for (int h0 = 0; h0 < gs; h0 += 4) {
+    float acc[4][R::EPL];
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh)
+#pragma unroll
+      for (int j = 0; j < R::EPL; ++j) acc[hh][j] = 0.f;
+    for (int base = warp * R::RPW; base < n; base += nwarps * R::RPW) {
+      const int t = base + rw;
+      if (t < n) {
+        const T* row = rowfn(t);
+        if (row != nullptr) {
+          float vv[R::EPL];
+          load_row_slice<T, D>(row, sub, vv);
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh) {
+            if (h0 + hh < gs) {
+              const float w = wfn(h0 + hh, t);
+#pragma unroll
+              for (int j = 0; j < R::EPL; ++j) acc[hh][j] = fmaf(w, vv[j], acc[hh][j]);
+            }
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int hh = 0; hh < 4; ++hh)
+#pragma unroll
+      for (int j = 0; j < R::EPL; ++j) {
+        float x = acc[hh][j];
+#pragma unroll
+        for (int o = R::LPR; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        acc[hh][j] = x;
+      }
+    if (rw == 0) {
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh)
+        if (h0 + hh < gs)
+#pragma unroll
+          for (int v = 0; v < R::VPL; ++v)
+#pragma unroll
+            for (int j = 0; j < R::EPV; ++j)
+              red_warp[(h0 + hh) * D + R::elem(sub, v) + j] += acc[hh][v * R::EPV + j];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
+// scan kernel: cosine chunks + static attention splits (+ append)
+// ------------------------------------------------------------------------
+
+template <typename T, int D>
+__device__ void cos_block(const DecodeParams& p, int bid, unsigned char* smem) {
+  using R = Row<T, D>;
+  const int cpu = p.cos_blocks_per_unit;
+  const int u = bid / cpu, chunk = bid % cpu;
+  const int bi = u / p.g, gi = u % p.g, gs = p.gs;
+  const int c0 = chunk * kCosChunk;
+  const int nc = min(kCosChunk, p.C - c0);
+  float* qs = reinterpret_cast<float*>(smem);                    // [gs][D]
+  double* qn = reinterpret_cast<double*>(qs + kMaxGroup * D);    // [gs]
+  double* cosv = qn + kMaxGroup;                                 // [gs][kCosChunk]
+  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
+  for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = to_f(q[i]);
+  __syncthreads();
+  if (threadIdx.x < gs) {
+    double s = 0.0;
+    for (int e = 0; e < D; ++e) s = fma((double)qs[threadIdx.x * D + e], (double)qs[threadIdx.x * D + e], s);
+    qn[threadIdx.x] = sqrt(s);
+  }
+  __syncthreads();
+  const T* cent = static_cast<const T*>(p.cent);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane % R::LPR, rw = lane / R::LPR;
+  const int nrows = gs * nc;
+  constexpr int U = 4;
+  for (int base = warp * R::RPW; base < nrows; base += kScanWarps * R::RPW * U) {
+    float kv[U][R::EPL];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int r = base + k * kScanWarps * R::RPW + rw;
+      if (r < nrows) {
+        const int hh = r / nc, c = c0 + r % nc;
+        const T* row = cent + (((int64_t)bi * p.h + gi * gs + hh) * p.C + c) * D;
+        load_row_slice<T, D, true>(row, sub, kv[k]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < R::EPL; ++j) kv[k][j] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int r = base + k * kScanWarps * R::RPW + rw;
+      const int hh = r < nrows ? r / nc : 0;
+      double dot = 0.0, nrm = 0.0;
+#pragma unroll
+      for (int v = 0; v < R::VPL; ++v) {
+        const float* qv = qs + hh * D + R::elem(sub, v);
+#pragma unroll
+        for (int j = 0; j < R::EPV; ++j) {
+          const double x = (double)kv[k][v * R::EPV + j];
+          dot = fma((double)qv[j], x, dot);
+          nrm = fma(x, x, nrm);
+        }
+      }
+      dot = row_sum<R::LPR>(dot);
+      nrm = row_sum<R::LPR>(nrm);
+      if (sub == 0 && r < nrows) {
+        const double den = qn[hh] * sqrt(nrm);
+        double c;
+        if (den == 0.0) {
+          c = 0.0;
+          set_flag(p.flags, kFlagDegenerate);
+        } else {
+          c = fmin(fmax(dot / den, -1.0), 1.0);
+        }
+        cosv[hh * kCosChunk + (r % nc)] = c;
+      }
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    double m = cosv[c];
+    for (int hh = 1; hh < gs; ++hh) m = fmax(m, cosv[hh * kCosChunk + c]);
+    p.gcos[(int64_t)u * p.C + c0 + c] = m;
+  }
+}
+
+struct StaticSpan {
+  int64_t n_init, ring_start, n_static;
+  __device__ StaticSpan(int64_t total, int init_len, int local_len) {
+    n_init = min((int64_t)init_len, total);
+    ring_start = max((int64_t)init_len, total - local_len);
+    n_static = n_init + (total - ring_start);
+  }
+  __device__ int64_t id(int64_t i) const { return i < n_init ? i : ring_start + (i - n_init); }
+};
+
+// softmax partial (m, l, unnormalised o) of the gs heads over up to
+// kAttnSplit tokens whose ids come from `idf(i)`; written to slot `part`.
+template <typename T, int D, typename IdFn>
+__device__ void attn_partial_block(const DecodeParams& p, int u, int ntok, IdFn idf,
+                                   int64_t t_new, int64_t total, double* pm, double* pl, float* po,
+                                   unsigned char* smem) {
+  using R = Row<T, D>;
+  const int bi = u / p.g, gi = u % p.g, gs = p.gs;
+  const int nwarps = blockDim.x >> 5;
+  float* qs = reinterpret_cast<float*>(smem);                          // [gs][D]
+  double* lg = reinterpret_cast<double*>(qs + kMaxGroup * D);          // [gs][kAttnSplit]
+  double* mh = lg + kMaxGroup * kAttnSplit;                            // [gs]
+  double* lh = mh + kMaxGroup;                                         // [gs]
+  float* red = reinterpret_cast<float*>(lh + kMaxGroup);               // [nwarps][gs][D]
+  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
+  for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = to_f(q[i]);
+  __syncthreads();
+  const T* keys = static_cast<const T*>(p.keys);
+  const T* vals = static_cast<const T*>(p.values);
+  const T* knew = static_cast<const T*>(p.k_new);
+  const T* vnew = static_cast<const T*>(p.v_new);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int sub = lane % R::LPR, rw = lane / R::LPR;
+  const double scale = 1.0 / sqrt((double)D);
+  // phase 1: logits (f64)
+  for (int base = warp * R::RPW; base < ntok; base += nwarps * R::RPW) {
+    const int t = base + rw;
+    float kv[R::EPL];
+    bool ok = t < ntok;
+    const int64_t id = ok ? idf(t) : 0;
+    if (ok && (id < 0 || id >= total)) {
+      set_flag(p.flags, kFlagIdRange);
+      ok = false;
+    }
+    if (ok) {
+      load_row_slice<T, D>(kv_row(keys, knew, p.cap, u, id, t_new, D), sub, kv);
+    } else {
+#pragma unroll
+      for (int j = 0; j < R::EPL; ++j) kv[j] = 0.f;
+    }
+    for (int hh = 0; hh < gs; ++hh) {
+      const double a = row_sum<R::LPR>(lane_dot<T, D>(qs, hh, kv, sub));
+      if (sub == 0 && t < ntok) lg[hh * kAttnSplit + t] = ok ? a * scale : -INFINITY;
+    }
+  }
+  for (int i = threadIdx.x; i < nwarps * gs * D; i += blockDim.x) red[i] = 0.f;
+  __syncthreads();
+  // per-head max and exp weights (f64)
+  if (threadIdx.x < gs) {
+    const int hh = threadIdx.x;
+    double m = -INFINITY;
+    for (int t = 0; t < ntok; ++t) m = fmax(m, lg[hh * kAttnSplit + t]);
+    double l = 0.0;
+    for (int t = 0; t < ntok; ++t) {
+      const double e = (m == -INFINITY) ? 0.0 : exp(lg[hh * kAttnSplit + t] - m);
+      lg[hh * kAttnSplit + t] = e;
+      l += e;
+    }
+    mh[hh] = m;
+    lh[hh] = l;
+  }
+  __syncthreads();
+  // phase 2: o[h] = sum_t w[h,t] * V[t]  (unnormalised)
+  accum_weighted_rows<T, D>(
+      ntok, gs,
+      [&](int t) -> const T* {
+        const int64_t id = idf(t);
+        if (id < 0 || id >= total) return nullptr;
+        return kv_row(vals, vnew, p.cap, u, id, t_new, D);
+      },
+      [&](int hh, int t) { return (float)lg[hh * kAttnSplit + t]; }, red + (int64_t)warp * gs * D);
+  __syncthreads();
+  for (int i = threadIdx.x; i < gs * D; i += blockDim.x) {
+    float s = 0.f;
+    for (int w = 0; w < nwarps; ++w) s += red[(int64_t)w * gs * D + i];
+    po[i] = s;
+  }
+  if (threadIdx.x < gs) {
+    pm[threadIdx.x] = mh[threadIdx.x];
+    pl[threadIdx.x] = lh[threadIdx.x];
+  }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kScanThreads) scan_kernel(DecodeParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t t0 = p.total ? *p.total : p.id_bound;
+  const bool appending = p.k_new != nullptr;
+  const int64_t total = t0 + (appending ? 1 : 0);
+  const int ncos = p.do_cos ? p.U * p.cos_blocks_per_unit : 0;
+  if ((int)blockIdx.x < ncos) {
+    cos_block<T, D>(p, blockIdx.x, smem);
+  } else {
+    const int sb = blockIdx.x - ncos;
+    const int u = sb / p.ns, split = sb % p.ns;
+    const StaticSpan span(total, p.init_len, p.local_len);
+    const int64_t i0 = (int64_t)split * kStaticSplit;
+    const int ntok = (int)max((int64_t)0, min((int64_t)kStaticSplit, span.n_static - i0));
+    const int64_t slot = (int64_t)u * p.ns + split;
+    attn_partial_block<T, D>(
+        p, u, ntok, [&](int t) { return span.id(i0 + t); }, appending ? t0 : -1, total,
+        p.pm + slot * p.gs, p.pl + slot * p.gs, p.po + slot * p.gs * D, smem);
+  }
+  if (appending && blockIdx.x == 0) {
+    // KvStore.append: new rows land at index t0 (ck/store.py:125-128)
+    T* keys = static_cast<T*>(const_cast<void*>(p.keys));
+    T* vals = static_cast<T*>(const_cast<void*>(p.values));
+    const T* kn = static_cast<const T*>(p.k_new);
+    const T* vn = static_cast<const T*>(p.v_new);
+    for (int64_t i = threadIdx.x; i < (int64_t)p.U * D; i += blockDim.x) {
+      const int64_t u = i / D, e = i % D;
+      keys[(u * p.cap + t0) * D + e] = kn[i];
+      vals[(u * p.cap + t0) * D + e] = vn[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
+// unit kernel: select -> union -> rerank -> order -> DCU -> sparse attend
+// ------------------------------------------------------------------------
+
+struct UnitSmem {
+  int32_t* sel;      // [c_prime]
+  uint32_t* bitmap;  // [nwords]
+  int32_t* rec;      // [lmax]
+  uint64_t* skey;    // [npad_max]  (reused as the attention reduce area)
+  int32_t* sval;     // [npad_max]
+  float* wts;        // [gs][kAttnChunk]
+  double* scratch;   // [64] reductions
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline size_t unit_smem_layout(const DecodeParams& p, int D, UnitSmem* s,
+                                                   unsigned char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    unsigned char* ptr = base ? base + off : nullptr;
+    off += align16(bytes);
+    return ptr;
+  };
+  const int npad = next_pow2(max(p.lmax, 1));
+  const size_t red_bytes = (size_t)kUnitWarps * p.gs * D * sizeof(float);
+  const size_t key_bytes =
+      (size_t)npad * sizeof(uint64_t) > red_bytes ? (size_t)npad * sizeof(uint64_t) : red_bytes;
+  UnitSmem t;
+  t.sel = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * max(p.c_prime, 1)));
+  t.bitmap = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * p.bitmap_words));
+  t.rec = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * max(p.lmax, 1)));
+  t.skey = reinterpret_cast<uint64_t*>(take(key_bytes));
+  t.sval = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * npad));
+  t.wts = reinterpret_cast<float*>(take(sizeof(float) * p.gs * kAttnChunk));
+  t.scratch = reinterpret_cast<double*>(take(sizeof(double) * 128));
+  if (s) *s = t;
+  return off;
+}
+
+size_t unit_smem_bytes(const DecodeParams& p, int D) {
+  return unit_smem_layout(p, D, nullptr, nullptr);
+}
+
+// block-wide arg-max over (key desc, idx asc) pairs; returns the winner idx
+__device__ int block_argmax(uint64_t key, int idx, double* scratch) {
+  auto better = [](uint64_t ka, int ia, uint64_t kb, int ib) {
+    return ka > kb || (ka == kb && ia < ib);
+  };
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t k2 = __shfl_xor_sync(0xffffffffu, key, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (better(k2, i2, key, idx)) { key = k2; idx = i2; }
+  }
+  uint64_t* sk = reinterpret_cast<uint64_t*>(scratch);  // [33]
+  int* si = reinterpret_cast<int*>(sk + 34);            // [33]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) { sk[warp] = key; si[warp] = idx; }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  if (warp == 0) {
+    key = lane < nw ? sk[lane] : 0;
+    idx = lane < nw ? si[lane] : INT32_MAX;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, key, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (better(k2, i2, key, idx)) { key = k2; idx = i2; }
+    }
+    if (lane == 0) { sk[32] = key; si[32] = idx; }
+  }
+  __syncthreads();
+  return si[32];
+}
+
+__device__ int block_exclusive_scan(int x, int* total, double* scratch) {
+  int* ws = reinterpret_cast<int*>(scratch);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int incl = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  if (warp == 0) {
+    int v = lane < nw ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane < nw) ws[lane] = v;  // inclusive prefix of warp totals
+  }
+  __syncthreads();
+  const int warp_prefix = warp ? ws[warp - 1] : 0;
+  *total = ws[nw - 1];
+  return warp_prefix + incl - x;
+}
+
+__device__ double block_max_f64(double x, double* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = x;
+  __syncthreads();
+  double m = -INFINITY;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, scratch[w]);
+  return m;
+}
+
+__device__ double block_sum_f64(double x, double* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) scratch[warp] = x;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += scratch[w];
+  return s;
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kUnitThreads, 1) unit_kernel(DecodeParams p) {
+  using R = Row<T, D>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  UnitSmem S;
+  unit_smem_layout(p, D, &S, smem);
+  const int u = blockIdx.x;
+  const int bi = u / p.g, gi = u % p.g, gs = p.gs;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t t0 = p.total ? *p.total : p.id_bound;
+  const bool appending = p.k_new != nullptr;
+  const int64_t total = t0 + (appending ? 1 : 0);
+  __shared__ int64_t s_slot;
+  __shared__ float qs[kMaxGroup * D];
+  if (tid == 0) s_slot = p.fifo ? (p.fifo[bi] % p.C) : 0;
+  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
+  for (int i = tid; i < gs * D; i += blockDim.x) qs[i] = to_f(q[i]);
+
+  // ---- 1. top-C' centroid slots (ck/retrieval.py:154) -------------------
+  int L = 0;
+  if (p.stages & kStageSelect) {
+    uint64_t prev_key = ~0ull;
+    int prev_idx = -1;
+    const double* gc = p.gcos + (int64_t)u * p.C;
+    for (int r = 0; r < p.c_prime; ++r) {
+      uint64_t bk = 0;
+      int bidx = INT32_MAX;
+      for (int i = tid; i < p.C; i += blockDim.x) {
+        const uint64_t k = okey64(gc[i]);
+        const bool below = k < prev_key || (k == prev_key && i > prev_idx);
+        if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
+      }
+      const int w = block_argmax(bk, bidx, S.scratch);
+      if (tid == 0) S.sel[r] = w;
+      prev_idx = w;
+      prev_key = okey64(gc[w]);
+    }
+    __syncthreads();
+    if (p.selected)
+      for (int r = tid; r < p.c_prime; r += blockDim.x)
+        p.selected[(int64_t)u * p.c_prime + r] = S.sel[r];
+  }
+
+  // ---- 2. union of the selected lists, first occurrence kept ------------
+  if (p.stages & kStageUnion) {
+    const int nwords = (int)((total + 31) >> 5);
+    for (int i = tid; i < nwords; i += blockDim.x) S.bitmap[i] = 0u;
+    __syncthreads();
+    const int per = (p.rho + blockDim.x - 1) / blockDim.x;
+    for (int j = 0; j < p.c_prime; ++j) {
+      const int32_t* row = p.lists + ((int64_t)u * p.C + S.sel[j]) * p.rho;
+      int keep_mask = 0, cnt = 0;
+      int ids[8];
+      // `per` <= 8 is guaranteed by the host (rho <= 8 * kUnitThreads)
+      for (int e = 0; e < per; ++e) {
+        const int i = tid * per + e;
+        int id = (i < p.rho) ? row[i] : kEmpty;
+        if (id != kEmpty && (id < 0 || id >= total)) {
+          set_flag(p.flags, kFlagIdRange);
+          id = kEmpty;
+        }
+        ids[e] = id;
+        if (id != kEmpty && !((S.bitmap[id >> 5] >> (id & 31)) & 1u)) {
+          keep_mask |= 1 << e;
+          ++cnt;
+        }
+      }
+      int tot_kept;
+      int pos = L + block_exclusive_scan(cnt, &tot_kept, S.scratch);
+      for (int e = 0; e < per; ++e)
+        if (keep_mask & (1 << e)) S.rec[pos++] = ids[e];
+      __syncthreads();  // every test of list j precedes any set of list j
+      for (int e = 0; e < per; ++e)
+        if (keep_mask & (1 << e)) atomicOr(&S.bitmap[ids[e] >> 5], 1u << (ids[e] & 31));
+      L += tot_kept;
+      __syncthreads();
+    }
+    if (p.rec_out)
+      for (int i = tid; i < p.lmax; i += blockDim.x)
+        p.rec_out[(int64_t)u * p.lmax + i] = i < L ? S.rec[i] : kEmpty;
+  } else {
+    L = p.len_in[u];
+    for (int i = tid; i < L; i += blockDim.x) S.rec[i] = p.rec_in[(int64_t)u * p.lmax + i];
+  }
+  if (p.recall_len && tid == 0) p.recall_len[u] = L;
+  if (tid == 0) set_flag(p.flags, L > 0 ? kFlagNonEmptyRecall : kFlagEmptyRecall);
+  __syncthreads();
+
+  // ---- 3. rerank logits (f64) + group max -------------------------------
+  const int npad = next_pow2(max(L, 1));
+  double* lg = p.logits + (int64_t)u * gs * p.lmax;
+  const double scale = 1.0 / sqrt((double)D);
+  if (L > 0 && (p.stages & kStageScores)) {
+    const T* keys = static_cast<const T*>(p.keys);
+    const int sub = lane % R::LPR, rw = lane / R::LPR;
+    constexpr int U = 4;
+    for (int base = warp * R::RPW; base < L; base += kUnitWarps * R::RPW * U) {
+      float kv[U][R::EPL];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int t = base + k * kUnitWarps * R::RPW + rw;
+        if (t < L) {
+          load_row_slice<T, D>(keys + ((int64_t)u * p.cap + S.rec[t]) * D, sub, kv[k]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < R::EPL; ++j) kv[k][j] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int t = base + k * kUnitWarps * R::RPW + rw;
+        double gmax = -INFINITY;
+        for (int hh = 0; hh < gs; ++hh) {
+          double a = 0.0;
+#pragma unroll
+          for (int v = 0; v < R::VPL; ++v) {
+            const float* qv = qs + hh * D + R::elem(sub, v);
+#pragma unroll
+            for (int j = 0; j < R::EPV; ++j) a = fma((double)qv[j], (double)kv[k][v * R::EPV + j], a);
+          }
+          a = row_sum<R::LPR>(a) * scale;
+          gmax = fmax(gmax, a);
+          if (sub == 0 && t < L) lg[(int64_t)hh * p.lmax + t] = a;
+        }
+        if (sub == 0 && t < L) {
+          S.skey[t] = ~okey64(gmax);
+          S.sval[t] = t;
+          if (p.grouped_out) p.grouped_out[(int64_t)u * p.lmax + t] = gmax;
+        }
+      }
+    }
+  } else if (L > 0) {
+    // scores supplied by the caller (fifo_update API)
+    for (int t = tid; t < L; t += blockDim.x) {
+      S.skey[t] = ~okey64(p.grouped_in[(int64_t)u * p.lmax + t]);
+      S.sval[t] = t;
+    }
+  }
+  for (int t = L + tid; t < npad; t += blockDim.x) {
+    S.skey[t] = ~0ull;
+    S.sval[t] = INT32_MAX;
+  }
+
+  // ---- 4. order by (score desc, recall position asc) --------------------
+  if (L > 0 && (p.stages & kStageSort)) bitonic_sort_pairs(S.skey, S.sval, npad);
+  __syncthreads();
+  if (p.order_out)
+    for (int i = tid; i < p.lmax; i += blockDim.x)
+      p.order_out[(int64_t)u * p.lmax + i] = i < L ? S.sval[i] : kEmpty;
+
+  // ---- 5. FIFO dynamic centroid update (ck/index.py:120-133) ------------
+  const bool dcu_here = (p.stages & kStageDcu) && (L > 0 || p.dcu_force);
+  if (dcu_here) {
+    const int64_t slot = s_slot;
+    int32_t* row = p.lists + ((int64_t)u * p.C + slot) * p.rho;
+    const int keep = min(p.rho, L);
+    for (int i = tid; i < p.rho; i += blockDim.x) row[i] = i < keep ? S.rec[S.sval[i]] : kEmpty;
+    T* cent = static_cast<T*>(p.cent);
+    for (int i = tid; i < gs * D; i += blockDim.x) {
+      const int hh = i / D, e = i % D;
+      cent[(((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D + e] = q[i];
+    }
+  }
+
+  // ---- 6. sparse attention over the top rho' (or the whole recall set) ---
+  if (p.stages & kStageAttend) {
+    const int R_ = (L > 0) ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
+    auto pos_of = [&](int i) { return p.use_rerank ? S.sval[i] : i; };
+    if (p.sparse_ids)
+      for (int i = tid; i < p.sparse_cap; i += blockDim.x)
+        p.sparse_ids[(int64_t)u * p.sparse_cap + i] = i < R_ ? S.rec[pos_of(i)] : kEmpty;
+    if (p.sparse_len && tid == 0) p.sparse_len[u] = R_;
+    __shared__ double ms[kMaxGroup], ls[kMaxGroup];
+    // per-head max over the sparse logits
+    for (int hh = 0; hh < gs; ++hh) {
+      double m = -INFINITY;
+      for (int i = tid; i < R_; i += blockDim.x) m = fmax(m, lg[(int64_t)hh * p.lmax + pos_of(i)]);
+      m = block_max_f64(m, S.scratch);
+      if (tid == 0) ms[hh] = m;
+    }
+    __syncthreads();
+    const T* vals = static_cast<const T*>(p.values);
+    // sparse set weights, chunk by chunk; accumulators live in the reduce
+    // area (aliases the sort keys, dead after ordering)
+    float* red = reinterpret_cast<float*>(S.skey);
+    for (int i = tid; i < kUnitWarps * gs * D; i += blockDim.x) red[i] = 0.f;
+    if (tid < gs) ls[tid] = 0.0;
+    for (int c0 = 0; c0 < R_; c0 += kAttnChunk) {
+      const int n = min(kAttnChunk, R_ - c0);
+      for (int hh = 0; hh < gs; ++hh) {
+        double lpart = 0.0;
+        for (int i = tid; i < n; i += blockDim.x) {
+          const double e = exp(lg[(int64_t)hh * p.lmax + pos_of(c0 + i)] - ms[hh]);
+          S.wts[hh * kAttnChunk + i] = (float)e;
+          lpart += e;
+        }
+        lpart = block_sum_f64(lpart, S.scratch);
+        if (tid == 0) ls[hh] += lpart;
+      }
+      __syncthreads();
+      accum_weighted_rows<T, D>(
+          n, gs,
+          [&](int t) -> const T* { return vals + ((int64_t)u * p.cap + S.rec[pos_of(c0 + t)]) * D; },
+          [&](int hh, int t) { return S.wts[hh * kAttnChunk + t]; }, red + (int64_t)warp * gs * D);
+      __syncthreads();
+    }
+    // ---- 7. exact merge with the static partials ------------------------
+    bool none = false;
+    for (int i = tid; i < gs * D; i += blockDim.x) {
+      const int hh = i / D;
+      float osp = 0.f;
+      for (int w = 0; w < kUnitWarps; ++w) osp += red[(int64_t)w * gs * D + i];
+      double M = R_ > 0 ? ms[hh] : -INFINITY;
+      const int64_t pbase = (int64_t)u * p.ns;
+      for (int j = 0; j < p.ns; ++j)
+        if (p.pl[(pbase + j) * gs + hh] > 0.0) M = fmax(M, p.pm[(pbase + j) * gs + hh]);
+      double Lsum = 0.0, O = 0.0;
+      if (R_ > 0) {
+        const double w = exp(ms[hh] - M);
+        Lsum += w * ls[hh];
+        O += w * (double)osp;
+      }
+      for (int j = 0; j < p.ns; ++j) {
+        const double lj = p.pl[(pbase + j) * gs + hh];
+        if (lj > 0.0) {
+          const double w = exp(p.pm[(pbase + j) * gs + hh] - M);
+          Lsum += w * lj;
+          O += w * (double)p.po[((pbase + j) * gs + hh) * D + (i % D)];
+        }
+      }
+      const int64_t oh = (int64_t)bi * p.h + gi * gs + hh;
+      if (Lsum > 0.0) {
+        p.out[oh * D + (i % D)] = (float)(O / Lsum);
+      } else {
+        p.out[oh * D + (i % D)] = 0.f;
+        none = true;
+      }
+      if (i % D == 0) {
+        if (p.row_max) p.row_max[oh] = M;
+        if (p.denom) p.denom[oh] = Lsum;
+      }
+    }
+    if (none) set_flag(p.flags, kFlagNoTokens);  // nothing attendable (ck/retrieval.py:355)
+  }
+
+  // ---- 8. completion: FIFO cursor advance and total++ by the last CTA ----
+  if (p.stages & (kStageDcu | kStageAppendTail)) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (dcu_here) atomicAdd(&p.sync[1 + bi], 1);
+      __threadfence();
+      const int prev = atomicAdd(&p.sync[0], 1);
+      if (prev == p.U - 1) {
+        __threadfence();
+        for (int b2 = 0; b2 < p.b; ++b2) {
+          const int hits = atomicExch(&p.sync[1 + b2], 0);
+          if (hits > 0) p.fifo[b2] = p.fifo[b2] % p.C + 1;
+        }
+        if (appending) *p.total = t0 + 1;
+        atomicExch(&p.sync[0], 0);
+        __threadfence();
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
+// generic id-list attention: split partials + merge (sparse_attention API)
+// ------------------------------------------------------------------------
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kScanThreads) attn_split_kernel(DecodeParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t total = *p.total;
+  const int per_unit = p.ns;  // splits per unit (list splits first, then static)
+  const int u = blockIdx.x / per_unit, split = blockIdx.x % per_unit;
+  const int slot = u * per_unit + split;
+  const int list_splits = p.list_splits;
+  if (split < list_splits) {
+    const int len = p.ids_shared ? p.len_in[0] : p.len_in[u];
+    const int32_t* ids = p.rec_in + (p.ids_shared ? 0 : (int64_t)u * p.lmax);
+    const int i0 = split * kAttnSplit;
+    const int ntok = max(0, min(kAttnSplit, len - i0));
+    attn_partial_block<T, D>(p, u, ntok, [&](int t) { return (int64_t)ids[i0 + t]; }, -1, total,
+                             p.pm + (int64_t)slot * p.gs, p.pl + (int64_t)slot * p.gs,
+                             p.po + (int64_t)slot * p.gs * D, smem);
+  } else {
+    const StaticSpan span(total, p.init_len, p.local_len);
+    const int64_t i0 = (int64_t)(split - list_splits) * kAttnSplit;
+    const int ntok = (int)max((int64_t)0, min((int64_t)kAttnSplit, span.n_static - i0));
+    attn_partial_block<T, D>(p, u, ntok, [&](int t) { return span.id(i0 + t); }, -1, total,
+                             p.pm + (int64_t)slot * p.gs, p.pl + (int64_t)slot * p.gs,
+                             p.po + (int64_t)slot * p.gs * D, smem);
+  }
+}
+
+// one thread per (unit, head, e): combine split partials
+__global__ void attn_merge_kernel(DecodeParams p, int D) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)p.U * p.gs * D;
+  if (i >= n) return;
+  const int e = (int)(i % D);
+  const int hh = (int)((i / D) % p.gs);
+  const int u = (int)(i / ((int64_t)D * p.gs));
+  const int bi = u / p.g, gi = u % p.g;
+  double M = -INFINITY;
+  for (int j = 0; j < p.ns; ++j) {
+    const int64_t s = ((int64_t)u * p.ns + j) * p.gs + hh;
+    if (p.pl[s] > 0.0) M = fmax(M, p.pm[s]);
+  }
+  double Lsum = 0.0, O = 0.0;
+  for (int j = 0; j < p.ns; ++j) {
+    const int64_t s = ((int64_t)u * p.ns + j) * p.gs + hh;
+    if (p.pl[s] > 0.0) {
+      const double w = exp(p.pm[s] - M);
+      Lsum += w * p.pl[s];
+      O += w * (double)p.po[s * D + e];
+    }
+  }
+  const int64_t oh = (int64_t)bi * p.h + gi * p.gs + hh;
+  p.out[oh * D + e] = Lsum > 0.0 ? (float)(O / Lsum) : 0.f;
+  if (e == 0) {
+    if (p.row_max) p.row_max[oh] = M;
+    if (p.denom) p.denom[oh] = Lsum;
+  }
+}
+
+__global__ void merge2_kernel(int64_t rows, int D, const float* oa, const double* ma,
+                              const double* la, const float* ob, const double* mb,
+                              const double* lb, float* out, double* mo, double* lo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * D) return;
+  const int64_t r = i / D;
+  const double m = fmax(ma[r], mb[r]);
+  const double wa = exp(ma[r] - m) * la[r];
+  const double wb = exp(mb[r] - m) * lb[r];
+  const double den = wa + wb;
+  out[i] = (float)(((double)oa[i] * wa + (double)ob[i] * wb) / den);
+  if (i % D == 0) {
+    if (mo) mo[r] = m;
+    if (lo) lo[r] = den;
+  }
+}
+
+template <typename T>
+__global__ void append_kernel(T* keys, T* vals, const T* kn, const T* vn, int64_t* total,
+                              int64_t units, int64_t cap, int D) {
+  const int64_t t0 = *total;
+  for (int64_t i = threadIdx.x; i < units * D; i += blockDim.x) {
+    const int64_t u = i / D, e = i % D;
+    keys[(u * cap + t0) * D + e] = kn[i];
+    vals[(u * cap + t0) * D + e] = vn[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *total = t0 + 1;
+}
+
+// ------------------------------------------------------------------------
+// launchers
+// ------------------------------------------------------------------------
+
+size_t scan_smem_bytes(const DecodeParams& p, int D) {
+  const size_t cosb = sizeof(float) * kMaxGroup * D + sizeof(double) * kMaxGroup +
+                      sizeof(double) * kMaxGroup * kCosChunk;
+  const size_t attb = sizeof(float) * kMaxGroup * D + sizeof(double) * kMaxGroup * kAttnSplit +
+                      2 * sizeof(double) * kMaxGroup + sizeof(float) * kScanWarps * p.gs * D;
+  return std::max(cosb, attb);
+}
+
+template <typename T, int D>
+static int launch_scan_t(const DecodeParams& p, int nblocks, cudaStream_t st) {
+  const size_t sm = scan_smem_bytes(p, D);
+  auto k = scan_kernel<T, D>;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (nblocks > 0) k<<<nblocks, kScanThreads, sm, st>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+}
+
+template <typename T, int D>
+static int launch_unit_t(const DecodeParams& p, cudaStream_t st) {
+  const size_t sm = unit_smem_bytes(p, D);
+  if (sm > 220 * 1024) return CTKV_ECONFIG;
+  auto k = unit_kernel<T, D>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k<<<p.U, kUnitThreads, sm, st>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+}
+
+template <typename T, int D>
+static int launch_attn_t(const DecodeParams& p, cudaStream_t st) {
+  const size_t sm = scan_smem_bytes(p, D);
+  auto k = attn_split_kernel<T, D>;
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k<<<p.U * p.ns, kScanThreads, sm, st>>>(p);
+  const int64_t n = (int64_t)p.U * p.gs * D;
+  attn_merge_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, D);
+  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+}
+
+#define CTKV_DISPATCH(DTYPE, DIM, FN, ...)                                              \
+  [&]() -> int {                                                                        \
+    if ((DTYPE) == CTKV_BF16) {                                                         \
+      switch (DIM) {                                                                    \
+        case 16: return FN<__nv_bfloat16, 16>(__VA_ARGS__);                             \
+        case 32: return FN<__nv_bfloat16, 32>(__VA_ARGS__);                             \
+        case 64: return FN<__nv_bfloat16, 64>(__VA_ARGS__);                             \
+        case 128: return FN<__nv_bfloat16, 128>(__VA_ARGS__);                           \
+        case 256: return FN<__nv_bfloat16, 256>(__VA_ARGS__);                           \
+      }                                                                                 \
+    } else {                                                                            \
+      switch (DIM) {                                                                    \
+        case 16: return FN<float, 16>(__VA_ARGS__);                                     \
+        case 32: return FN<float, 32>(__VA_ARGS__);                                     \
+        case 64: return FN<float, 64>(__VA_ARGS__);                                     \
+        case 128: return FN<float, 128>(__VA_ARGS__);                                   \
+        case 256: return FN<float, 256>(__VA_ARGS__);                                   \
+      }                                                                                 \
+    }                                                                                   \
+    return (int)CTKV_ESHAPE;                                                            \
+  }()
+
+int launch_scan(const DecodeParams& p, int dtype, int D, int nblocks, cudaStream_t st) {
+  return CTKV_DISPATCH(dtype, D, launch_scan_t, p, nblocks, st);
+}
+int launch_unit(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
+  return CTKV_DISPATCH(dtype, D, launch_unit_t, p, st);
+}
+int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
+  return CTKV_DISPATCH(dtype, D, launch_attn_t, p, st);
+}
+int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const double* la,
+                  const float* ob, const double* mb, const double* lb, float* out, double* mo,
+                  double* lo, cudaStream_t st) {
+  const int64_t n = rows * D;
+  if (n == 0) return 0;
+  merge2_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rows, D, oa, ma, la, ob, mb, lb, out,
+                                                              mo, lo);
+  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+}
+int launch_append(int dtype, void* keys, void* vals, const void* kn, const void* vn,
+                  int64_t* total, int64_t units, int64_t cap, int D, cudaStream_t st) {
+  if (dtype == CTKV_BF16)
+    append_kernel<__nv_bfloat16><<<1, 256, 0, st>>>(
+        (__nv_bfloat16*)keys, (__nv_bfloat16*)vals, (const __nv_bfloat16*)kn,
+        (const __nv_bfloat16*)vn, total, units, cap, D);
+  else
+    append_kernel<float><<<1, 256, 0, st>>>((float*)keys, (float*)vals, (const float*)kn,
+                                            (const float*)vn, total, units, cap, D);
+  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+}
+
+}  // namespace ctkv

@@ -1,0 +1,113 @@
+// Internal host<->device parameter blocks shared by the kernel files and
+// the C-ABI layer.  Not part of the public ABI (include/ctkv.h is).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ctkv {
+
+enum : int32_t {
+  kStageSelect = 1,      // top-C' slots from gcos
+  kStageUnion = 2,       // union of the selected lists (else rec_in/len_in)
+  kStageScores = 4,      // rerank logits + group max (else grouped_in)
+  kStageSort = 8,        // (score desc, position asc) order
+  kStageDcu = 16,        // FIFO dynamic centroid update
+  kStageAttend = 32,     // sparse attention + merge with static partials
+  kStageAppendTail = 64  // last CTA advances *total (fused append)
+};
+
+constexpr int32_t kFlagNoTokens = 128;  // nothing attendable (ConfigError)
+
+struct DecodeParams {
+  // layout
+  int b, h, g, gs, U;  // U = b * g units
+  int64_t cap;
+  int init_len, local_len;
+  // store
+  const void* keys;
+  const void* values;
+  int64_t* total;      // device scalar; nullptr -> id_bound is used instead
+  int64_t id_bound;
+  const void* k_new;  // fused append (nullable)
+  const void* v_new;
+  // index
+  void* cent;
+  int32_t* lists;
+  int64_t* fifo;
+  int32_t* sync;
+  int C, rho;
+  // step
+  const void* q;
+  int c_prime, rho_prime, use_rerank, dcu_force;
+  int stages;
+  int do_cos;
+  int cos_blocks_per_unit;
+  int ns;           // partial slots per unit (static splits, or list+static splits)
+  int list_splits;  // attn_split_kernel: leading splits that read id lists
+  int ids_shared;
+  int bitmap_words;
+  int lmax;
+  // workspace
+  double* gcos;     // [U][C]
+  double* pm;       // [U][ns][gs]
+  double* pl;       // [U][ns][gs]
+  float* po;        // [U][ns][gs][D]
+  double* logits;   // [U][gs][lmax]
+  // staged io
+  const int32_t* rec_in;
+  const int32_t* len_in;
+  const double* grouped_in;
+  int32_t* rec_out;
+  double* grouped_out;
+  int32_t* order_out;
+  // outputs
+  float* out;
+  double* row_max;
+  double* denom;
+  int32_t* selected;
+  int32_t* recall_len;
+  int32_t* sparse_ids;
+  int32_t* sparse_len;
+  int sparse_cap;
+  int32_t* flags;
+};
+
+size_t scan_smem_bytes(const DecodeParams& p, int D);
+size_t unit_smem_bytes(const DecodeParams& p, int D);
+int launch_scan(const DecodeParams& p, int dtype, int D, int nblocks, cudaStream_t st);
+int launch_unit(const DecodeParams& p, int dtype, int D, cudaStream_t st);
+int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st);
+int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const double* la,
+                  const float* ob, const double* mb, const double* lb, float* out, double* mo,
+                  double* lo, cudaStream_t st);
+int launch_append(int dtype, void* keys, void* vals, const void* kn, const void* vn,
+                  int64_t* total, int64_t units, int64_t cap, int D, cudaStream_t st);
+
+constexpr int kCosChunkHost = 64;
+constexpr int kStaticSplitHost = 64;
+constexpr int kAttnSplitHost = 64;
+
+// ---- build ---------------------------------------------------------------
+struct BuildParams {
+  int b, h, g, gs, d;
+  int64_t cap;            // key rows per (b,g)
+  const void* cent;       // [b,h,C,d]
+  const void* keys;       // [b,g,cap,d]
+  int64_t off_begin, n_off;
+  int C, rho;
+  int32_t* lists;         // [b,g,C,rho]
+  int32_t* flags;
+  int mode;
+};
+
+size_t build_workspace_bytes(const BuildParams& p);
+int launch_build(const BuildParams& p, int dtype, void* ws, size_t ws_bytes, cudaStream_t st);
+int launch_scores(int dtype, int b, int h, int g, int d, const void* q, int64_t m, const void* k,
+                  int64_t n, int64_t k_row_stride, int grouped, float* out, cudaStream_t st);
+size_t topk_workspace_bytes(int64_t rows, int64_t n, int k);
+int launch_topk_rows(const float* v, int64_t rows, int64_t n, int k, int32_t* idx, void* ws,
+                     size_t ws_bytes, cudaStream_t st);
+
+}  // namespace ctkv
