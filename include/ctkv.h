@@ -154,6 +154,15 @@ size_t ctkv_decode_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32
 int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctkv_step_args* A,
                      void* workspace, size_t workspace_bytes, void* stream);
 
+/* Same step split by kernel: phase 1 = scan kernel (cosine vs all
+ * centroids + static-partition attention partials + append), phase 2 =
+ * unit kernel (select, union, rerank, order, DCU, sparse attention,
+ * merge), 3 = both.  Lets a caller time each kernel with events or place
+ * other work between them; phase 2 must follow phase 1 of the same step. */
+int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
+                           const ctkv_step_args* A, int32_t phase, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
 /* recall (ck/retrieval.py:132-168): selected [b,g,C'], recalled
  * [b,g,C'*rho] first-occurrence order, recall_len [b,g].  Like the
  * reference it needs no store: `id_bound` is an exclusive upper bound of

@@ -70,6 +70,8 @@ SIGNATURES = {
     "ctkv_decode_workspace_bytes": (c_size, [ctypes.POINTER(Layout), c_i32, c_i32, c_i32, c_i32]),
     "ctkv_decode_step": (c_i32, [ctypes.POINTER(Layout), StoreDesc, IndexDesc,
                                  ctypes.POINTER(StepArgs), c_vp, c_size, c_vp]),
+    "ctkv_decode_step_phase": (c_i32, [ctypes.POINTER(Layout), StoreDesc, IndexDesc,
+                                       ctypes.POINTER(StepArgs), c_i32, c_vp, c_size, c_vp]),
     "ctkv_recall": (c_i32, [ctypes.POINTER(Layout), IndexDesc, c_i64, c_vp, c_i32, c_vp, c_vp,
                             c_vp, c_vp, c_vp, c_size, c_vp]),
     "ctkv_rerank": (c_i32, [ctypes.POINTER(Layout), StoreDesc, c_vp, c_vp, c_vp, c_i32, c_vp,

@@ -165,6 +165,13 @@ size_t ctkv_decode_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32
 
 int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctkv_step_args* A,
                      void* workspace, size_t workspace_bytes, void* stream) {
+  return ctkv_decode_step_phase(L, S, I, A, 3, workspace, workspace_bytes, stream);
+}
+
+int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
+                           const ctkv_step_args* A, int32_t phase, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  if (phase < 1 || phase > 3) return CTKV_ECONFIG;
   if (int rc = check_layout(L)) return rc;
   if (!A || !A->query || !A->out || !S.keys || !S.values || !S.total) return CTKV_ECONFIG;
   if (I.capacity < 1) return CTKV_ECONFIG;                            // "recall: empty index"
@@ -218,8 +225,10 @@ int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctk
   if (unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
-  if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;
-  return launch_unit(p, L->dtype, L->head_dim, st);
+  if (phase & 1)
+    if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;
+  if (phase & 2) return launch_unit(p, L->dtype, L->head_dim, st);
+  return CTKV_OK;
 }
 
 int ctkv_recall(const ctkv_layout* L, ctkv_index I, int64_t id_bound, const void* query,

@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(kUnitThreads, 1) unit_kernel(DecodeParams p) {
         }
       }
     }
-  } else if (L > 0) {
+  } else if (L > 0 && p.grouped_in != nullptr) {
     // scores supplied by the caller (fifo_update API)
     for (int t = tid; t < L; t += blockDim.x) {
       S.skey[t] = ~okey64(p.grouped_in[(int64_t)u * p.lmax + t]);

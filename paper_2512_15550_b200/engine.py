@@ -1,0 +1,128 @@
+"""Multi-layer decode engine: the serving-shaped entry point.
+
+One (KvStore, QueryCentroidIndex) pair per layer lives in HBM; a decode
+step walks the layers in order and, per layer, enqueues the fused kernel
+pair (scan + unit: append, recall, rerank, sparse/static attention, merge,
+DCU) -- two launches per layer, no host synchronisation, so the whole step
+is captured once as a CUDA graph and replayed per token.  Under a ShardPlan
+each rank owns a (batch x kv-head) shard and all-gathers the head-sharded
+outputs after every layer (captured in the same graph).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+from .index import QueryCentroidIndex
+from .parallel import ShardPlan, all_gather_outputs
+from .retrieval import DecodeConfig, StepBuffers, launch_step
+from .store import KvStore
+
+
+@dataclass
+class Layer:
+    store: KvStore
+    index: QueryCentroidIndex
+    bufs: StepBuffers
+
+
+class DecodeEngine:
+    def __init__(self, layers: list[tuple[KvStore, QueryCentroidIndex]], cfg: DecodeConfig, *,
+                 plan: ShardPlan | None = None, group=None):
+        if not layers:
+            raise ValueError("DecodeEngine needs at least one layer")
+        self.cfg = cfg
+        self.plan = plan
+        self.group = group
+        st0 = layers[0][0]
+        lay = st0.layout
+        self.b, self.h, self.g, self.d = lay.batch, lay.query_heads, lay.kv_heads, lay.head_dim
+        self.dtype = st0.dtype
+        dev = st0.keys.device
+        shared_ws = None
+        self.layers: list[Layer] = []
+        for store, index in layers:
+            bufs = StepBuffers.allocate(store, index, cfg)
+            # layers run back to back on one stream: one workspace serves all
+            if shared_ws is None or shared_ws.numel() < bufs.ws.numel():
+                shared_ws = bufs.ws
+            self.layers.append(Layer(store, index, bufs))
+        for layer in self.layers:
+            layer.bufs.ws = shared_ws
+        nl = len(self.layers)
+        # step inputs (device): q [L,b,h,d], k/v [L,b,g,d]
+        self.q = torch.zeros((nl, self.b, self.h, self.d), dtype=self.dtype, device=dev)
+        self.k = torch.zeros((nl, self.b, self.g, self.d), dtype=self.dtype, device=dev)
+        self.v = torch.zeros((nl, self.b, self.g, self.d), dtype=self.dtype, device=dev)
+        self.out = torch.zeros((nl, self.b, self.h, self.d), dtype=torch.float32, device=dev)
+        world = plan.world if plan else 1
+        self.gathered = (torch.zeros((nl, plan.batch, plan.query_heads, self.d), dtype=torch.float32,
+                                     device=dev) if world > 1 else self.out)
+        self._gbuf = (torch.empty((world, self.b, self.h, self.d), dtype=torch.float32, device=dev)
+                      if world > 1 else None)
+        self.graph: torch.cuda.CUDAGraph | None = None
+        self.steps_done = 0
+
+    # -- one step -------------------------------------------------------------
+
+    def _enqueue(self, events=None) -> None:
+        for li, layer in enumerate(self.layers):
+            if events is not None:
+                events[li][0].record()
+                launch_step(layer.store, layer.index, self.cfg, self.q[li], layer.bufs,
+                            self.k[li], self.v[li], phase=1)
+                events[li][1].record()
+                launch_step(layer.store, layer.index, self.cfg, self.q[li], layer.bufs,
+                            self.k[li], self.v[li], phase=2)
+                events[li][2].record()
+            else:
+                launch_step(layer.store, layer.index, self.cfg, self.q[li], layer.bufs,
+                            self.k[li], self.v[li])
+            self.out[li].copy_(layer.bufs.out)
+            if self._gbuf is not None:
+                self.gathered[li].copy_(all_gather_outputs(self.plan, self.out[li], self.group,
+                                                           self._gbuf))
+
+    def _note(self) -> None:
+        for layer in self.layers:
+            layer.store.note_device_append()
+        self.steps_done += 1
+
+    def reserve(self, steps: int) -> None:
+        for layer in self.layers:
+            layer.store.ensure_room(steps)
+
+    def step(self, events=None) -> None:
+        """Enqueue one decode step (all layers) eagerly."""
+        self._enqueue(events)
+        self._note()
+
+    def capture(self) -> None:
+        """Capture one step as a CUDA graph (state is device-resident, so
+        replays advance the stores, cursors and FIFO exactly like eager
+        steps).  Call after at least one eager warm-up step."""
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        # the capture itself must not run the kernels: snapshot nothing, the
+        # graph records launches only
+        with torch.cuda.graph(g):
+            self._enqueue()
+        self.graph = g
+
+    def replay(self) -> None:
+        if self.graph is None:
+            raise RuntimeError("capture() first")
+        self.graph.replay()
+        self._note()
+
+    def flags(self) -> int:
+        f = 0
+        for layer in self.layers:
+            f |= int(layer.bufs.flags.item())
+        return f
+
+    def check(self) -> None:
+        N.raise_flags(self.flags(), "decode step")

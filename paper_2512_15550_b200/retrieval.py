@@ -360,7 +360,7 @@ class StepBuffers:
 
 def launch_step(store: KvStore, index: QueryCentroidIndex, cfg: DecodeConfig, q: torch.Tensor,
                 bufs: StepBuffers, k_new: torch.Tensor | None = None,
-                v_new: torch.Tensor | None = None, stream=None) -> None:
+                v_new: torch.Tensor | None = None, stream=None, phase: int = 3) -> None:
     """Enqueue one fused decode step (append when k_new is given) -- no
     host synchronisation; safe to capture in a CUDA graph."""
     if cfg.c_prime > index.capacity:
@@ -370,9 +370,9 @@ def launch_step(store: KvStore, index: QueryCentroidIndex, cfg: DecodeConfig, q:
                       bufs.row_max.data_ptr(), bufs.denom.data_ptr(), bufs.selected.data_ptr(),
                       bufs.recall_len.data_ptr(), bufs.sparse_ids.data_ptr(),
                       bufs.sparse_len.data_ptr(), bufs.sparse_cap, bufs.flags.data_ptr())
-    N.check(N.lib().ctkv_decode_step(store.ctkv_layout(), store.desc(), index.desc(), args,
-                                     bufs.ws.data_ptr(), bufs.ws.numel(), N.stream_ptr(stream)),
-            "decode_step")
+    N.check(N.lib().ctkv_decode_step_phase(store.ctkv_layout(), store.desc(), index.desc(), args,
+                                           phase, bufs.ws.data_ptr(), bufs.ws.numel(),
+                                           N.stream_ptr(stream)), "decode_step")
 
 
 def trace_row(step: int, cfg: DecodeConfig, store: KvStore, index: QueryCentroidIndex,
