@@ -90,6 +90,7 @@ SIGNATURES = {
 }
 
 _lib = None
+_device_ok: dict[int, bool] = {}
 
 
 def load_library(require_device: bool = True):
@@ -110,10 +111,14 @@ def load_library(require_device: bool = True):
             raise RuntimeError("libctkv.so ABI version mismatch")
         _lib = lib
     if require_device:
-        if not torch.cuda.is_available():
-            raise RuntimeError("paper_2512_15550_b200 needs a CUDA device (B200, sm_100a); "
-                               "there is no CPU fallback")
-        if not _lib.ctkv_device_ok():
+        dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+        ok = _device_ok.get(dev)
+        if ok is None:
+            if dev < 0:
+                raise RuntimeError("paper_2512_15550_b200 needs a CUDA device (B200, sm_100a); "
+                                   "there is no CPU fallback")
+            ok = _device_ok[dev] = bool(_lib.ctkv_device_ok())
+        if not ok:
             raise RuntimeError("libctkv.so is built for sm_100a only; this device is not a B200")
     return _lib
 

@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(kTThreads) topk_rows_kernel(const float* __res
                                                               int32_t* __restrict__ idx_out,
                                                               int64_t out_ld, int32_t add,
                                                               int64_t rows_per_group,
-                                                              int64_t group_stride) {
+                                                              int64_t group_stride,
+                                                              const int32_t* row_map) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int64_t row = blockIdx.x;
   const float* v = vals + row * ld;
@@ -216,7 +217,8 @@ __global__ void __launch_bounds__(kTThreads) topk_rows_kernel(const float* __res
   __syncthreads();
   for (int i = k + tid; i < kp; i += kTThreads) cand[i] = ~0ull;
   bitonic_sort_u64(cand, kp);
-  int32_t* dst = idx_out + (row / rows_per_group) * group_stride + (row % rows_per_group) * out_ld;
+  int32_t* dst = row_map ? idx_out + (int64_t)row_map[row] * out_ld
+                        : idx_out + (row / rows_per_group) * group_stride + (row % rows_per_group) * out_ld;
   for (int i = tid; i < k; i += kTThreads) dst[i] = (int32_t)(cand[i] & 0xffffffffu) + add;
 }
 
@@ -230,8 +232,8 @@ static size_t topk_smem(int64_t n, int k, bool smem_row) {
 }
 
 int topk_launch(const float* v, int64_t rows, int64_t n, int64_t ld, int k, int32_t* out,
-                int64_t out_ld, int32_t add, cudaStream_t st, int64_t rows_per_group = -1,
-                int64_t group_stride = 0) {
+                int64_t out_ld, int32_t add, cudaStream_t st, int64_t rows_per_group,
+                int64_t group_stride, const int32_t* row_map) {
   if (rows_per_group <= 0) {
     rows_per_group = rows > 0 ? rows : 1;
     group_stride = 0;
@@ -243,11 +245,13 @@ int topk_launch(const float* v, int64_t rows, int64_t n, int64_t ld, int k, int3
   if (smem_row) {
     cudaFuncSetAttribute(topk_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     topk_rows_kernel<true><<<(unsigned)rows, kTThreads, sm, st>>>(v, n, ld, k, out, out_ld, add,
-                                                                  rows_per_group, group_stride);
+                                                                  rows_per_group, group_stride,
+                                                                  row_map);
   } else {
     cudaFuncSetAttribute(topk_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     topk_rows_kernel<false><<<(unsigned)rows, kTThreads, sm, st>>>(v, n, ld, k, out, out_ld, add,
-                                                                  rows_per_group, group_stride);
+                                                                  rows_per_group, group_stride,
+                                                                  row_map);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
@@ -256,7 +260,7 @@ size_t topk_workspace_bytes(int64_t, int64_t, int) { return 0; }
 
 int launch_topk_rows(const float* v, int64_t rows, int64_t n, int k, int32_t* idx, void*, size_t,
                      cudaStream_t st) {
-  return topk_launch(v, rows, n, n, k, idx, k, 0, st);
+  return topk_launch(v, rows, n, n, k, idx, k, 0, st, -1, 0, nullptr);
 }
 
 template <typename T, typename ACC>
@@ -320,7 +324,22 @@ static int chunk_rows(const BuildParams& p, size_t ws_bytes) {
   return (int)c;
 }
 
+bool build_tc_supported(const BuildParams& p, int dtype);
+size_t build_tc_workspace_bytes(const BuildParams& p);
+int build_tc(const BuildParams& p, int dtype, void* ws, size_t ws_bytes, cudaStream_t st);
+
+size_t build_simt_workspace_bytes(const BuildParams& p);
+
 size_t build_workspace_bytes(const BuildParams& p) {
+  size_t b = build_simt_workspace_bytes(p);
+  if (p.mode == CTKV_BUILD_FAST && build_tc_supported(p, p.dtype)) {
+    const size_t t = build_tc_workspace_bytes(p);
+    if (t > b) b = t;
+  }
+  return b;
+}
+
+size_t build_simt_workspace_bytes(const BuildParams& p) {
   // one materialised chunk of up to 64 centroids (or all C when smaller),
   // capped at 2 GiB
   const int U = p.b * p.g;
@@ -331,10 +350,11 @@ size_t build_workspace_bytes(const BuildParams& p) {
   return c * per_c;
 }
 
-int build_tc(const BuildParams& p, int dtype, void* ws, size_t ws_bytes, cudaStream_t st);
-
 int launch_build(const BuildParams& p, int dtype, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (p.rho == 0 || p.C == 0) return 0;
+  if (p.mode == CTKV_BUILD_FAST && build_tc_supported(p, dtype) &&
+      build_tc_workspace_bytes(p) <= ws_bytes)
+    return build_tc(p, dtype, ws, ws_bytes, st);
   const int U = p.b * p.g;
   const int cr = chunk_rows(p, ws_bytes);
   if (cr < 1) return CTKV_EWORKSPACE;
@@ -346,7 +366,7 @@ int launch_build(const BuildParams& p, int dtype, void* ws, size_t ws_bytes, cud
     if (rc) return rc;
     // lists[u][c_lo + r][:] = off_begin + topk(S[u][r][:]), one launch
     rc = topk_launch(S, (int64_t)U * nc, p.n_off, p.n_off, p.rho, p.lists + (int64_t)c_lo * p.rho,
-                     p.rho, (int32_t)p.off_begin, st, nc, (int64_t)p.C * p.rho);
+                     p.rho, (int32_t)p.off_begin, st, nc, (int64_t)p.C * p.rho, nullptr);
     if (rc) return rc;
   }
   return 0;

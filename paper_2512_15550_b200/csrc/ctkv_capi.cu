@@ -97,9 +97,11 @@ const char* ctkv_status_string(int s) {
 int ctkv_device_ok(void) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return 0;
-  return prop.major == 10 && prop.minor == 0 ? 1 : 0;
+  int major = 0, minor = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
+    return 0;
+  return major == 10 && minor == 0 ? 1 : 0;
 }
 
 int ctkv_append(const ctkv_layout* L, ctkv_store S, const void* k_new, const void* v_new,
@@ -124,6 +126,8 @@ size_t ctkv_build_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32_
   p.rho = rho;
   p.n_off = n_off;
   p.mode = mode;
+  p.dtype = L->dtype;
+  p.cap = L->capacity;
   return build_workspace_bytes(p);
 }
 
@@ -154,6 +158,7 @@ int ctkv_build_lists(const ctkv_layout* L, const void* centroids, const void* ke
   p.lists = lists;
   p.flags = flags;
   p.mode = mode;
+  p.dtype = L->dtype;
   return launch_build(p, L->dtype, workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
@@ -377,7 +382,11 @@ int ctkv_merge(int64_t rows, int32_t head_dim, const float* out_a, const double*
 
 int ctkv_scores(const ctkv_layout* L, const void* q, int64_t m, const void* k, int64_t n,
                 int64_t k_row_stride, int32_t grouped, float* out, void* stream) {
-  if (int rc = check_layout(L)) return rc;
+  // any head_dim works here (the SIMT scores kernel tiles d generically)
+  if (!L || L->head_dim < 1) return CTKV_ESHAPE;
+  ctkv_layout l2 = *L;
+  l2.head_dim = 16;
+  if (int rc = check_layout(&l2)) return rc;
   const int gs = L->query_heads / L->kv_heads;
   if (gs != 1 && gs != 2 && gs != 4 && gs != 8) return CTKV_ESHAPE;
   if (m < 0 || n < 0) return CTKV_ESHAPE;

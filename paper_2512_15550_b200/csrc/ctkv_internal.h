@@ -100,6 +100,7 @@ struct BuildParams {
   int32_t* lists;         // [b,g,C,rho]
   int32_t* flags;
   int mode;
+  int dtype;
 };
 
 size_t build_workspace_bytes(const BuildParams& p);

@@ -98,5 +98,8 @@ def all_gather_outputs(plan: ShardPlan, local: torch.Tensor, group=None,
         return local
     if buf is None:
         buf = local.new_empty((plan.world,) + tuple(local.shape))
-    dist.all_gather_into_tensor(buf, local.contiguous(), group=group)
+    # output passed as [world * b_loc, h_loc, d] (rank-major concat): the
+    # form both NCCL and gloo accept
+    dist.all_gather_into_tensor(buf.view((-1,) + tuple(local.shape[1:])), local.contiguous(),
+                                group=group)
     return plan.assemble(buf)
