@@ -28,9 +28,17 @@ int check_layout(const ctkv_layout* L) {
   return CTKV_OK;
 }
 
+// static-partition partial slots of the fused scan kernel (dtype-sized splits)
 int static_slots(const ctkv_layout* L) {
   const int64_t n = (int64_t)L->init_len + L->local_len;
-  return (int)((n + kStaticSplitHost - 1) / kStaticSplitHost);
+  const int st = static_tok_for(L->dtype);
+  return (int)((n + st - 1) / st);
+}
+
+// static slots of the generic attend kernel (64-token splits)
+int attend_static_slots(const ctkv_layout* L) {
+  const int64_t n = (int64_t)L->init_len + L->local_len;
+  return (int)((n + kAttnSplitHost - 1) / kAttnSplitHost);
 }
 
 struct DecodeWs {
@@ -210,7 +218,7 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.stages = kStageSelect | kStageUnion | kStageScores | kStageSort | kStageAttend |
              (A->use_dcu ? kStageDcu : 0) | (A->k_new ? kStageAppendTail : 0);
   p.do_cos = 1;
-  p.cos_blocks_per_unit = (I.capacity + kCosChunkHost - 1) / kCosChunkHost;
+  p.cos_blocks_per_unit = (I.capacity + (256 / p.gs) - 1) / (256 / p.gs);
   p.ns = ns;
   p.lmax = lmax;
   p.gcos = w.gcos;
@@ -227,12 +235,15 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.sparse_len = A->sparse_len;
   p.sparse_cap = A->sparse_ids ? A->sparse_cap : 0;
   p.flags = A->flags;
-  if (unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
+  // bf16: 2-CTA cluster unit kernel (f32-chunked logits); f32: exact f64 unit kernel
+  const bool v2 = L->dtype == CTKV_BF16 && L->head_dim >= 64 && unit2_smem_bytes(p, L->head_dim) <= 200 * 1024;
+  if (!v2 && unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
   if (phase & 1)
     if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;
-  if (phase & 2) return launch_unit(p, L->dtype, L->head_dim, st);
+  if (phase & 2) return v2 ? launch_unit2(p, L->dtype, L->head_dim, st)
+                           : launch_unit(p, L->dtype, L->head_dim, st);
   return CTKV_OK;
 }
 
@@ -260,7 +271,7 @@ int ctkv_recall(const ctkv_layout* L, ctkv_index I, int64_t id_bound, const void
   p.c_prime = c_prime;
   p.stages = kStageSelect | kStageUnion;
   p.do_cos = 1;
-  p.cos_blocks_per_unit = (I.capacity + kCosChunkHost - 1) / kCosChunkHost;
+  p.cos_blocks_per_unit = (I.capacity + (256 / p.gs) - 1) / (256 / p.gs);
   p.ns = 0;
   p.lmax = lmax;
   p.gcos = w.gcos;
@@ -335,7 +346,7 @@ int ctkv_fifo_update(const ctkv_layout* L, ctkv_index I, const void* query,
 
 size_t ctkv_attend_workspace_bytes(const ctkv_layout* L, int32_t lmax, int32_t with_static) {
   if (check_layout(L)) return 0;
-  const int ns = (lmax + kAttnSplitHost - 1) / kAttnSplitHost + (with_static ? static_slots(L) : 0);
+  const int ns = (lmax + kAttnSplitHost - 1) / kAttnSplitHost + (with_static ? attend_static_slots(L) : 0);
   return carve_decode(L, 0, 0, ns, nullptr).bytes;
 }
 
@@ -346,7 +357,7 @@ int ctkv_attend(const ctkv_layout* L, ctkv_store S, const void* query, const int
   if (int rc = check_layout(L)) return rc;
   if (!out || lmax < 0 || (lmax > 0 && (!ids || !ids_len))) return CTKV_ECONFIG;
   const int list_splits = lmax > 0 ? (lmax + kAttnSplitHost - 1) / kAttnSplitHost : 0;
-  const int ns = list_splits + (with_static ? static_slots(L) : 0);
+  const int ns = list_splits + (with_static ? attend_static_slots(L) : 0);
   if (ns == 0) return CTKV_ECONFIG;
   DecodeWs w = carve_decode(L, 0, 0, ns, workspace);
   if (w.bytes > workspace_bytes) return CTKV_EWORKSPACE;

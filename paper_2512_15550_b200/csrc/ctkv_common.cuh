@@ -176,4 +176,95 @@ __device__ __forceinline__ void set_flag(int32_t* flags, int32_t bit) {
   if (flags) atomicOr(flags, bit);
 }
 
+// ---- async-proxy helpers (mbarrier + TMA bulk copies) ----------------------
+
+__device__ __forceinline__ uint32_t sa(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "BW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra BD_%=;\n\t"
+      "bra BW_%=;\n\t"
+      "BD_%=:\n\t}" ::"r"(sa(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared (16 B aligned, multiple of 16 B)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          sa(dst)),
+      "l"(src), "r"(bytes), "r"(sa(bar))
+      : "memory");
+}
+
+// Register bitonic sort of packed u64 keys across a block: element
+// t*IPT + i lives in thread t, register i; strides inside a thread are
+// register swaps, inside a warp shuffles, beyond a warp go through `xch`
+// (blockDim*IPT u64 of shared memory).  Ascending.
+template <int IPT>
+__device__ void bitonic_regs(uint64_t (&k)[IPT], uint64_t* xch) {
+  const int t = threadIdx.x;
+  const int n = blockDim.x * IPT;
+  for (int size = 2; size <= n; size <<= 1) {
+    // strides >= IPT: partner in another lane (shuffle) or another warp (smem)
+    for (int stride = size >> 1; stride >= IPT; stride >>= 1) {
+      if (stride < 32 * IPT) {
+        const int lm = stride / IPT;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const int e = t * IPT + i;
+          const bool up = (e & size) == 0;
+          const bool lower = (e & stride) == 0;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, k[i], lm);
+          const uint64_t mn = o < k[i] ? o : k[i], mx = o < k[i] ? k[i] : o;
+          k[i] = (lower == up) ? mn : mx;
+        }
+      } else {
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) xch[t * IPT + i] = k[i];
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const int e = t * IPT + i;
+          const bool up = (e & size) == 0;
+          const bool lower = (e & stride) == 0;
+          const uint64_t o = xch[e ^ stride];
+          const uint64_t mn = o < k[i] ? o : k[i], mx = o < k[i] ? k[i] : o;
+          k[i] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+    // strides < IPT: compile-time register pairs
+#pragma unroll
+    for (int stride = IPT / 2; stride > 0; stride >>= 1) {
+      if (stride < size) {
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const int j = i ^ stride;
+          if (j > i) {
+            const bool up = ((t * IPT + i) & size) == 0;
+            const uint64_t a = k[i], b = k[j];
+            const bool sw = (a > b) == up;
+            k[i] = sw ? b : a;
+            k[j] = sw ? a : b;
+          }
+        }
+      }
+    }
+  }
+}
+
 }  // namespace ctkv

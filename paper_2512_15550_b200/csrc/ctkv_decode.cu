@@ -27,16 +27,19 @@
 #include <cmath>
 #include <cstdio>
 
+#include <cooperative_groups.h>
+
 #include "ctkv.h"
 #include "ctkv_common.cuh"
 #include "ctkv_internal.h"
 
 namespace ctkv {
 
+constexpr int kScanRowsV2 = 256;   // threads (and centroid rows) per v2 scan CTA
+
 constexpr int kScanThreads = 256;
 constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kCosChunk = 64;       // centroids per scan CTA (all gs heads)
-constexpr int kStaticSplit = 64;    // static tokens per scan CTA
 constexpr int kUnitThreads = 512;
 constexpr int kUnitWarps = kUnitThreads / 32;
 constexpr int kAttnChunk = 512;     // sparse tokens per weight chunk
@@ -132,83 +135,6 @@ __device__ void accum_weighted_rows(int n, int gs, RowFn rowfn, WFn wfn, float* 
 // scan kernel: cosine chunks + static attention splits (+ append)
 // ------------------------------------------------------------------------
 
-template <typename T, int D>
-__device__ void cos_block(const DecodeParams& p, int bid, unsigned char* smem) {
-  using R = Row<T, D>;
-  const int cpu = p.cos_blocks_per_unit;
-  const int u = bid / cpu, chunk = bid % cpu;
-  const int bi = u / p.g, gi = u % p.g, gs = p.gs;
-  const int c0 = chunk * kCosChunk;
-  const int nc = min(kCosChunk, p.C - c0);
-  float* qs = reinterpret_cast<float*>(smem);                    // [gs][D]
-  double* qn = reinterpret_cast<double*>(qs + kMaxGroup * D);    // [gs]
-  double* cosv = qn + kMaxGroup;                                 // [gs][kCosChunk]
-  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = to_f(q[i]);
-  __syncthreads();
-  if (threadIdx.x < gs) {
-    double s = 0.0;
-    for (int e = 0; e < D; ++e) s = fma((double)qs[threadIdx.x * D + e], (double)qs[threadIdx.x * D + e], s);
-    qn[threadIdx.x] = sqrt(s);
-  }
-  __syncthreads();
-  const T* cent = static_cast<const T*>(p.cent);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = lane % R::LPR, rw = lane / R::LPR;
-  const int nrows = gs * nc;
-  constexpr int U = 4;
-  for (int base = warp * R::RPW; base < nrows; base += kScanWarps * R::RPW * U) {
-    float kv[U][R::EPL];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int r = base + k * kScanWarps * R::RPW + rw;
-      if (r < nrows) {
-        const int hh = r / nc, c = c0 + r % nc;
-        const T* row = cent + (((int64_t)bi * p.h + gi * gs + hh) * p.C + c) * D;
-        load_row_slice<T, D, true>(row, sub, kv[k]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < R::EPL; ++j) kv[k][j] = 0.f;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int r = base + k * kScanWarps * R::RPW + rw;
-      const int hh = r < nrows ? r / nc : 0;
-      double dot = 0.0, nrm = 0.0;
-#pragma unroll
-      for (int v = 0; v < R::VPL; ++v) {
-        const float* qv = qs + hh * D + R::elem(sub, v);
-#pragma unroll
-        for (int j = 0; j < R::EPV; ++j) {
-          const double x = (double)kv[k][v * R::EPV + j];
-          dot = fma((double)qv[j], x, dot);
-          nrm = fma(x, x, nrm);
-        }
-      }
-      dot = row_sum<R::LPR>(dot);
-      nrm = row_sum<R::LPR>(nrm);
-      if (sub == 0 && r < nrows) {
-        const double den = qn[hh] * sqrt(nrm);
-        double c;
-        if (den == 0.0) {
-          c = 0.0;
-          set_flag(p.flags, kFlagDegenerate);
-        } else {
-          c = fmin(fmax(dot / den, -1.0), 1.0);
-        }
-        cosv[hh * kCosChunk + (r % nc)] = c;
-      }
-    }
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-    double m = cosv[c];
-    for (int hh = 1; hh < gs; ++hh) m = fmax(m, cosv[hh * kCosChunk + c]);
-    p.gcos[(int64_t)u * p.C + c0 + c] = m;
-  }
-}
-
 struct StaticSpan {
   int64_t n_init, ring_start, n_static;
   __device__ StaticSpan(int64_t total, int init_len, int local_len) {
@@ -302,38 +228,249 @@ __device__ void attn_partial_block(const DecodeParams& p, int u, int ntok, IdFn 
   }
 }
 
+// ------------------------------------------------------------------------
+// v2 scan: one task per CTA, operands pulled with TMA bulk copies into
+// shared memory, one row per thread.  For bf16 rows the bf16 x bf16
+// products are exact in f32; each 8-element chunk is summed in f32 and the
+// chunk partials in f64 (relative error <= 7 * 2^-24 of the chunk's
+// absolute sum -- inside the 1e-6 tie window).  f32 rows use f64 products.
+// ------------------------------------------------------------------------
+
+template <typename T> struct Prec;
+template <> struct Prec<__nv_bfloat16> { static constexpr bool kChunkF32 = true; };
+template <> struct Prec<float> { static constexpr bool kChunkF32 = false; };
+
+// dot(q, row) and |row|^2 with rotated 16-byte chunk order (conflict-free
+// when consecutive threads own consecutive rows)
+template <typename T, int D, bool kNorm>
+__device__ __forceinline__ void row_dot(const float* qv, const T* row, int rot, double& dot,
+                                        double& nrm) {
+  constexpr int EPV = 16 / int(sizeof(T));
+  constexpr int VPR = D / EPV;
+  const uint4* r4 = reinterpret_cast<const uint4*>(row);
+  dot = 0.0;
+  nrm = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < VPR; ++k) {
+    const int kk = (k + rot) & (VPR - 1);
+    float x[EPV];
+    unpack16<T>(r4[kk], x);
+    const float* q = qv + kk * EPV;
+    if (Prec<T>::kChunkF32) {
+      float pd = 0.f, pn = 0.f;
+#pragma unroll
+      for (int j = 0; j < EPV; ++j) {
+        pd = fmaf(q[j], x[j], pd);
+        if (kNorm) pn = fmaf(x[j], x[j], pn);
+      }
+      dot += (double)pd;
+      if (kNorm) nrm += (double)pn;
+    } else {
+#pragma unroll
+      for (int j = 0; j < EPV; ++j) {
+        dot = fma((double)q[j], (double)x[j], dot);
+        if (kNorm) nrm = fma((double)x[j], (double)x[j], nrm);
+      }
+    }
+  }
+}
+
+template <typename T>
+__host__ __device__ constexpr int static_tok() { return sizeof(T) == 2 ? 128 : 64; }
+
 template <typename T, int D>
-__global__ void __launch_bounds__(kScanThreads) scan_kernel(DecodeParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+__device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, uint64_t* bar) {
+  constexpr int RB = D * int(sizeof(T));
+  const int gs = p.gs, CC = kScanRowsV2 / gs;
+  const int cpu = p.cos_blocks_per_unit;
+  const int u = task / cpu, chunk = task % cpu;
+  const int bi = u / p.g, gi = u % p.g;
+  const int c0 = chunk * CC, nc = min(CC, p.C - c0);
+  T* rows = reinterpret_cast<T*>(smem);                                   // [gs][CC][D]
+  float* qs = reinterpret_cast<float*>(smem + (size_t)kScanRowsV2 * RB);  // [gs][D]
+  double* qn = reinterpret_cast<double*>(qs + gs * D);                    // [gs]
+  double* cosv = qn + gs;                                                 // [gs*CC]
+  const T* cent = static_cast<const T*>(p.cent);
+  if (threadIdx.x == 0) {
+    bar_init(bar, 1);
+    bar_expect(bar, (uint32_t)(gs * nc * RB));
+    for (int j = 0; j < gs; ++j)
+      bulk_g2s(rows + (size_t)j * CC * D, cent + (((int64_t)bi * p.h + gi * gs + j) * p.C + c0) * D,
+               (uint32_t)(nc * RB), bar);
+  }
+  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
+  for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = to_f(q[i]);
+  __syncthreads();
+  if (threadIdx.x < gs) {
+    double s = 0.0;
+    for (int e = 0; e < D; ++e) s = fma((double)qs[threadIdx.x * D + e], (double)qs[threadIdx.x * D + e], s);
+    qn[threadIdx.x] = sqrt(s);
+  }
+  __syncthreads();
+  bar_wait(bar, 0);
+  for (int r = threadIdx.x; r < gs * CC; r += blockDim.x) {
+    const int j = r / CC, c = r % CC;
+    if (c >= nc) continue;
+    double dot, nrm;
+    row_dot<T, D, true>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
+    const double den = qn[j] * sqrt(nrm);
+    double cv;
+    if (den == 0.0) {
+      cv = 0.0;
+      set_flag(p.flags, kFlagDegenerate);
+    } else {
+      cv = fmin(fmax(dot / den, -1.0), 1.0);
+    }
+    cosv[r] = cv;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+    double m = cosv[c];
+    for (int j = 1; j < gs; ++j) m = fmax(m, cosv[j * CC + c]);
+    p.gcos[(int64_t)u * p.C + c0 + c] = m;
+  }
+}
+
+// attention partial over static tokens [i0, i0+ST) of the static index space
+template <typename T, int D>
+__device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t total,
+                            unsigned char* smem, uint64_t* bar) {
+  constexpr int RB = D * int(sizeof(T));
+  constexpr int ST = static_tok<T>();
+  const int gs = p.gs;
+  const int u = task / p.ns, split = task % p.ns;
+  const int bi = u / p.g, gi = u % p.g;
+  const StaticSpan span(total, p.init_len, p.local_len);
+  const int64_t i0 = (int64_t)split * ST;
+  const int nt = (int)max((int64_t)0, min((int64_t)ST, span.n_static - i0));
+  T* Ks = reinterpret_cast<T*>(smem);                           // [ST][D]
+  T* Vs = Ks + (size_t)ST * D;                                  // [ST][D]
+  float* qs = reinterpret_cast<float*>(Vs + (size_t)ST * D);    // [gs][D]
+  double* lg = reinterpret_cast<double*>(qs + gs * D);          // [gs][ST]
+  float* w = reinterpret_cast<float*>(lg + gs * ST);            // [gs][ST]
+  double* ml = reinterpret_cast<double*>(w + gs * ST);          // [2][gs]
+  const int64_t slot = (int64_t)u * p.ns + split;
+  double* pm = p.pm + slot * gs;
+  double* pl = p.pl + slot * gs;
+  float* po = p.po + slot * gs * D;
+  if (nt == 0) {
+    for (int i = threadIdx.x; i < gs * D; i += blockDim.x) po[i] = 0.f;
+    if (threadIdx.x < gs) { pm[threadIdx.x] = -INFINITY; pl[threadIdx.x] = 0.0; }
+    return;
+  }
+  const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
+  const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
+  const bool appending = p.k_new != nullptr;
+  if (threadIdx.x == 0) {
+    bar_init(bar, 1);
+    bar_expect(bar, (uint32_t)(2 * nt * RB));
+    // contiguous runs of ids: [i0, n_init) and the ring part
+    int64_t i = i0;
+    const int64_t i1 = i0 + nt;
+    while (i < i1) {
+      const int64_t id = span.id(i);
+      int64_t run_end = (i < span.n_init) ? min(i1, span.n_init) : i1;
+      int64_t n = run_end - i;
+      // the token appended by this step comes from the caller's buffer
+      const bool has_new = appending && id <= t0 && t0 < id + n;
+      if (has_new) n = t0 - id;  // rows before the new token
+      if (n > 0) {
+        bulk_g2s(Ks + (size_t)(i - i0) * D, keys + id * D, (uint32_t)(n * RB), bar);
+        bulk_g2s(Vs + (size_t)(i - i0) * D, vals + id * D, (uint32_t)(n * RB), bar);
+      }
+      if (has_new) {
+        const int64_t at = i + n - i0;
+        bulk_g2s(Ks + (size_t)at * D, static_cast<const T*>(p.k_new) + (int64_t)u * D, RB, bar);
+        bulk_g2s(Vs + (size_t)at * D, static_cast<const T*>(p.v_new) + (int64_t)u * D, RB, bar);
+        n += 1;
+      }
+      i += n;
+    }
+  }
+  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
+  for (int k = threadIdx.x; k < gs * D; k += blockDim.x) qs[k] = to_f(q[k]);
+  __syncthreads();
+  bar_wait(bar, 0);
+  const double scale = 1.0 / sqrt((double)D);
+  // logits: pair (t, j), consecutive threads -> consecutive tokens
+  for (int pr = threadIdx.x; pr < nt * gs; pr += blockDim.x) {
+    const int t = pr % nt, j = pr / nt;
+    double dot, nrm;
+    row_dot<T, D, false>(qs + j * D, Ks + (size_t)t * D, t, dot, nrm);
+    lg[j * ST + t] = dot * scale;
+  }
+  __syncthreads();
+  // per-head max / exp weights / denominators: one warp per head
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < gs; j += nw) {
+    double m = -INFINITY;
+    for (int t = lane; t < nt; t += 32) m = fmax(m, lg[j * ST + t]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    double l = 0.0;
+    for (int t = lane; t < nt; t += 32) {
+      const double e = exp(lg[j * ST + t] - m);
+      w[j * ST + t] = (float)e;
+      l += e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) { ml[j] = m; ml[gs + j] = l; }
+  }
+  __syncthreads();
+  // o[j][e] = sum_t w[j][t] * V[t][e]; a thread owns two adjacent elements
+  for (int pr = threadIdx.x; pr < gs * (D / 2); pr += blockDim.x) {
+    const int j = pr / (D / 2), e = 2 * (pr % (D / 2));
+    float a0 = 0.f, a1 = 0.f;
+    const float* wj = w + j * ST;
+    for (int t = 0; t < nt; ++t) {
+      const T* vr = Vs + (size_t)t * D + e;
+      a0 = fmaf(wj[t], to_f(vr[0]), a0);
+      a1 = fmaf(wj[t], to_f(vr[1]), a1);
+    }
+    po[j * D + e] = a0;
+    po[j * D + e + 1] = a1;
+  }
+  if (threadIdx.x < gs) {
+    pm[threadIdx.x] = ml[threadIdx.x];
+    pl[threadIdx.x] = ml[gs + threadIdx.x];
+  }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t bar;
   const int64_t t0 = p.total ? *p.total : p.id_bound;
   const bool appending = p.k_new != nullptr;
   const int64_t total = t0 + (appending ? 1 : 0);
   const int ncos = p.do_cos ? p.U * p.cos_blocks_per_unit : 0;
-  if ((int)blockIdx.x < ncos) {
-    cos_block<T, D>(p, blockIdx.x, smem);
-  } else {
-    const int sb = blockIdx.x - ncos;
-    const int u = sb / p.ns, split = sb % p.ns;
-    const StaticSpan span(total, p.init_len, p.local_len);
-    const int64_t i0 = (int64_t)split * kStaticSplit;
-    const int ntok = (int)max((int64_t)0, min((int64_t)kStaticSplit, span.n_static - i0));
-    const int64_t slot = (int64_t)u * p.ns + split;
-    attn_partial_block<T, D>(
-        p, u, ntok, [&](int t) { return span.id(i0 + t); }, appending ? t0 : -1, total,
-        p.pm + slot * p.gs, p.pl + slot * p.gs, p.po + slot * p.gs * D, smem);
-  }
+  if ((int)blockIdx.x < ncos)
+    cos_task<T, D>(p, blockIdx.x, smem, &bar);
+  else
+    static_task<T, D>(p, blockIdx.x - ncos, t0, total, smem, &bar);
   if (appending && blockIdx.x == 0) {
-    // KvStore.append: new rows land at index t0 (ck/store.py:125-128)
     T* keys = static_cast<T*>(const_cast<void*>(p.keys));
     T* vals = static_cast<T*>(const_cast<void*>(p.values));
     const T* kn = static_cast<const T*>(p.k_new);
     const T* vn = static_cast<const T*>(p.v_new);
     for (int64_t i = threadIdx.x; i < (int64_t)p.U * D; i += blockDim.x) {
-      const int64_t u = i / D, e = i % D;
-      keys[(u * p.cap + t0) * D + e] = kn[i];
-      vals[(u * p.cap + t0) * D + e] = vn[i];
+      const int64_t uu = i / D, e = i % D;
+      keys[(uu * p.cap + t0) * D + e] = kn[i];
+      vals[(uu * p.cap + t0) * D + e] = vn[i];
     }
   }
+}
+
+template <typename T, int D>
+size_t scan2_smem(int gs) {
+  constexpr int RB = D * int(sizeof(T));
+  constexpr int ST = static_tok<T>();
+  const size_t cosb = (size_t)kScanRowsV2 * RB + sizeof(float) * gs * D + sizeof(double) * gs +
+                      sizeof(double) * kScanRowsV2;
+  const size_t stb = (size_t)2 * ST * RB + sizeof(float) * gs * D + sizeof(double) * gs * ST +
+                     sizeof(float) * gs * ST + sizeof(double) * 2 * gs;
+  return cosb > stb ? cosb : stb;
 }
 
 // ------------------------------------------------------------------------
@@ -468,7 +605,7 @@ __device__ double block_sum_f64(double x, double* scratch) {
 template <typename T, int D>
 __global__ void __launch_bounds__(kUnitThreads, 1) unit_kernel(DecodeParams p) {
   using R = Row<T, D>;
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   UnitSmem S;
   unit_smem_layout(p, D, &S, smem);
   const int u = blockIdx.x;
@@ -535,10 +672,13 @@ __global__ void __launch_bounds__(kUnitThreads, 1) unit_kernel(DecodeParams p) {
       int tot_kept;
       int pos = L + block_exclusive_scan(cnt, &tot_kept, S.scratch);
       for (int e = 0; e < per; ++e)
-        if (keep_mask & (1 << e)) S.rec[pos++] = ids[e];
+        if (keep_mask & (1 << e)) S.rec[pos++] = row[tid * per + e];
       __syncthreads();  // every test of list j precedes any set of list j
       for (int e = 0; e < per; ++e)
-        if (keep_mask & (1 << e)) atomicOr(&S.bitmap[ids[e] >> 5], 1u << (ids[e] & 31));
+        if (keep_mask & (1 << e)) {
+          const int id = row[tid * per + e];
+          atomicOr(&S.bitmap[id >> 5], 1u << (id & 31));
+        }
       L += tot_kept;
       __syncthreads();
     }
@@ -733,12 +873,362 @@ __global__ void __launch_bounds__(kUnitThreads, 1) unit_kernel(DecodeParams p) {
 }
 
 // ------------------------------------------------------------------------
+// v2 fused unit kernel (bf16): a 2-CTA cluster per (b, g) unit.  Both CTAs
+// redundantly pick the C' slots and build the union (cheap, deterministic);
+// each computes the rerank logits of half the recalled positions and writes
+// the packed (score, position) keys into both CTAs' shared memory (DSMEM);
+// both sort; rank 1 applies the FIFO DCU while the pair splits the sparse
+// attention, rank 1 ships its partial to rank 0 over DSMEM, and rank 0
+// merges it with the static partials and writes the output.
+// ------------------------------------------------------------------------
+
+constexpr int kU2Threads = 512;
+constexpr int kU2Warps = kU2Threads / 32;
+
+struct U2Smem {
+  int32_t* sel;
+  uint32_t* bitmap;
+  int32_t* rec;
+  uint64_t* skey;
+  float* wts;
+  float* red;
+  float* xo;       // rank 1 -> rank 0: o [gs][D]
+  double* xml;     // rank 1 -> rank 0: m, l [2][gs]
+  double* scratch;
+};
+
+__host__ __device__ inline int u2_npad(int lmax) {
+  const int n = next_pow2(lmax > 1 ? lmax : 1);
+  return n < kU2Threads ? kU2Threads : n;
+}
+
+__host__ __device__ inline size_t u2_layout(const DecodeParams& p, int D, U2Smem* s,
+                                            unsigned char* base) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    unsigned char* ptr = base ? base + off : nullptr;
+    off += align16(bytes);
+    return ptr;
+  };
+  U2Smem t;
+  t.sel = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (p.c_prime > 1 ? p.c_prime : 1)));
+  t.bitmap = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * p.bitmap_words));
+  t.rec = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (p.lmax > 1 ? p.lmax : 1)));
+  t.skey = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * u2_npad(p.lmax)));
+  t.wts = reinterpret_cast<float*>(take(sizeof(float) * p.gs * kAttnChunk));
+  t.red = reinterpret_cast<float*>(take(sizeof(float) * kU2Warps * p.gs * D));
+  t.xo = reinterpret_cast<float*>(take(sizeof(float) * p.gs * D));
+  t.xml = reinterpret_cast<double*>(take(sizeof(double) * 2 * p.gs));
+  t.scratch = reinterpret_cast<double*>(take(sizeof(double) * 128));
+  if (s) *s = t;
+  return off;
+}
+
+size_t unit2_smem_bytes(const DecodeParams& p, int D) { return u2_layout(p, D, nullptr, nullptr); }
+
+template <int IPT>
+__device__ void sort_keys(uint64_t* skey) {
+  uint64_t k[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) k[i] = skey[threadIdx.x * IPT + i];
+  bitonic_regs<IPT>(k, skey);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) skey[threadIdx.x * IPT + i] = k[i];
+  __syncthreads();
+}
+
+template <typename T, int D>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
+    unit2_kernel(DecodeParams p) {
+  namespace cg = cooperative_groups;
+  using R = Row<T, D>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  U2Smem S;
+  u2_layout(p, D, &S, smem);
+  const int u = blockIdx.x >> 1;
+  const int bi = u / p.g, gi = u % p.g, gs = p.gs;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t t0 = *p.total;
+  const bool appending = p.k_new != nullptr;
+  const int64_t total = t0 + (appending ? 1 : 0);
+  __shared__ int64_t s_slot;
+  __shared__ float qs[kMaxGroup * D];
+  __shared__ double ms[kMaxGroup], ls[kMaxGroup];
+  if (tid == 0) s_slot = p.fifo ? (p.fifo[bi] % p.C) : 0;
+  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
+  for (int i = tid; i < gs * D; i += blockDim.x) qs[i] = to_f(q[i]);
+
+  // ---- 1. top-C' slots (both ranks; deterministic) -----------------------
+  {
+    uint64_t prev_key = ~0ull;
+    int prev_idx = -1;
+    const double* gc = p.gcos + (int64_t)u * p.C;
+    for (int r = 0; r < p.c_prime; ++r) {
+      uint64_t bk = 0;
+      int bidx = INT32_MAX;
+      for (int i = tid; i < p.C; i += blockDim.x) {
+        const uint64_t k = okey64(gc[i]);
+        const bool below = k < prev_key || (k == prev_key && i > prev_idx);
+        if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
+      }
+      const int w = block_argmax(bk, bidx, S.scratch);
+      if (tid == 0) S.sel[r] = w;
+      prev_idx = w;
+      prev_key = okey64(gc[w]);
+    }
+    __syncthreads();
+  }
+  // ---- 2. union, first occurrence kept (both ranks) -----------------------
+  int L = 0;
+  {
+    const int nwords = (int)((total + 31) >> 5);
+    for (int i = tid; i < nwords; i += blockDim.x) S.bitmap[i] = 0u;
+    __syncthreads();
+    const int per = (p.rho + blockDim.x - 1) / blockDim.x;
+    for (int j = 0; j < p.c_prime; ++j) {
+      const int32_t* row = p.lists + ((int64_t)u * p.C + S.sel[j]) * p.rho;
+      int keep_mask = 0, cnt = 0;
+      for (int e = 0; e < per; ++e) {
+        const int i = tid * per + e;
+        int id = (i < p.rho) ? row[i] : kEmpty;
+        if (id != kEmpty && (id < 0 || id >= total)) {
+          set_flag(p.flags, kFlagIdRange);
+          id = kEmpty;
+        }
+        if (id != kEmpty && !((S.bitmap[id >> 5] >> (id & 31)) & 1u)) {
+          keep_mask |= 1 << e;
+          ++cnt;
+        }
+      }
+      int tot_kept;
+      int pos = L + block_exclusive_scan(cnt, &tot_kept, S.scratch);
+      for (int e = 0; e < per; ++e)
+        if (keep_mask & (1 << e)) S.rec[pos++] = row[tid * per + e];
+      __syncthreads();
+      for (int e = 0; e < per; ++e)
+        if (keep_mask & (1 << e)) {
+          const int id = row[tid * per + e];
+          atomicOr(&S.bitmap[id >> 5], 1u << (id & 31));
+        }
+      L += tot_kept;
+      __syncthreads();
+    }
+  }
+  const int npad = u2_npad(L);
+  // ---- 3. rerank logits for this rank's half (row per thread) ------------
+  double* lg = p.logits + (int64_t)u * gs * p.lmax;
+  uint64_t* peer_skey = cl.map_shared_rank(S.skey, rank ^ 1);
+  {
+    const int half = (L + 1) >> 1;
+    const int lo = rank ? half : 0, hi = rank ? L : half;
+    const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
+    const double scale = 1.0 / sqrt((double)D);
+    constexpr int VPR = D * int(sizeof(T)) / 16, EPV = 16 / int(sizeof(T));
+    for (int t = lo + tid; t < hi; t += blockDim.x) {
+      const uint4* r4 = reinterpret_cast<const uint4*>(keys + (int64_t)S.rec[t] * D);
+      constexpr int KC = VPR < 8 ? VPR : 8;     // 16-byte chunks held in registers at once
+      double gmax = -INFINITY;
+#pragma unroll 1
+      for (int h0 = 0; h0 < gs; h0 += 8) {      // heads in groups of 8: registers, not local memory
+        double acc[8];
+#pragma unroll
+        for (int hh = 0; hh < 8; ++hh) acc[hh] = 0.0;
+#pragma unroll 1
+        for (int k0 = 0; k0 < VPR; k0 += KC) {
+          uint4 raw[KC];
+#pragma unroll
+          for (int k = 0; k < KC; ++k) raw[k] = ldg16(r4 + k0 + k);
+#pragma unroll
+          for (int k = 0; k < KC; ++k) {
+            float x[EPV];
+            unpack16<T>(raw[k], x);
+#pragma unroll
+            for (int hh = 0; hh < 8; ++hh) {
+              if (h0 + hh < gs) {
+                const float* qh = qs + (h0 + hh) * D + (k0 + k) * EPV;
+                float pd = 0.f;
+#pragma unroll
+                for (int j = 0; j < EPV; ++j) pd = fmaf(qh[j], x[j], pd);
+                acc[hh] += (double)pd;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int hh = 0; hh < 8; ++hh) {
+          if (h0 + hh < gs) {
+            const double a = acc[hh] * scale;
+            lg[(int64_t)(h0 + hh) * p.lmax + t] = a;
+            gmax = fmax(gmax, a);
+          }
+        }
+      }
+      const uint64_t key = ((uint64_t)(~okey32((float)gmax)) << 32) | (uint32_t)t;
+      S.skey[t] = key;
+      peer_skey[t] = key;
+    }
+    for (int t = L + tid; t < npad; t += blockDim.x) S.skey[t] = ~0ull;
+  }
+  cl.sync();  // both halves of the keys (and of the logits in global) are in place
+
+  // ---- 4. order by (score desc, recall position asc) ---------------------
+  if (L > 0) {
+    switch (npad) {
+      case 512: sort_keys<1>(S.skey); break;
+      case 1024: sort_keys<2>(S.skey); break;
+      case 2048: sort_keys<4>(S.skey); break;
+      case 4096: sort_keys<8>(S.skey); break;
+      default: sort_keys<16>(S.skey); break;
+    }
+  }
+  auto pos_at = [&](int i) { return (int)(uint32_t)(S.skey[i] & 0xffffffffu); };
+
+  // ---- 5. FIFO DCU (rank 1) -------------------------------------------------
+  const bool dcu_here = (p.stages & kStageDcu) && L > 0;
+  if (rank == 1 && dcu_here) {
+    const int64_t slot = s_slot;
+    int32_t* row = p.lists + ((int64_t)u * p.C + slot) * p.rho;
+    const int keep = min(p.rho, L);
+    for (int i = tid; i < p.rho; i += blockDim.x) row[i] = i < keep ? S.rec[pos_at(i)] : kEmpty;
+    T* cent = static_cast<T*>(p.cent);
+    for (int i = tid; i < gs * D; i += blockDim.x) {
+      const int hh = i / D, e = i % D;
+      cent[(((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D + e] = q[i];
+    }
+  }
+  // ---- 6. sparse attention over this rank's share of the sparse set -------
+  const int Rn = (L > 0) ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
+  auto pos_of = [&](int i) { return p.use_rerank ? pos_at(i) : i; };
+  const int r0 = (Rn + 1) >> 1;
+  const int my_lo = rank ? r0 : 0, my_n = rank ? Rn - r0 : r0;
+  {
+    for (int hh = 0; hh < gs; ++hh) {
+      double m = -INFINITY;
+      for (int i = tid; i < my_n; i += blockDim.x) m = fmax(m, lg[(int64_t)hh * p.lmax + pos_of(my_lo + i)]);
+      m = block_max_f64(m, S.scratch);
+      if (tid == 0) { ms[hh] = m; ls[hh] = 0.0; }
+    }
+    for (int i = tid; i < kU2Warps * gs * D; i += blockDim.x) S.red[i] = 0.f;
+    __syncthreads();
+    const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
+    for (int c0 = 0; c0 < my_n; c0 += kAttnChunk) {
+      const int n = min(kAttnChunk, my_n - c0);
+      for (int hh = 0; hh < gs; ++hh) {
+        double lp = 0.0;
+        for (int i = tid; i < n; i += blockDim.x) {
+          const double e = exp(lg[(int64_t)hh * p.lmax + pos_of(my_lo + c0 + i)] - ms[hh]);
+          S.wts[hh * kAttnChunk + i] = (float)e;
+          lp += e;
+        }
+        lp = block_sum_f64(lp, S.scratch);
+        if (tid == 0) ls[hh] += lp;
+      }
+      __syncthreads();
+      accum_weighted_rows<T, D>(
+          n, gs, [&](int t) -> const T* { return vals + (int64_t)S.rec[pos_of(my_lo + c0 + t)] * D; },
+          [&](int hh, int t) { return S.wts[hh * kAttnChunk + t]; }, S.red + (int64_t)warp * gs * D);
+      __syncthreads();
+    }
+    // this rank's partial: o [gs][D] (unnormalised), m, l
+    float* xo = rank ? cl.map_shared_rank(S.xo, 0) : S.xo;
+    double* xml = rank ? cl.map_shared_rank(S.xml, 0) : S.xml;
+    if (rank == 1) {
+      for (int i = tid; i < gs * D; i += blockDim.x) {
+        float s = 0.f;
+        for (int w = 0; w < kU2Warps; ++w) s += S.red[(int64_t)w * gs * D + i];
+        xo[i] = s;
+      }
+      if (tid < gs) { xml[tid] = ms[tid]; xml[gs + tid] = ls[tid]; }
+    }
+  }
+  cl.sync();  // rank 1's partial has landed in rank 0's shared memory
+  if (rank == 1) return;
+
+  // ---- 7. rank 0: merge sparse halves + static partials -> output ---------
+  bool none = false;
+  const int64_t pbase = (int64_t)u * p.ns;
+  for (int i = tid; i < gs * D; i += blockDim.x) {
+    const int hh = i / D, e = i % D;
+    float o0 = 0.f;
+    for (int w = 0; w < kU2Warps; ++w) o0 += S.red[(int64_t)w * gs * D + i];
+    double M = -INFINITY;
+    if (ls[hh] > 0.0) M = ms[hh];
+    if (S.xml[gs + hh] > 0.0) M = fmax(M, S.xml[hh]);
+    for (int j = 0; j < p.ns; ++j)
+      if (p.pl[(pbase + j) * gs + hh] > 0.0) M = fmax(M, p.pm[(pbase + j) * gs + hh]);
+    double Ls = 0.0, O = 0.0;
+    if (ls[hh] > 0.0) {
+      const double w = exp(ms[hh] - M);
+      Ls += w * ls[hh];
+      O += w * (double)o0;
+    }
+    if (S.xml[gs + hh] > 0.0) {
+      const double w = exp(S.xml[hh] - M);
+      Ls += w * S.xml[gs + hh];
+      O += w * (double)S.xo[i];
+    }
+    for (int j = 0; j < p.ns; ++j) {
+      const double lj = p.pl[(pbase + j) * gs + hh];
+      if (lj > 0.0) {
+        const double w = exp(p.pm[(pbase + j) * gs + hh] - M);
+        Ls += w * lj;
+        O += w * (double)p.po[((pbase + j) * gs + hh) * D + e];
+      }
+    }
+    const int64_t oh = (int64_t)bi * p.h + gi * gs + hh;
+    if (Ls > 0.0) {
+      p.out[oh * D + e] = (float)(O / Ls);
+    } else {
+      p.out[oh * D + e] = 0.f;
+      none = true;
+    }
+    if (e == 0) {
+      if (p.row_max) p.row_max[oh] = M;
+      if (p.denom) p.denom[oh] = Ls;
+    }
+  }
+  if (none) set_flag(p.flags, kFlagNoTokens);
+  if (p.selected)
+    for (int r = tid; r < p.c_prime; r += blockDim.x) p.selected[(int64_t)u * p.c_prime + r] = S.sel[r];
+  if (p.recall_len && tid == 0) p.recall_len[u] = L;
+  if (tid == 0) set_flag(p.flags, L > 0 ? kFlagNonEmptyRecall : kFlagEmptyRecall);
+  if (p.sparse_ids)
+    for (int i = tid; i < p.sparse_cap; i += blockDim.x)
+      p.sparse_ids[(int64_t)u * p.sparse_cap + i] = i < Rn ? S.rec[pos_of(i)] : kEmpty;
+  if (p.sparse_len && tid == 0) p.sparse_len[u] = Rn;
+
+  // ---- 8. completion: FIFO cursor advance + total++ by the last unit -------
+  if (p.stages & (kStageDcu | kStageAppendTail)) {
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (dcu_here) atomicAdd(&p.sync[1 + bi], 1);
+      __threadfence();
+      const int prev = atomicAdd(&p.sync[0], 1);
+      if (prev == p.U - 1) {
+        __threadfence();
+        for (int b2 = 0; b2 < p.b; ++b2) {
+          const int hits = atomicExch(&p.sync[1 + b2], 0);
+          if (hits > 0) p.fifo[b2] = p.fifo[b2] % p.C + 1;
+        }
+        if (appending) *p.total = t0 + 1;
+        atomicExch(&p.sync[0], 0);
+        __threadfence();
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
 // generic id-list attention: split partials + merge (sparse_attention API)
 // ------------------------------------------------------------------------
 
 template <typename T, int D>
 __global__ void __launch_bounds__(kScanThreads) attn_split_kernel(DecodeParams p) {
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   const int64_t total = *p.total;
   const int per_unit = p.ns;  // splits per unit (list splits first, then static)
   const int u = blockIdx.x / per_unit, split = blockIdx.x % per_unit;
@@ -837,10 +1327,28 @@ size_t scan_smem_bytes(const DecodeParams& p, int D) {
 
 template <typename T, int D>
 static int launch_scan_t(const DecodeParams& p, int nblocks, cudaStream_t st) {
-  const size_t sm = scan_smem_bytes(p, D);
-  auto k = scan_kernel<T, D>;
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (nblocks > 0) k<<<nblocks, kScanThreads, sm, st>>>(p);
+  const size_t sm = scan2_smem<T, D>(p.gs);
+  auto k = scan2_kernel<T, D>;
+  static size_t configured = 0;
+  if (sm > 48 * 1024 && sm > configured) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = sm;
+  }
+  if (nblocks > 0) k<<<nblocks, kScanRowsV2, sm, st>>>(p);
+  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+}
+
+template <typename T, int D>
+static int launch_unit2_t(const DecodeParams& p, cudaStream_t st) {
+  const size_t sm = unit2_smem_bytes(p, D);
+  if (sm > 200 * 1024) return CTKV_ECONFIG;
+  auto k = unit2_kernel<T, D>;
+  static size_t configured = 0;
+  if (sm > configured) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = sm;
+  }
+  k<<<2 * p.U, kU2Threads, sm, st>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
 
@@ -893,6 +1401,16 @@ int launch_scan(const DecodeParams& p, int dtype, int D, int nblocks, cudaStream
 int launch_unit(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
   return CTKV_DISPATCH(dtype, D, launch_unit_t, p, st);
 }
+int launch_unit2(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
+  if (dtype != CTKV_BF16) return CTKV_ECONFIG;
+  switch (D) {
+    case 64: return launch_unit2_t<__nv_bfloat16, 64>(p, st);
+    case 128: return launch_unit2_t<__nv_bfloat16, 128>(p, st);
+    case 256: return launch_unit2_t<__nv_bfloat16, 256>(p, st);
+  }
+  return CTKV_ESHAPE;
+}
+int static_tok_for(int dtype) { return dtype == CTKV_BF16 ? static_tok<__nv_bfloat16>() : static_tok<float>(); }
 int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
   return CTKV_DISPATCH(dtype, D, launch_attn_t, p, st);
 }

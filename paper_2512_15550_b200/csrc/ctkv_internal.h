@@ -78,6 +78,9 @@ size_t scan_smem_bytes(const DecodeParams& p, int D);
 size_t unit_smem_bytes(const DecodeParams& p, int D);
 int launch_scan(const DecodeParams& p, int dtype, int D, int nblocks, cudaStream_t st);
 int launch_unit(const DecodeParams& p, int dtype, int D, cudaStream_t st);
+int launch_unit2(const DecodeParams& p, int dtype, int D, cudaStream_t st);
+size_t unit2_smem_bytes(const DecodeParams& p, int D);
+int static_tok_for(int dtype);
 int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const double* la,
                   const float* ob, const double* mb, const double* lb, float* out, double* mo,
