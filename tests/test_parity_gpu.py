@@ -168,21 +168,41 @@ def test_cfg1_bf16_fast_build_within_tie_window():
 
 
 def test_cfg1_bf16_decode_recall_parity():
-    """bf16 decode vs the reference's sparse sets on the same inputs:
-    >= 90% top-k recall parity is the north-star bar; f64 selection
-    arithmetic makes it exact here unless the build lists differ."""
+    """bf16 fused decode (f32-chunk exact-product logits, 2-CTA cluster unit
+    kernel) vs the oracle on the same bf16-rounded inputs, step by step:
+    sparse sets equal except swaps inside the 1e-6 tie window of the
+    reference's own f64 scores; recall parity >= 0.999 (north-star bar: 0.9);
+    outputs within 1e-3."""
     meta, arr = G.load("cfg1_bf16")
     _, p, flags, (q, k, v), store, index = _prefill("cfg1_bf16", mode=0, dtype=torch.bfloat16,
                                                     reserve=meta["steps"])
     s, T = meta["drift"]["s"], meta["steps"]
-    cfg = P.DecodeConfig(p["c_prime"], p["rho_prime"])
+    cfg = P.DecodeConfig(p["c_prime"], p["rho_prime"], keep_sets=True)
     outs, trace = P.run_decode(store, index, cfg, np.ascontiguousarray(q[:, :, s:s + T]),
                                np.ascontiguousarray(k[:, :, s:s + T]),
                                np.ascontiguousarray(v[:, :, s:s + T]))
-    match = sum(tr.sparse_digest == meta["digests"][t] for t, tr in enumerate(trace))
-    assert match == T
+    ost, oidx = O.prefill(np.ascontiguousarray(q[:, :, :s]), np.ascontiguousarray(k[:, :, :s]),
+                          np.ascontiguousarray(v[:, :, :s]), p["init_len"], p["local_len"],
+                          p["capacity"], p["rho"])
+    _, recs = O.run_decode(ost, oidx, q[:, :, s:s + T], k[:, :, s:s + T], v[:, :, s:s + T],
+                           p["c_prime"], p["rho_prime"])
+    hits = total = hard = exact_steps = 0
     for t in range(T):
         assert nrel(outs[:, :, t], arr["step_out"][t]) < 1e-3
+        exact_steps += trace[t].sparse_digest == meta["digests"][t]
+        r = recs[t]
+        for gi in range(8):
+            mine, ref = set(trace[t].sparse[0][gi].tolist()), set(r.sparse[0][gi].tolist())
+            hits += len(mine & ref)
+            total += len(ref)
+            if mine != ref:
+                ids = np.asarray(r.recalled[0][gi])
+                sc = dict(zip(ids.tolist(), np.asarray(r.grouped[0][gi]).tolist()))
+                kth = sorted(sc.values(), reverse=True)[p["rho_prime"] - 1]
+                hard += any(abs(sc.get(i, -np.inf) - kth) > TIE_REL * abs(kth) for i in mine ^ ref)
+    assert hard == 0
+    assert hits / total >= 0.999
+    assert exact_steps >= T - 2     # order differs only at f32-resolution ties
 
 
 # ---------------------------------------------------------------------------
