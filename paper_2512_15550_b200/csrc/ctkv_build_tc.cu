@@ -396,6 +396,21 @@ __global__ void __launch_bounds__(256) kth_value_kernel(const float* __restrict_
   if (threadIdx.x == 0) thr[blockIdx.x] = okey32_inv(prefix);
 }
 
+template <int IPT>
+__device__ void select_sort(const uint64_t* src, int cnt, uint64_t* cs) {
+  uint64_t k[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int e = threadIdx.x * IPT + i;
+    k[i] = e < cnt ? src[e] : ~0ull;
+  }
+  bitonic_regs<IPT>(k, cs);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) cs[threadIdx.x * IPT + i] = k[i];
+  __syncthreads();
+}
+
 // per row: exact top-rho of the candidates (sorted), or flag for fallback
 __global__ void __launch_bounds__(512) select_kernel(const uint64_t* __restrict__ cand,
                                                      const int32_t* __restrict__ counts, int cap,
@@ -409,9 +424,17 @@ __global__ void __launch_bounds__(512) select_kernel(const uint64_t* __restrict_
     if (threadIdx.x == 0) fail_rows[atomicAdd(fail_n, 1)] = (int32_t)row;
     return;
   }
-  const int np = next_pow2(max(cnt, 1));
-  for (int i = threadIdx.x; i < np; i += blockDim.x) cs[i] = i < cnt ? cand[row * cap + i] : ~0ull;
-  bitonic_sort_u64(cs, np);
+  int np = next_pow2(max(cnt, 1));
+  if (np < 512) np = 512;
+  const uint64_t* src = cand + row * cap;
+  // register/shuffle bitonic: strides inside a warp never touch shared memory
+  switch (np) {
+    case 512: select_sort<1>(src, cnt, cs); break;
+    case 1024: select_sort<2>(src, cnt, cs); break;
+    case 2048: select_sort<4>(src, cnt, cs); break;
+    case 4096: select_sort<8>(src, cnt, cs); break;
+    default: select_sort<16>(src, cnt, cs); break;
+  }
   int32_t* dst = lists + row * rho;
   for (int i = threadIdx.x; i < rho; i += blockDim.x) dst[i] = (int32_t)(cs[i] & 0xffffffffu) + add;
 }
@@ -624,7 +647,7 @@ int build_tc(const BuildParams& p, int /*dtype*/, void* ws, size_t ws_bytes, cud
   if (int rc = launch_gemm(mapK, mapC, gp, katoms, st)) return rc;
   // 4. select
   cudaMemsetAsync(fail_n, 0, sizeof(int32_t), st);
-  const size_t sel_smem = (size_t)pl.cap * 8;
+  const size_t sel_smem = (size_t)std::max(pl.cap, 512) * 8;
   cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
   select_kernel<<<(unsigned)(U * p.C), 512, sel_smem, st>>>(cand, counts, pl.cap, p.rho, p.C,
                                                             p.lists, (int32_t)p.off_begin, fail_n,

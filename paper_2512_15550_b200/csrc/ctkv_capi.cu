@@ -47,10 +47,18 @@ struct DecodeWs {
   double* pl;
   float* po;
   double* logits;
+  double* cval;
+  int32_t* cidx;
   size_t bytes;
 };
 
-DecodeWs carve_decode(const ctkv_layout* L, int C, int lmax, int ns, void* base) {
+// chunk-local top-C' candidates the fused scan writes: [U][C / (256/gs)][min(C', 256/gs)]
+int ncand_for(const ctkv_layout* L, int c_prime) {
+  const int cc = 256 / (L->query_heads / L->kv_heads);
+  return c_prime < cc ? c_prime : cc;
+}
+
+DecodeWs carve_decode(const ctkv_layout* L, int C, int lmax, int ns, void* base, int c_prime = 0) {
   const int U = L->batch * L->kv_heads;
   const int gs = L->query_heads / L->kv_heads;
   const int d = L->head_dim;
@@ -66,6 +74,11 @@ DecodeWs carve_decode(const ctkv_layout* L, int C, int lmax, int ns, void* base)
   w.pl = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * std::max(ns, 1) * gs));
   w.po = reinterpret_cast<float*>(take(sizeof(float) * (size_t)U * std::max(ns, 1) * gs * d));
   w.logits = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * gs * std::max(lmax, 1)));
+  const int cc = 256 / gs;
+  const size_t ncand_total =
+      c_prime > 0 ? (size_t)U * ((std::max(C, 1) + cc - 1) / cc) * ncand_for(L, c_prime) : 1;
+  w.cval = reinterpret_cast<double*>(take(sizeof(double) * ncand_total));
+  w.cidx = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * ncand_total));
   w.bytes = off;
   return w;
 }
@@ -173,7 +186,7 @@ int ctkv_build_lists(const ctkv_layout* L, const void* centroids, const void* ke
 size_t ctkv_decode_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32_t rho,
                                    int32_t c_prime, int32_t) {
   if (check_layout(L)) return 0;
-  return carve_decode(L, capacity, c_prime * rho, static_slots(L), nullptr).bytes;
+  return carve_decode(L, capacity, c_prime * rho, static_slots(L), nullptr, c_prime).bytes;
 }
 
 int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctkv_step_args* A,
@@ -196,7 +209,7 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   if (A->k_new && !I.sync) return CTKV_ECONFIG;
   const int ns = static_slots(L);
   const int lmax = A->c_prime * I.rho;
-  DecodeWs w = carve_decode(L, I.capacity, lmax, ns, workspace);
+  DecodeWs w = carve_decode(L, I.capacity, lmax, ns, workspace, A->c_prime);
   if (w.bytes > workspace_bytes) return CTKV_EWORKSPACE;
   DecodeParams p;
   fill_layout(p, L);
@@ -226,6 +239,9 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.pl = w.pl;
   p.po = w.po;
   p.logits = w.logits;
+  p.cval = w.cval;
+  p.cidx = w.cidx;
+  p.ncand = ncand_for(L, A->c_prime);
   p.out = A->out;
   p.row_max = A->row_max;
   p.denom = A->denom;
@@ -236,7 +252,9 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.sparse_cap = A->sparse_ids ? A->sparse_cap : 0;
   p.flags = A->flags;
   // bf16: 2-CTA cluster unit kernel (f32-chunked logits); f32: exact f64 unit kernel
-  const bool v2 = L->dtype == CTKV_BF16 && L->head_dim >= 64 && unit2_smem_bytes(p, L->head_dim) <= 200 * 1024;
+  const bool v2 = L->dtype == CTKV_BF16 && L->head_dim >= 64 && p.gs <= 8 && I.rho <= 4096 &&
+                  unit2_smem_bytes(p, L->head_dim) <= 200 * 1024;
+  if (!v2) p.cval = nullptr;   // the f64 unit kernel selects from gcos directly
   if (!v2 && unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;

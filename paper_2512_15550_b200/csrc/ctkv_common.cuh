@@ -176,6 +176,24 @@ __device__ __forceinline__ void set_flag(int32_t* flags, int32_t bit) {
   if (flags) atomicOr(flags, bit);
 }
 
+// ---- bf16 x bf16 -> f32 mixed-precision FMA (sm_100 FHFMA.BF16) -----------
+// acc + sum_i q_i * x_i over the 8 bf16 lanes of a 16-byte chunk; every
+// product is exact and every add rounds once to f32, exactly like
+// unpack-to-f32 + FFMA, without the unpack instructions.
+__device__ __forceinline__ float bf16x8_dot(const uint4& q, const uint4& x, float acc) {
+  const uint32_t qa[4] = {q.x, q.y, q.z, q.w}, xa[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    asm("{.reg .b16 ql, qh, xl, xh;\n\t"
+        "mov.b32 {ql, qh}, %1;\n\t"
+        "mov.b32 {xl, xh}, %2;\n\t"
+        "fma.rn.f32.bf16 %0, ql, xl, %0;\n\t"
+        "fma.rn.f32.bf16 %0, qh, xh, %0;}"
+        : "+f"(acc)
+        : "r"(qa[i]), "r"(xa[i]));
+  return acc;
+}
+
 // ---- async-proxy helpers (mbarrier + TMA bulk copies) ----------------------
 
 __device__ __forceinline__ uint32_t sa(const void* p) {

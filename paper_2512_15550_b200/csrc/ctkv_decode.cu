@@ -241,35 +241,32 @@ template <> struct Prec<__nv_bfloat16> { static constexpr bool kChunkF32 = true;
 template <> struct Prec<float> { static constexpr bool kChunkF32 = false; };
 
 // dot(q, row) and |row|^2 with rotated 16-byte chunk order (conflict-free
-// when consecutive threads own consecutive rows)
+// when consecutive threads own consecutive rows).  `q` has the row's type:
+// bf16 rows use the mixed-precision FMA on raw bf16 pairs.
 template <typename T, int D, bool kNorm>
-__device__ __forceinline__ void row_dot(const float* qv, const T* row, int rot, double& dot,
+__device__ __forceinline__ void row_dot(const T* q, const T* row, int rot, double& dot,
                                         double& nrm) {
   constexpr int EPV = 16 / int(sizeof(T));
   constexpr int VPR = D / EPV;
   const uint4* r4 = reinterpret_cast<const uint4*>(row);
+  const uint4* q4 = reinterpret_cast<const uint4*>(q);
   dot = 0.0;
   nrm = 0.0;
 #pragma unroll 4
   for (int k = 0; k < VPR; ++k) {
     const int kk = (k + rot) & (VPR - 1);
-    float x[EPV];
-    unpack16<T>(r4[kk], x);
-    const float* q = qv + kk * EPV;
+    const uint4 x = r4[kk];
     if (Prec<T>::kChunkF32) {
-      float pd = 0.f, pn = 0.f;
-#pragma unroll
-      for (int j = 0; j < EPV; ++j) {
-        pd = fmaf(q[j], x[j], pd);
-        if (kNorm) pn = fmaf(x[j], x[j], pn);
-      }
-      dot += (double)pd;
-      if (kNorm) nrm += (double)pn;
+      dot += (double)bf16x8_dot(q4[kk], x, 0.f);
+      if (kNorm) nrm += (double)bf16x8_dot(x, x, 0.f);
     } else {
+      float xf[EPV], qf[EPV];
+      unpack16<T>(x, xf);
+      unpack16<T>(q4[kk], qf);
 #pragma unroll
       for (int j = 0; j < EPV; ++j) {
-        dot = fma((double)q[j], (double)x[j], dot);
-        if (kNorm) nrm = fma((double)x[j], (double)x[j], nrm);
+        dot = fma((double)qf[j], (double)xf[j], dot);
+        if (kNorm) nrm = fma((double)xf[j], (double)xf[j], nrm);
       }
     }
   }
@@ -279,7 +276,7 @@ template <typename T>
 __host__ __device__ constexpr int static_tok() { return sizeof(T) == 2 ? 128 : 64; }
 
 template <typename T, int D>
-__device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, uint64_t* bar) {
+__device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, uint64_t* bars) {
   constexpr int RB = D * int(sizeof(T));
   const int gs = p.gs, CC = kScanRowsV2 / gs;
   const int cpu = p.cos_blocks_per_unit;
@@ -287,30 +284,36 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
   const int bi = u / p.g, gi = u % p.g;
   const int c0 = chunk * CC, nc = min(CC, p.C - c0);
   T* rows = reinterpret_cast<T*>(smem);                                   // [gs][CC][D]
-  float* qs = reinterpret_cast<float*>(smem + (size_t)kScanRowsV2 * RB);  // [gs][D]
+  T* qs = reinterpret_cast<T*>(smem + (size_t)kScanRowsV2 * RB);          // [gs][D] raw
   double* qn = reinterpret_cast<double*>(qs + gs * D);                    // [gs]
   double* cosv = qn + gs;                                                 // [gs*CC]
+  double* gv = cosv + kScanRowsV2;                                        // [CC] group max
   const T* cent = static_cast<const T*>(p.cent);
   if (threadIdx.x == 0) {
-    bar_init(bar, 1);
-    bar_expect(bar, (uint32_t)(gs * nc * RB));
-    for (int j = 0; j < gs; ++j)
+    // one barrier per head block: rows of head j are computed as soon as they land
+    for (int j = 0; j < gs; ++j) {
+      bar_init(&bars[j], 1);
+      bar_expect(&bars[j], (uint32_t)(nc * RB));
       bulk_g2s(rows + (size_t)j * CC * D, cent + (((int64_t)bi * p.h + gi * gs + j) * p.C + c0) * D,
-               (uint32_t)(nc * RB), bar);
+               (uint32_t)(nc * RB), &bars[j]);
+    }
   }
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = to_f(q[i]);
+  for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = q[i];
   __syncthreads();
   if (threadIdx.x < gs) {
     double s = 0.0;
-    for (int e = 0; e < D; ++e) s = fma((double)qs[threadIdx.x * D + e], (double)qs[threadIdx.x * D + e], s);
+    for (int e = 0; e < D; ++e) {
+      const double x = (double)to_f(qs[threadIdx.x * D + e]);
+      s = fma(x, x, s);
+    }
     qn[threadIdx.x] = sqrt(s);
   }
   __syncthreads();
-  bar_wait(bar, 0);
   for (int r = threadIdx.x; r < gs * CC; r += blockDim.x) {
     const int j = r / CC, c = r % CC;
     if (c >= nc) continue;
+    bar_wait(&bars[j], 0);
     double dot, nrm;
     row_dot<T, D, true>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
     const double den = qn[j] * sqrt(nrm);
@@ -328,6 +331,40 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
     double m = cosv[c];
     for (int j = 1; j < gs; ++j) m = fmax(m, cosv[j * CC + c]);
     p.gcos[(int64_t)u * p.C + c0 + c] = m;
+    gv[c] = m;
+  }
+  // chunk-local top-C' candidates (value desc, slot asc): the global top-C'
+  // is contained in the union of the chunks' candidates
+  if (p.cval != nullptr) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      uint64_t prev_key = ~0ull;
+      int prev_idx = -1;
+      const int64_t base = ((int64_t)u * cpu + chunk) * p.ncand;
+      for (int r = 0; r < p.ncand; ++r) {
+        uint64_t bk = 0;
+        int bidx = INT32_MAX;
+        for (int c = lane; c < nc; c += 32) {
+          const uint64_t k = okey64(gv[c]);
+          const int i = c0 + c;
+          const bool below = k < prev_key || (k == prev_key && i > prev_idx);
+          if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+          const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
+          if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
+        }
+        if (lane == 0) {
+          p.cval[base + r] = bidx == INT32_MAX ? -INFINITY : gv[bidx - c0];
+          p.cidx[base + r] = bidx;
+        }
+        prev_key = bk;
+        prev_idx = bidx;
+      }
+    }
   }
 }
 
@@ -345,7 +382,7 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
   const int nt = (int)max((int64_t)0, min((int64_t)ST, span.n_static - i0));
   T* Ks = reinterpret_cast<T*>(smem);                           // [ST][D]
   T* Vs = Ks + (size_t)ST * D;                                  // [ST][D]
-  float* qs = reinterpret_cast<float*>(Vs + (size_t)ST * D);    // [gs][D]
+  T* qs = Vs + (size_t)ST * D;                                  // [gs][D] raw
   double* lg = reinterpret_cast<double*>(qs + gs * D);          // [gs][ST]
   float* w = reinterpret_cast<float*>(lg + gs * ST);            // [gs][ST]
   double* ml = reinterpret_cast<double*>(w + gs * ST);          // [2][gs]
@@ -361,9 +398,13 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
   const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
   const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
   const bool appending = p.k_new != nullptr;
+  uint64_t* barK = bar;
+  uint64_t* barV = bar + 1;
   if (threadIdx.x == 0) {
-    bar_init(bar, 1);
-    bar_expect(bar, (uint32_t)(2 * nt * RB));
+    bar_init(barK, 1);
+    bar_init(barV, 1);
+    bar_expect(barK, (uint32_t)(nt * RB));
+    bar_expect(barV, (uint32_t)(nt * RB));
     // contiguous runs of ids: [i0, n_init) and the ring part
     int64_t i = i0;
     const int64_t i1 = i0 + nt;
@@ -375,22 +416,22 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
       const bool has_new = appending && id <= t0 && t0 < id + n;
       if (has_new) n = t0 - id;  // rows before the new token
       if (n > 0) {
-        bulk_g2s(Ks + (size_t)(i - i0) * D, keys + id * D, (uint32_t)(n * RB), bar);
-        bulk_g2s(Vs + (size_t)(i - i0) * D, vals + id * D, (uint32_t)(n * RB), bar);
+        bulk_g2s(Ks + (size_t)(i - i0) * D, keys + id * D, (uint32_t)(n * RB), barK);
+        bulk_g2s(Vs + (size_t)(i - i0) * D, vals + id * D, (uint32_t)(n * RB), barV);
       }
       if (has_new) {
         const int64_t at = i + n - i0;
-        bulk_g2s(Ks + (size_t)at * D, static_cast<const T*>(p.k_new) + (int64_t)u * D, RB, bar);
-        bulk_g2s(Vs + (size_t)at * D, static_cast<const T*>(p.v_new) + (int64_t)u * D, RB, bar);
+        bulk_g2s(Ks + (size_t)at * D, static_cast<const T*>(p.k_new) + (int64_t)u * D, RB, barK);
+        bulk_g2s(Vs + (size_t)at * D, static_cast<const T*>(p.v_new) + (int64_t)u * D, RB, barV);
         n += 1;
       }
       i += n;
     }
   }
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int k = threadIdx.x; k < gs * D; k += blockDim.x) qs[k] = to_f(q[k]);
+  for (int k = threadIdx.x; k < gs * D; k += blockDim.x) qs[k] = q[k];
   __syncthreads();
-  bar_wait(bar, 0);
+  bar_wait(barK, 0);
   const double scale = 1.0 / sqrt((double)D);
   // logits: pair (t, j), consecutive threads -> consecutive tokens
   for (int pr = threadIdx.x; pr < nt * gs; pr += blockDim.x) {
@@ -418,6 +459,7 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
     if (lane == 0) { ml[j] = m; ml[gs + j] = l; }
   }
   __syncthreads();
+  bar_wait(barV, 0);
   // o[j][e] = sum_t w[j][t] * V[t][e]; a thread owns two adjacent elements
   for (int pr = threadIdx.x; pr < gs * (D / 2); pr += blockDim.x) {
     const int j = pr / (D / 2), e = 2 * (pr % (D / 2));
@@ -440,15 +482,15 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
 template <typename T, int D>
 __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bars[kMaxGroup];
   const int64_t t0 = p.total ? *p.total : p.id_bound;
   const bool appending = p.k_new != nullptr;
   const int64_t total = t0 + (appending ? 1 : 0);
   const int ncos = p.do_cos ? p.U * p.cos_blocks_per_unit : 0;
   if ((int)blockIdx.x < ncos)
-    cos_task<T, D>(p, blockIdx.x, smem, &bar);
+    cos_task<T, D>(p, blockIdx.x, smem, bars);
   else
-    static_task<T, D>(p, blockIdx.x - ncos, t0, total, smem, &bar);
+    static_task<T, D>(p, blockIdx.x - ncos, t0, total, smem, bars);
   if (appending && blockIdx.x == 0) {
     T* keys = static_cast<T*>(const_cast<void*>(p.keys));
     T* vals = static_cast<T*>(const_cast<void*>(p.values));
@@ -467,7 +509,7 @@ size_t scan2_smem(int gs) {
   constexpr int RB = D * int(sizeof(T));
   constexpr int ST = static_tok<T>();
   const size_t cosb = (size_t)kScanRowsV2 * RB + sizeof(float) * gs * D + sizeof(double) * gs +
-                      sizeof(double) * kScanRowsV2;
+                      sizeof(double) * 2 * kScanRowsV2;
   const size_t stb = (size_t)2 * ST * RB + sizeof(float) * gs * D + sizeof(double) * gs * ST +
                      sizeof(float) * gs * ST + sizeof(double) * 2 * gs;
   return cosb > stb ? cosb : stb;
@@ -873,33 +915,43 @@ __global__ void __launch_bounds__(kUnitThreads, 1) unit_kernel(DecodeParams p) {
 }
 
 // ------------------------------------------------------------------------
-// v2 fused unit kernel (bf16): a 2-CTA cluster per (b, g) unit.  Both CTAs
-// redundantly pick the C' slots and build the union (cheap, deterministic);
-// each computes the rerank logits of half the recalled positions and writes
-// the packed (score, position) keys into both CTAs' shared memory (DSMEM);
-// both sort; rank 1 applies the FIFO DCU while the pair splits the sparse
-// attention, rank 1 ships its partial to rank 0 over DSMEM, and rank 0
-// merges it with the static partials and writes the output.
+// v3 fused unit kernel (bf16): a 2-CTA cluster per (b, g) unit.
+//   both ranks : top-C' slots from the scan's chunk candidates (one warp),
+//                union via per-list bitmaps tested in parallel, rerank
+//                logits for half the recalled positions -> packed
+//                (score, position) keys in both CTAs' smem (DSMEM)
+//   cluster barrier
+//   rank 0     : radix-select the top-rho' set, sparse attention over it,
+//                exact merge with the (prefetched) static partials -> out
+//   rank 1     : full (score desc, position asc) sort, FIFO DCU write,
+//                ordered sparse-id outputs
 // ------------------------------------------------------------------------
 
 constexpr int kU2Threads = 512;
 constexpr int kU2Warps = kU2Threads / 32;
+constexpr int kMaxParLists = 8;   // C' lists unioned in parallel (else sequentially)
 
 struct U2Smem {
-  int32_t* sel;
-  uint32_t* bitmap;
-  int32_t* rec;
-  uint64_t* skey;
-  float* wts;
-  float* red;
-  float* xo;       // rank 1 -> rank 0: o [gs][D]
-  double* xml;     // rank 1 -> rank 0: m, l [2][gs]
-  double* scratch;
+  int32_t* sel;      // [c_prime]
+  uint32_t* areaA;   // union bitmaps; then static-partial o prefetch + selected positions
+  int32_t* rec;      // [lmax]
+  uint64_t* skey;    // [npad]; rank 0 reuses it as the attention reduce area
+  float* wts;        // [gs][kAttnChunk]
+  double* spml;      // [2][ns][gs] static m, l
+  int* hist;         // [256]
+  double* scratch;   // [128]
 };
 
 __host__ __device__ inline int u2_npad(int lmax) {
   const int n = next_pow2(lmax > 1 ? lmax : 1);
   return n < kU2Threads ? kU2Threads : n;
+}
+
+__host__ __device__ inline size_t u2_area_a(const DecodeParams& p, int D) {
+  const int nb = p.c_prime <= kMaxParLists ? p.c_prime : 1;
+  const size_t bm = (size_t)nb * p.bitmap_words * 4;
+  const size_t po = (size_t)p.ns * p.gs * D * 4 + (size_t)4 * (p.lmax > 1 ? p.lmax : 1);
+  return bm > po ? bm : po;
 }
 
 __host__ __device__ inline size_t u2_layout(const DecodeParams& p, int D, U2Smem* s,
@@ -910,15 +962,16 @@ __host__ __device__ inline size_t u2_layout(const DecodeParams& p, int D, U2Smem
     off += align16(bytes);
     return ptr;
   };
+  const size_t red = (size_t)kU2Warps * p.gs * D * 4;
+  const size_t keys = (size_t)u2_npad(p.lmax) * 8;
   U2Smem t;
   t.sel = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (p.c_prime > 1 ? p.c_prime : 1)));
-  t.bitmap = reinterpret_cast<uint32_t*>(take(sizeof(uint32_t) * p.bitmap_words));
+  t.areaA = reinterpret_cast<uint32_t*>(take(u2_area_a(p, D)));
   t.rec = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (p.lmax > 1 ? p.lmax : 1)));
-  t.skey = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * u2_npad(p.lmax)));
+  t.skey = reinterpret_cast<uint64_t*>(take(keys > red ? keys : red));
   t.wts = reinterpret_cast<float*>(take(sizeof(float) * p.gs * kAttnChunk));
-  t.red = reinterpret_cast<float*>(take(sizeof(float) * kU2Warps * p.gs * D));
-  t.xo = reinterpret_cast<float*>(take(sizeof(float) * p.gs * D));
-  t.xml = reinterpret_cast<double*>(take(sizeof(double) * 2 * p.gs));
+  t.spml = reinterpret_cast<double*>(take(sizeof(double) * 2 * (p.ns > 1 ? p.ns : 1) * p.gs));
+  t.hist = reinterpret_cast<int*>(take(sizeof(int) * 256));
   t.scratch = reinterpret_cast<double*>(take(sizeof(double) * 128));
   if (s) *s = t;
   return off;
@@ -938,11 +991,70 @@ __device__ void sort_keys(uint64_t* skey) {
   __syncthreads();
 }
 
+// positions of the R smallest of the (unique) keys key[0..L) -> spos (any order)
+__device__ int select_smallest(const uint64_t* key, int L, int R, int* spos, int* hist,
+                               int* s_state) {
+  if (R >= L) {
+    for (int i = threadIdx.x; i < L; i += blockDim.x) spos[i] = i;
+    __syncthreads();
+    return L;
+  }
+  uint64_t prefix = 0;
+  int need = R, shift = 56;
+  while (true) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+      const uint64_t k = key[i];
+      if (shift == 56 || ((k ^ prefix) >> (shift + 8)) == 0) atomicAdd(&hist[(k >> shift) & 255], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int sum = 0;
+      for (int b = 8 * lane; b < 8 * lane + 8; ++b) sum += hist[b];
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int excl = incl - sum;
+      const unsigned bal = __ballot_sync(0xffffffffu, incl >= need && excl < need);
+      if (lane == __ffs(bal) - 1) {
+        int run = excl;
+        for (int b = 8 * lane; b < 8 * lane + 8; ++b) {
+          if (run + hist[b] >= need) {
+            s_state[0] = b;
+            s_state[1] = run;
+            s_state[2] = hist[b];
+            break;
+          }
+          run += hist[b];
+        }
+      }
+    }
+    __syncthreads();
+    const int b = s_state[0], below = s_state[1], cnt = s_state[2];
+    prefix |= (uint64_t)b << shift;
+    need -= below;
+    if (cnt == need || shift == 0) break;
+    shift -= 8;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) s_state[3] = 0;
+  __syncthreads();
+  const uint64_t lim = prefix >> shift;
+  for (int i = threadIdx.x; i < L; i += blockDim.x)
+    if ((key[i] >> shift) <= lim) spos[atomicAdd(&s_state[3], 1)] = i;
+  __syncthreads();
+  return s_state[3];
+}
+
 template <typename T, int D>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
     unit2_kernel(DecodeParams p) {
   namespace cg = cooperative_groups;
-  using R = Row<T, D>;
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cl = cg::this_cluster();
   const int rank = (int)cl.block_rank();
@@ -955,37 +1067,92 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
   const bool appending = p.k_new != nullptr;
   const int64_t total = t0 + (appending ? 1 : 0);
   __shared__ int64_t s_slot;
-  __shared__ float qs[kMaxGroup * D];
+  __shared__ __align__(16) T qs[kMaxGroup * D];
   __shared__ double ms[kMaxGroup], ls[kMaxGroup];
+  __shared__ int s_state[4];
   if (tid == 0) s_slot = p.fifo ? (p.fifo[bi] % p.C) : 0;
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int i = tid; i < gs * D; i += blockDim.x) qs[i] = to_f(q[i]);
+  for (int i = tid; i < gs * D; i += blockDim.x) qs[i] = q[i];
+  const int64_t pbase = (int64_t)u * p.ns;
+  if (rank == 0)   // static m, l (ready since the scan kernel finished)
+    for (int i = tid; i < p.ns * gs; i += blockDim.x) {
+      S.spml[i] = p.pm[pbase * gs + i];
+      S.spml[p.ns * gs + i] = p.pl[pbase * gs + i];
+    }
 
-  // ---- 1. top-C' slots (both ranks; deterministic) -----------------------
-  {
+  // ---- 1. top-C' slots from the chunk candidates (one warp) -------------
+  if (warp == 0) {
+    const int M = p.cos_blocks_per_unit * p.ncand;
+    const double* cv = p.cval + (int64_t)u * M;
+    const int32_t* ci = p.cidx + (int64_t)u * M;
     uint64_t prev_key = ~0ull;
     int prev_idx = -1;
-    const double* gc = p.gcos + (int64_t)u * p.C;
     for (int r = 0; r < p.c_prime; ++r) {
       uint64_t bk = 0;
       int bidx = INT32_MAX;
-      for (int i = tid; i < p.C; i += blockDim.x) {
-        const uint64_t k = okey64(gc[i]);
+      for (int m = lane; m < M; m += 32) {
+        const uint64_t k = okey64(cv[m]);
+        const int i = ci[m];
         const bool below = k < prev_key || (k == prev_key && i > prev_idx);
         if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
       }
-      const int w = block_argmax(bk, bidx, S.scratch);
-      if (tid == 0) S.sel[r] = w;
-      prev_idx = w;
-      prev_key = okey64(gc[w]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
+        if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
+      }
+      if (lane == 0) S.sel[r] = bidx;
+      prev_key = bk;
+      prev_idx = bidx;
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. union of the selected lists, first occurrence kept -------------
+  int L = 0;
+  const int nwords = (int)((total + 31) >> 5);
+  if (p.c_prime <= kMaxParLists) {
+    // every list marks its own bitmap, then an id of list j survives iff no
+    // earlier list holds it; one ordered scan compacts (list, position) order
+    const int nb = p.c_prime;
+    for (int i = tid; i < nb * p.bitmap_words; i += blockDim.x) S.areaA[i] = 0u;
+    __syncthreads();
+    const int n = nb * p.rho;
+    for (int o = tid; o < n; o += blockDim.x) {
+      const int j = o / p.rho;
+      const int id = p.lists[((int64_t)u * p.C + S.sel[j]) * p.rho + (o - j * p.rho)];
+      if (id == kEmpty) continue;
+      if (id < 0 || id >= total) { set_flag(p.flags, kFlagIdRange); continue; }
+      atomicOr(&S.areaA[j * p.bitmap_words + (id >> 5)], 1u << (id & 31));
     }
     __syncthreads();
-  }
-  // ---- 2. union, first occurrence kept (both ranks) -----------------------
-  int L = 0;
-  {
-    const int nwords = (int)((total + 31) >> 5);
-    for (int i = tid; i < nwords; i += blockDim.x) S.bitmap[i] = 0u;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int o0 = tid * per;
+    int cnt = 0;
+    uint64_t keep = 0;   // per <= 64: n = C' * rho <= 8 * 4096
+    for (int e = 0; e < per; ++e) {
+      const int o = o0 + e;
+      if (o >= n) break;
+      const int j = o / p.rho;
+      const int id = p.lists[((int64_t)u * p.C + S.sel[j]) * p.rho + (o - j * p.rho)];
+      if (id == kEmpty || id < 0 || id >= total) continue;
+      bool dup = false;
+      for (int j2 = 0; j2 < j; ++j2) dup |= (S.areaA[j2 * p.bitmap_words + (id >> 5)] >> (id & 31)) & 1u;
+      if (!dup) { keep |= 1ull << e; ++cnt; }
+    }
+    int tot;
+    int pos = block_exclusive_scan(cnt, &tot, S.scratch);
+    for (int e = 0; e < per; ++e)
+      if (keep & (1ull << e)) {
+        const int o = o0 + e, j = o / p.rho;
+        S.rec[pos++] = p.lists[((int64_t)u * p.C + S.sel[j]) * p.rho + (o - j * p.rho)];
+      }
+    L = tot;
+    __syncthreads();
+  } else {
+    uint32_t* bitmap = S.areaA;
+    for (int i = tid; i < nwords; i += blockDim.x) bitmap[i] = 0u;
     __syncthreads();
     const int per = (p.rho + blockDim.x - 1) / blockDim.x;
     for (int j = 0; j < p.c_prime; ++j) {
@@ -994,30 +1161,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
       for (int e = 0; e < per; ++e) {
         const int i = tid * per + e;
         int id = (i < p.rho) ? row[i] : kEmpty;
-        if (id != kEmpty && (id < 0 || id >= total)) {
-          set_flag(p.flags, kFlagIdRange);
-          id = kEmpty;
-        }
-        if (id != kEmpty && !((S.bitmap[id >> 5] >> (id & 31)) & 1u)) {
-          keep_mask |= 1 << e;
-          ++cnt;
-        }
+        if (id != kEmpty && (id < 0 || id >= total)) { set_flag(p.flags, kFlagIdRange); id = kEmpty; }
+        if (id != kEmpty && !((bitmap[id >> 5] >> (id & 31)) & 1u)) { keep_mask |= 1 << e; ++cnt; }
       }
-      int tot_kept;
-      int pos = L + block_exclusive_scan(cnt, &tot_kept, S.scratch);
+      int tot;
+      int pos = L + block_exclusive_scan(cnt, &tot, S.scratch);
       for (int e = 0; e < per; ++e)
         if (keep_mask & (1 << e)) S.rec[pos++] = row[tid * per + e];
       __syncthreads();
       for (int e = 0; e < per; ++e)
         if (keep_mask & (1 << e)) {
           const int id = row[tid * per + e];
-          atomicOr(&S.bitmap[id >> 5], 1u << (id & 31));
+          atomicOr(&bitmap[id >> 5], 1u << (id & 31));
         }
-      L += tot_kept;
+      L += tot;
       __syncthreads();
     }
   }
   const int npad = u2_npad(L);
+  // rank 0: prefetch the static partials' o into area A (free after the union)
+  float* spo = reinterpret_cast<float*>(S.areaA);
+  int* spos = reinterpret_cast<int*>(spo + (size_t)p.ns * gs * D);
+  if (rank == 0)
+    for (int i = tid; i < p.ns * gs * D; i += blockDim.x) spo[i] = p.po[pbase * gs * D + i];
+
   // ---- 3. rerank logits for this rank's half (row per thread) ------------
   double* lg = p.logits + (int64_t)u * gs * p.lmax;
   uint64_t* peer_skey = cl.map_shared_rank(S.skey, rank ^ 1);
@@ -1026,13 +1193,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
     const int lo = rank ? half : 0, hi = rank ? L : half;
     const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
     const double scale = 1.0 / sqrt((double)D);
-    constexpr int VPR = D * int(sizeof(T)) / 16, EPV = 16 / int(sizeof(T));
+    constexpr int VPR = D * int(sizeof(T)) / 16;
     for (int t = lo + tid; t < hi; t += blockDim.x) {
       const uint4* r4 = reinterpret_cast<const uint4*>(keys + (int64_t)S.rec[t] * D);
-      constexpr int KC = VPR < 8 ? VPR : 8;     // 16-byte chunks held in registers at once
+      constexpr int KC = VPR < 8 ? VPR : 8;
       double gmax = -INFINITY;
 #pragma unroll 1
-      for (int h0 = 0; h0 < gs; h0 += 8) {      // heads in groups of 8: registers, not local memory
+      for (int h0 = 0; h0 < gs; h0 += 8) {
         double acc[8];
 #pragma unroll
         for (int hh = 0; hh < 8; ++hh) acc[hh] = 0.0;
@@ -1043,16 +1210,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
           for (int k = 0; k < KC; ++k) raw[k] = ldg16(r4 + k0 + k);
 #pragma unroll
           for (int k = 0; k < KC; ++k) {
-            float x[EPV];
-            unpack16<T>(raw[k], x);
 #pragma unroll
             for (int hh = 0; hh < 8; ++hh) {
               if (h0 + hh < gs) {
-                const float* qh = qs + (h0 + hh) * D + (k0 + k) * EPV;
-                float pd = 0.f;
-#pragma unroll
-                for (int j = 0; j < EPV; ++j) pd = fmaf(qh[j], x[j], pd);
-                acc[hh] += (double)pd;
+                const uint4 qq = reinterpret_cast<const uint4*>(qs + (h0 + hh) * D)[k0 + k];
+                acc[hh] += (double)bf16x8_dot(qq, raw[k], 0.f);
               }
             }
           }
@@ -1072,135 +1234,154 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
     }
     for (int t = L + tid; t < npad; t += blockDim.x) S.skey[t] = ~0ull;
   }
-  cl.sync();  // both halves of the keys (and of the logits in global) are in place
+  cl.sync();  // keys complete in both CTAs; logits visible in global memory
 
-  // ---- 4. order by (score desc, recall position asc) ---------------------
-  if (L > 0) {
-    switch (npad) {
-      case 512: sort_keys<1>(S.skey); break;
-      case 1024: sort_keys<2>(S.skey); break;
-      case 2048: sort_keys<4>(S.skey); break;
-      case 4096: sort_keys<8>(S.skey); break;
-      default: sort_keys<16>(S.skey); break;
-    }
-  }
-  auto pos_at = [&](int i) { return (int)(uint32_t)(S.skey[i] & 0xffffffffu); };
-
-  // ---- 5. FIFO DCU (rank 1) -------------------------------------------------
-  const bool dcu_here = (p.stages & kStageDcu) && L > 0;
-  if (rank == 1 && dcu_here) {
-    const int64_t slot = s_slot;
-    int32_t* row = p.lists + ((int64_t)u * p.C + slot) * p.rho;
-    const int keep = min(p.rho, L);
-    for (int i = tid; i < p.rho; i += blockDim.x) row[i] = i < keep ? S.rec[pos_at(i)] : kEmpty;
-    T* cent = static_cast<T*>(p.cent);
-    for (int i = tid; i < gs * D; i += blockDim.x) {
-      const int hh = i / D, e = i % D;
-      cent[(((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D + e] = q[i];
-    }
-  }
-  // ---- 6. sparse attention over this rank's share of the sparse set -------
   const int Rn = (L > 0) ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
-  auto pos_of = [&](int i) { return p.use_rerank ? pos_at(i) : i; };
-  const int r0 = (Rn + 1) >> 1;
-  const int my_lo = rank ? r0 : 0, my_n = rank ? Rn - r0 : r0;
-  {
-    for (int hh = 0; hh < gs; ++hh) {
-      double m = -INFINITY;
-      for (int i = tid; i < my_n; i += blockDim.x) m = fmax(m, lg[(int64_t)hh * p.lmax + pos_of(my_lo + i)]);
-      m = block_max_f64(m, S.scratch);
-      if (tid == 0) { ms[hh] = m; ls[hh] = 0.0; }
+  const bool dcu_here = (p.stages & kStageDcu) && L > 0;
+  if (rank == 1) {
+    // ---- rank 1: full order, DCU, ordered sparse ids -------------------------
+    if (L > 0 && (dcu_here || (p.sparse_ids && p.use_rerank))) {
+      switch (npad) {
+        case 512: sort_keys<1>(S.skey); break;
+        case 1024: sort_keys<2>(S.skey); break;
+        case 2048: sort_keys<4>(S.skey); break;
+        case 4096: sort_keys<8>(S.skey); break;
+        default: sort_keys<16>(S.skey); break;
+      }
     }
-    for (int i = tid; i < kU2Warps * gs * D; i += blockDim.x) S.red[i] = 0.f;
+    auto pos_at = [&](int i) { return (int)(uint32_t)(S.skey[i] & 0xffffffffu); };
+    if (dcu_here) {
+      const int64_t slot = s_slot;
+      int32_t* row = p.lists + ((int64_t)u * p.C + slot) * p.rho;
+      const int keep = min(p.rho, L);
+      for (int i = tid; i < p.rho; i += blockDim.x) row[i] = i < keep ? S.rec[pos_at(i)] : kEmpty;
+      T* cent = static_cast<T*>(p.cent);
+      for (int i = tid; i < gs * D; i += blockDim.x) {
+        const int hh = i / D, e = i % D;
+        cent[(((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D + e] = q[i];
+      }
+    }
+    if (p.sparse_ids)
+      for (int i = tid; i < p.sparse_cap; i += blockDim.x)
+        p.sparse_ids[(int64_t)u * p.sparse_cap + i] =
+            i < Rn ? S.rec[p.use_rerank ? pos_at(i) : i] : kEmpty;
+    return;
+  }
+
+  // ---- rank 0: top-rho' set, sparse attention, merge --------------------
+  const int nsel = Rn > 0 ? select_smallest(S.skey, L, Rn, spos, S.hist, s_state) : 0;
+  {
+    // per-head max over the selected logits: thread-local, warp, then block
+    double* wm = S.scratch;             // [kU2Warps][gs] (gs <= 8 here) as doubles
+    for (int h0 = 0; h0 < gs; h0 += 4) {
+      double m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      for (int i = tid; i < nsel; i += blockDim.x) {
+        const int ps = spos[i];
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh)
+          if (h0 + hh < gs) m4[hh] = fmax(m4[hh], lg[(int64_t)(h0 + hh) * p.lmax + ps]);
+      }
+#pragma unroll
+      for (int hh = 0; hh < 4; ++hh) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m4[hh] = fmax(m4[hh], __shfl_xor_sync(0xffffffffu, m4[hh], o));
+      }
+      __syncthreads();
+      if (lane == 0)
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) wm[warp * 4 + hh] = m4[hh];
+      __syncthreads();
+      if (tid < 4 && h0 + tid < gs) {
+        double m = -INFINITY;
+        for (int w = 0; w < kU2Warps; ++w) m = fmax(m, wm[w * 4 + tid]);
+        ms[h0 + tid] = m;
+        ls[h0 + tid] = 0.0;
+      }
+    }
     __syncthreads();
+    float* red = reinterpret_cast<float*>(S.skey);   // keys are dead on rank 0 now
+    for (int i = tid; i < kU2Warps * gs * D; i += blockDim.x) red[i] = 0.f;
     const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
-    for (int c0 = 0; c0 < my_n; c0 += kAttnChunk) {
-      const int n = min(kAttnChunk, my_n - c0);
-      for (int hh = 0; hh < gs; ++hh) {
-        double lp = 0.0;
+    for (int c0 = 0; c0 < nsel; c0 += kAttnChunk) {
+      const int n = min(kAttnChunk, nsel - c0);
+      for (int h0 = 0; h0 < gs; h0 += 4) {
+        double l4[4] = {0.0, 0.0, 0.0, 0.0};
         for (int i = tid; i < n; i += blockDim.x) {
-          const double e = exp(lg[(int64_t)hh * p.lmax + pos_of(my_lo + c0 + i)] - ms[hh]);
-          S.wts[hh * kAttnChunk + i] = (float)e;
-          lp += e;
+          const int ps = spos[c0 + i];
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh)
+            if (h0 + hh < gs) {
+              const double e = exp(lg[(int64_t)(h0 + hh) * p.lmax + ps] - ms[h0 + hh]);
+              S.wts[(h0 + hh) * kAttnChunk + i] = (float)e;
+              l4[hh] += e;
+            }
         }
-        lp = block_sum_f64(lp, S.scratch);
-        if (tid == 0) ls[hh] += lp;
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) l4[hh] += __shfl_xor_sync(0xffffffffu, l4[hh], o);
+        }
+        __syncthreads();
+        if (lane == 0)
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh) S.scratch[warp * 4 + hh] = l4[hh];
+        __syncthreads();
+        if (tid < 4 && h0 + tid < gs) {
+          double l = 0.0;
+          for (int w = 0; w < kU2Warps; ++w) l += S.scratch[w * 4 + tid];
+          ls[h0 + tid] += l;
+        }
       }
       __syncthreads();
       accum_weighted_rows<T, D>(
-          n, gs, [&](int t) -> const T* { return vals + (int64_t)S.rec[pos_of(my_lo + c0 + t)] * D; },
-          [&](int hh, int t) { return S.wts[hh * kAttnChunk + t]; }, S.red + (int64_t)warp * gs * D);
+          n, gs, [&](int t) -> const T* { return vals + (int64_t)S.rec[spos[c0 + t]] * D; },
+          [&](int hh, int t) { return S.wts[hh * kAttnChunk + t]; }, red + (int64_t)warp * gs * D);
       __syncthreads();
     }
-    // this rank's partial: o [gs][D] (unnormalised), m, l
-    float* xo = rank ? cl.map_shared_rank(S.xo, 0) : S.xo;
-    double* xml = rank ? cl.map_shared_rank(S.xml, 0) : S.xml;
-    if (rank == 1) {
-      for (int i = tid; i < gs * D; i += blockDim.x) {
-        float s = 0.f;
-        for (int w = 0; w < kU2Warps; ++w) s += S.red[(int64_t)w * gs * D + i];
-        xo[i] = s;
+    // exact merge with the static partials
+    bool none = false;
+    for (int i = tid; i < gs * D; i += blockDim.x) {
+      const int hh = i / D, e = i % D;
+      float o0 = 0.f;
+      for (int w = 0; w < kU2Warps; ++w) o0 += red[(int64_t)w * gs * D + i];
+      double M = ls[hh] > 0.0 ? ms[hh] : -INFINITY;
+      for (int j = 0; j < p.ns; ++j)
+        if (S.spml[p.ns * gs + j * gs + hh] > 0.0) M = fmax(M, S.spml[j * gs + hh]);
+      double Ls = 0.0, O = 0.0;
+      if (ls[hh] > 0.0) {
+        const double w = exp(ms[hh] - M);
+        Ls += w * ls[hh];
+        O += w * (double)o0;
       }
-      if (tid < gs) { xml[tid] = ms[tid]; xml[gs + tid] = ls[tid]; }
-    }
-  }
-  cl.sync();  // rank 1's partial has landed in rank 0's shared memory
-  if (rank == 1) return;
-
-  // ---- 7. rank 0: merge sparse halves + static partials -> output ---------
-  bool none = false;
-  const int64_t pbase = (int64_t)u * p.ns;
-  for (int i = tid; i < gs * D; i += blockDim.x) {
-    const int hh = i / D, e = i % D;
-    float o0 = 0.f;
-    for (int w = 0; w < kU2Warps; ++w) o0 += S.red[(int64_t)w * gs * D + i];
-    double M = -INFINITY;
-    if (ls[hh] > 0.0) M = ms[hh];
-    if (S.xml[gs + hh] > 0.0) M = fmax(M, S.xml[hh]);
-    for (int j = 0; j < p.ns; ++j)
-      if (p.pl[(pbase + j) * gs + hh] > 0.0) M = fmax(M, p.pm[(pbase + j) * gs + hh]);
-    double Ls = 0.0, O = 0.0;
-    if (ls[hh] > 0.0) {
-      const double w = exp(ms[hh] - M);
-      Ls += w * ls[hh];
-      O += w * (double)o0;
-    }
-    if (S.xml[gs + hh] > 0.0) {
-      const double w = exp(S.xml[hh] - M);
-      Ls += w * S.xml[gs + hh];
-      O += w * (double)S.xo[i];
-    }
-    for (int j = 0; j < p.ns; ++j) {
-      const double lj = p.pl[(pbase + j) * gs + hh];
-      if (lj > 0.0) {
-        const double w = exp(p.pm[(pbase + j) * gs + hh] - M);
-        Ls += w * lj;
-        O += w * (double)p.po[((pbase + j) * gs + hh) * D + e];
+      for (int j = 0; j < p.ns; ++j) {
+        const double lj = S.spml[p.ns * gs + j * gs + hh];
+        if (lj > 0.0) {
+          const double w = exp(S.spml[j * gs + hh] - M);
+          Ls += w * lj;
+          O += w * (double)spo[(j * gs + hh) * D + e];
+        }
+      }
+      const int64_t oh = (int64_t)bi * p.h + gi * gs + hh;
+      if (Ls > 0.0) {
+        p.out[oh * D + e] = (float)(O / Ls);
+      } else {
+        p.out[oh * D + e] = 0.f;
+        none = true;
+      }
+      if (e == 0) {
+        if (p.row_max) p.row_max[oh] = M;
+        if (p.denom) p.denom[oh] = Ls;
       }
     }
-    const int64_t oh = (int64_t)bi * p.h + gi * gs + hh;
-    if (Ls > 0.0) {
-      p.out[oh * D + e] = (float)(O / Ls);
-    } else {
-      p.out[oh * D + e] = 0.f;
-      none = true;
-    }
-    if (e == 0) {
-      if (p.row_max) p.row_max[oh] = M;
-      if (p.denom) p.denom[oh] = Ls;
-    }
+    if (none) set_flag(p.flags, kFlagNoTokens);
   }
-  if (none) set_flag(p.flags, kFlagNoTokens);
   if (p.selected)
     for (int r = tid; r < p.c_prime; r += blockDim.x) p.selected[(int64_t)u * p.c_prime + r] = S.sel[r];
   if (p.recall_len && tid == 0) p.recall_len[u] = L;
-  if (tid == 0) set_flag(p.flags, L > 0 ? kFlagNonEmptyRecall : kFlagEmptyRecall);
-  if (p.sparse_ids)
-    for (int i = tid; i < p.sparse_cap; i += blockDim.x)
-      p.sparse_ids[(int64_t)u * p.sparse_cap + i] = i < Rn ? S.rec[pos_of(i)] : kEmpty;
   if (p.sparse_len && tid == 0) p.sparse_len[u] = Rn;
+  if (tid == 0) set_flag(p.flags, L > 0 ? kFlagNonEmptyRecall : kFlagEmptyRecall);
 
-  // ---- 8. completion: FIFO cursor advance + total++ by the last unit -------
+  // ---- completion: FIFO cursor advance + total++ by the last unit ----------
   if (p.stages & (kStageDcu | kStageAppendTail)) {
     __syncthreads();
     if (tid == 0) {

@@ -55,6 +55,9 @@ struct DecodeParams {
   double* pl;       // [U][ns][gs]
   float* po;        // [U][ns][gs][D]
   double* logits;   // [U][gs][lmax]
+  double* cval;     // [U][cos_blocks_per_unit][ncand] chunk top-C' cosines
+  int32_t* cidx;    // [U][cos_blocks_per_unit][ncand] their centroid slots
+  int ncand;        // min(C', centroids per cos chunk)
   // staged io
   const int32_t* rec_in;
   const int32_t* len_in;

@@ -18,7 +18,7 @@ import torch
 from . import _native as N
 from .index import QueryCentroidIndex
 from .parallel import ShardPlan, all_gather_outputs
-from .retrieval import DecodeConfig, StepBuffers, launch_step
+from .retrieval import DecodeConfig, StepBuffers
 from .store import KvStore
 
 
@@ -27,6 +27,7 @@ class Layer:
     store: KvStore
     index: QueryCentroidIndex
     bufs: StepBuffers
+    call: tuple | None = None   # cached ctypes arguments of ctkv_decode_step_phase
 
 
 class DecodeEngine:
@@ -58,6 +59,8 @@ class DecodeEngine:
         self.k = torch.zeros((nl, self.b, self.g, self.d), dtype=self.dtype, device=dev)
         self.v = torch.zeros((nl, self.b, self.g, self.d), dtype=self.dtype, device=dev)
         self.out = torch.zeros((nl, self.b, self.h, self.d), dtype=torch.float32, device=dev)
+        for li, layer in enumerate(self.layers):
+            layer.bufs.out = self.out[li]          # kernels write the layer output in place
         world = plan.world if plan else 1
         self.gathered = (torch.zeros((nl, plan.batch, plan.query_heads, self.d), dtype=torch.float32,
                                      device=dev) if world > 1 else self.out)
@@ -68,20 +71,42 @@ class DecodeEngine:
 
     # -- one step -------------------------------------------------------------
 
+    def _prepare(self) -> None:
+        """Build every layer's ctypes argument block once (pointers are fixed
+        for the engine's lifetime), so a launch costs one foreign call."""
+        cfg = self.cfg
+        for li, layer in enumerate(self.layers):
+            st, ix, bf = layer.store, layer.index, layer.bufs
+            if cfg.c_prime > ix.capacity:
+                raise ValueError("c_prime exceeds the index capacity")
+            args = N.StepArgs(self.q[li].data_ptr(), self.k[li].data_ptr(), self.v[li].data_ptr(),
+                              cfg.c_prime, cfg.rho_prime, int(cfg.use_dcu), int(cfg.use_rerank),
+                              bf.out.data_ptr(), bf.row_max.data_ptr(), bf.denom.data_ptr(),
+                              bf.selected.data_ptr(), bf.recall_len.data_ptr(),
+                              bf.sparse_ids.data_ptr(), bf.sparse_len.data_ptr(), bf.sparse_cap,
+                              bf.flags.data_ptr())
+            layer.call = (st.ctkv_layout(), st.desc(), ix.desc(), args, bf.ws.data_ptr(),
+                          bf.ws.numel())
+
+    def _launch(self, layer: Layer, phase: int) -> None:
+        lay, sd, idd, args, ws, wsn = layer.call
+        rc = self._fn(lay, sd, idd, args, phase, ws, wsn, torch.cuda.current_stream().cuda_stream)
+        if rc:
+            N.check(rc, "decode_step")
+
     def _enqueue(self, events=None) -> None:
+        if self.layers[0].call is None:
+            self._prepare()
+            self._fn = N.lib().ctkv_decode_step_phase
         for li, layer in enumerate(self.layers):
             if events is not None:
                 events[li][0].record()
-                launch_step(layer.store, layer.index, self.cfg, self.q[li], layer.bufs,
-                            self.k[li], self.v[li], phase=1)
+                self._launch(layer, 1)
                 events[li][1].record()
-                launch_step(layer.store, layer.index, self.cfg, self.q[li], layer.bufs,
-                            self.k[li], self.v[li], phase=2)
+                self._launch(layer, 2)
                 events[li][2].record()
             else:
-                launch_step(layer.store, layer.index, self.cfg, self.q[li], layer.bufs,
-                            self.k[li], self.v[li])
-            self.out[li].copy_(layer.bufs.out)
+                self._launch(layer, 3)
             if self._gbuf is not None:
                 self.gathered[li].copy_(all_gather_outputs(self.plan, self.out[li], self.group,
                                                            self._gbuf))
@@ -94,6 +119,7 @@ class DecodeEngine:
     def reserve(self, steps: int) -> None:
         for layer in self.layers:
             layer.store.ensure_room(steps)
+            layer.call = None   # storage may have moved
 
     def step(self, events=None) -> None:
         """Enqueue one decode step (all layers) eagerly."""
