@@ -211,6 +211,11 @@ size_t ctkv_topk_workspace_bytes(int64_t rows, int64_t n, int32_t k);
 int ctkv_topk_rows(const float* values, int64_t rows, int64_t n, int32_t k, int32_t* idx,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* Profiling aid: on=1/0 switches per-CTA phase timestamps of the fused unit
+ * kernel on/off (on<0 leaves it); host_out (may be NULL) receives up to n
+ * u64 globaltimer stamps laid out [256 CTAs][12 checkpoints]. */
+int ctkv_debug_phase_timing(int32_t on, uint64_t* host_out, int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

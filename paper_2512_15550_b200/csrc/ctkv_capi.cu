@@ -437,4 +437,8 @@ int ctkv_topk_rows(const float* values, int64_t rows, int64_t n, int32_t k, int3
                           static_cast<cudaStream_t>(stream));
 }
 
+int ctkv_debug_phase_timing(int32_t on, uint64_t* host_out, int32_t n) {
+  return ctkv::phase_timing(on, reinterpret_cast<unsigned long long*>(host_out), n);
+}
+
 }  // extern "C"

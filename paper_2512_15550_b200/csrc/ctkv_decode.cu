@@ -37,6 +37,19 @@ namespace ctkv {
 
 constexpr int kScanRowsV2 = 256;   // threads (and centroid rows) per v2 scan CTA
 
+// Per-CTA phase timestamps of the fused unit kernel (globaltimer, ns), for
+// profiling only: [cta][checkpoint].  Written when g_phase_on != 0.
+constexpr int kPhaseCtas = 256, kPhases = 12;
+__device__ unsigned long long g_phase[kPhaseCtas][kPhases];
+__device__ int g_phase_on;
+__device__ __forceinline__ void phase_mark(int k) {
+  if (g_phase_on && threadIdx.x == 0 && blockIdx.x < kPhaseCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_phase[blockIdx.x][k] = t;
+  }
+}
+
 constexpr int kScanThreads = 256;
 constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kCosChunk = 64;       // centroids per scan CTA (all gs heads)
@@ -1070,6 +1083,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
   __shared__ __align__(16) T qs[kMaxGroup * D];
   __shared__ double ms[kMaxGroup], ls[kMaxGroup];
   __shared__ int s_state[4];
+  phase_mark(0);
   if (tid == 0) s_slot = p.fifo ? (p.fifo[bi] % p.C) : 0;
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = tid; i < gs * D; i += blockDim.x) qs[i] = q[i];
@@ -1108,6 +1122,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
     }
   }
   __syncthreads();
+  phase_mark(1);
 
   // ---- 2. union of the selected lists, first occurrence kept -------------
   int L = 0;
@@ -1178,6 +1193,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
       __syncthreads();
     }
   }
+  phase_mark(2);
   const int npad = u2_npad(L);
   // rank 0: prefetch the static partials' o into area A (free after the union)
   float* spo = reinterpret_cast<float*>(S.areaA);
@@ -1234,7 +1250,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
     }
     for (int t = L + tid; t < npad; t += blockDim.x) S.skey[t] = ~0ull;
   }
+  phase_mark(3);
   cl.sync();  // keys complete in both CTAs; logits visible in global memory
+  phase_mark(4);
 
   const int Rn = (L > 0) ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
   const bool dcu_here = (p.stages & kStageDcu) && L > 0;
@@ -1249,6 +1267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
         default: sort_keys<16>(S.skey); break;
       }
     }
+    phase_mark(5);
     auto pos_at = [&](int i) { return (int)(uint32_t)(S.skey[i] & 0xffffffffu); };
     if (dcu_here) {
       const int64_t slot = s_slot;
@@ -1265,11 +1284,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
       for (int i = tid; i < p.sparse_cap; i += blockDim.x)
         p.sparse_ids[(int64_t)u * p.sparse_cap + i] =
             i < Rn ? S.rec[p.use_rerank ? pos_at(i) : i] : kEmpty;
+    phase_mark(6);
     return;
   }
 
   // ---- rank 0: top-rho' set, sparse attention, merge --------------------
   const int nsel = Rn > 0 ? select_smallest(S.skey, L, Rn, spos, S.hist, s_state) : 0;
+  phase_mark(5);
   {
     // per-head max over the selected logits: thread-local, warp, then block
     double* wm = S.scratch;             // [kU2Warps][gs] (gs <= 8 here) as doubles
@@ -1299,6 +1320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
       }
     }
     __syncthreads();
+    phase_mark(6);
     float* red = reinterpret_cast<float*>(S.skey);   // keys are dead on rank 0 now
     for (int i = tid; i < kU2Warps * gs * D; i += blockDim.x) red[i] = 0.f;
     const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
@@ -1338,6 +1360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
           [&](int hh, int t) { return S.wts[hh * kAttnChunk + t]; }, red + (int64_t)warp * gs * D);
       __syncthreads();
     }
+    phase_mark(7);
     // exact merge with the static partials
     bool none = false;
     for (int i = tid; i < gs * D; i += blockDim.x) {
@@ -1375,6 +1398,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
     }
     if (none) set_flag(p.flags, kFlagNoTokens);
   }
+  phase_mark(8);
   if (p.selected)
     for (int r = tid; r < p.c_prime; r += blockDim.x) p.selected[(int64_t)u * p.c_prime + r] = S.sel[r];
   if (p.recall_len && tid == 0) p.recall_len[u] = L;
@@ -1590,6 +1614,16 @@ int launch_unit2(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
     case 256: return launch_unit2_t<__nv_bfloat16, 256>(p, st);
   }
   return CTKV_ESHAPE;
+}
+int phase_timing(int on, unsigned long long* out, int n) {
+  if (out != nullptr) {
+    const int m = n < kPhaseCtas * kPhases ? n : kPhaseCtas * kPhases;
+    if (cudaMemcpyFromSymbol(out, g_phase, sizeof(unsigned long long) * m) != cudaSuccess) return CTKV_ECUDA;
+  }
+  if (on >= 0) {
+    if (cudaMemcpyToSymbol(g_phase_on, &on, sizeof(int)) != cudaSuccess) return CTKV_ECUDA;
+  }
+  return 0;
 }
 int static_tok_for(int dtype) { return dtype == CTKV_BF16 ? static_tok<__nv_bfloat16>() : static_tok<float>(); }
 int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st) {

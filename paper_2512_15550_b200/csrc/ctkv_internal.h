@@ -84,6 +84,7 @@ int launch_unit(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_unit2(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 size_t unit2_smem_bytes(const DecodeParams& p, int D);
 int static_tok_for(int dtype);
+int phase_timing(int on, unsigned long long* out, int n);
 int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const double* la,
                   const float* ob, const double* mb, const double* lb, float* out, double* mo,
