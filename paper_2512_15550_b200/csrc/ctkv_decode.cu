@@ -91,33 +91,47 @@ __device__ __forceinline__ double lane_dot(const float* qs, int hh, const float*
 
 // Per-warp weighted row sums: red_warp[hh][:] += sum_t w(hh,t) * row(t)[:]
 // for t in [0,n) strided over the block's warps.  Heads are processed four
-// at a time so the accumulators stay in registers for any group size.
+// at a time so the accumulators stay in registers for any group size; UN
+// row passes are loaded before any is consumed (memory-level parallelism).
 template <typename T, int D, typename RowFn, typename WFn>
 __device__ void accum_weighted_rows(int n, int gs, RowFn rowfn, WFn wfn, float* red_warp) {
   using R = Row<T, D>;
+  constexpr int UN = 4;
   const int nwarps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int sub = lane % R::LPR, rw = lane / R::LPR;
+  const int step = nwarps * R::RPW;
   for (int h0 = 0; h0 < gs; h0 += 4) {
     float acc[4][R::EPL];
 #pragma unroll
     for (int hh = 0; hh < 4; ++hh)
 #pragma unroll
       for (int j = 0; j < R::EPL; ++j) acc[hh][j] = 0.f;
-    for (int base = warp * R::RPW; base < n; base += nwarps * R::RPW) {
-      const int t = base + rw;
-      if (t < n) {
-        const T* row = rowfn(t);
-        if (row != nullptr) {
-          float vv[R::EPL];
-          load_row_slice<T, D>(row, sub, vv);
+    for (int base = warp * R::RPW; base < n; base += step * UN) {
+      float vv[UN][R::EPL];
+      bool ok[UN];
 #pragma unroll
-          for (int hh = 0; hh < 4; ++hh) {
-            if (h0 + hh < gs) {
-              const float w = wfn(h0 + hh, t);
+      for (int u2 = 0; u2 < UN; ++u2) {
+        const int t = base + u2 * step + rw;
+        const T* row = t < n ? rowfn(t) : nullptr;
+        ok[u2] = row != nullptr;
+        if (ok[u2]) {
+          load_row_slice<T, D>(row, sub, vv[u2]);
+        } else {
 #pragma unroll
-              for (int j = 0; j < R::EPL; ++j) acc[hh][j] = fmaf(w, vv[j], acc[hh][j]);
-            }
+          for (int j = 0; j < R::EPL; ++j) vv[u2][j] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u2 = 0; u2 < UN; ++u2) {
+        if (!ok[u2]) continue;
+        const int t = base + u2 * step + rw;
+#pragma unroll
+        for (int hh = 0; hh < 4; ++hh) {
+          if (h0 + hh < gs) {
+            const float w = wfn(h0 + hh, t);
+#pragma unroll
+            for (int j = 0; j < R::EPL; ++j) acc[hh][j] = fmaf(w, vv[u2][j], acc[hh][j]);
           }
         }
       }
@@ -943,6 +957,7 @@ __global__ void __launch_bounds__(kUnitThreads, 1) unit_kernel(DecodeParams p) {
 constexpr int kU2Threads = 512;
 constexpr int kU2Warps = kU2Threads / 32;
 constexpr int kMaxParLists = 8;   // C' lists unioned in parallel (else sequentially)
+constexpr int kUnionItems = 16;   // union elements per thread held in registers
 
 struct U2Smem {
   int32_t* sel;      // [c_prime]
@@ -985,7 +1000,8 @@ __host__ __device__ inline size_t u2_layout(const DecodeParams& p, int D, U2Smem
   t.wts = reinterpret_cast<float*>(take(sizeof(float) * p.gs * kAttnChunk));
   t.spml = reinterpret_cast<double*>(take(sizeof(double) * 2 * (p.ns > 1 ? p.ns : 1) * p.gs));
   t.hist = reinterpret_cast<int*>(take(sizeof(int) * 256));
-  t.scratch = reinterpret_cast<double*>(take(sizeof(double) * 128));
+  const int nscr = p.gs * (p.ns + 1) > 128 ? p.gs * (p.ns + 1) : 128;
+  t.scratch = reinterpret_cast<double*>(take(sizeof(double) * nscr));
   if (s) *s = t;
   return off;
 }
@@ -1099,12 +1115,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
     const int M = p.cos_blocks_per_unit * p.ncand;
     const double* cv = p.cval + (int64_t)u * M;
     const int32_t* ci = p.cidx + (int64_t)u * M;
+    constexpr int KR = 8;                 // candidates per lane kept in registers
+    uint64_t rk[KR];
+    int ri[KR];
+#pragma unroll
+    for (int r = 0; r < KR; ++r) {
+      const int m = lane + 32 * r;
+      rk[r] = m < M ? okey64(cv[m]) : 0ull;
+      ri[r] = m < M ? ci[m] : INT32_MAX;
+    }
     uint64_t prev_key = ~0ull;
     int prev_idx = -1;
     for (int r = 0; r < p.c_prime; ++r) {
       uint64_t bk = 0;
       int bidx = INT32_MAX;
-      for (int m = lane; m < M; m += 32) {
+#pragma unroll
+      for (int x = 0; x < KR; ++x) {
+        const uint64_t k = rk[x];
+        const int i = ri[x];
+        const bool below = k < prev_key || (k == prev_key && i > prev_idx);
+        if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
+      }
+      for (int m = lane + 32 * KR; m < M; m += 32) {   // only when M > 256
         const uint64_t k = okey64(cv[m]);
         const int i = ci[m];
         const bool below = k < prev_key || (k == prev_key && i > prev_idx);
@@ -1127,43 +1159,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
   // ---- 2. union of the selected lists, first occurrence kept -------------
   int L = 0;
   const int nwords = (int)((total + 31) >> 5);
-  if (p.c_prime <= kMaxParLists) {
+  if (p.c_prime <= kMaxParLists && p.c_prime * p.rho <= kU2Threads * kUnionItems) {
     // every list marks its own bitmap, then an id of list j survives iff no
-    // earlier list holds it; one ordered scan compacts (list, position) order
+    // earlier list holds it.  Warp w owns the contiguous element range
+    // [w*P, (w+1)*P) in (list, position) order, lane-interleaved, so ballots
+    // give each survivor its rank without a block-wide scan per list.
     const int nb = p.c_prime;
-    for (int i = tid; i < nb * p.bitmap_words; i += blockDim.x) S.areaA[i] = 0u;
-    __syncthreads();
     const int n = nb * p.rho;
-    for (int o = tid; o < n; o += blockDim.x) {
-      const int j = o / p.rho;
-      const int id = p.lists[((int64_t)u * p.C + S.sel[j]) * p.rho + (o - j * p.rho)];
-      if (id == kEmpty) continue;
-      if (id < 0 || id >= total) { set_flag(p.flags, kFlagIdRange); continue; }
-      atomicOr(&S.areaA[j * p.bitmap_words + (id >> 5)], 1u << (id & 31));
+    for (int i = tid; i < nb * p.bitmap_words; i += blockDim.x) S.areaA[i] = 0u;
+    const int P = ((n + kU2Warps - 1) / kU2Warps + 31) & ~31;
+    const int nit = P / 32;
+    int ids[kUnionItems];
+    int lst[kUnionItems];
+#pragma unroll
+    for (int it = 0; it < kUnionItems; ++it) {
+      ids[it] = kEmpty;
+      lst[it] = 0;
+      const int o = warp * P + it * 32 + lane;
+      if (it < nit && o < n) {
+        const int j = o / p.rho;
+        int id = p.lists[((int64_t)u * p.C + S.sel[j]) * p.rho + (o - j * p.rho)];
+        if (id != kEmpty && (id < 0 || id >= total)) { set_flag(p.flags, kFlagIdRange); id = kEmpty; }
+        ids[it] = id;
+        lst[it] = j;
+      }
+    }
+    __syncthreads();   // bitmaps cleared
+#pragma unroll
+    for (int it = 0; it < kUnionItems; ++it)
+      if (ids[it] != kEmpty)
+        atomicOr(&S.areaA[lst[it] * p.bitmap_words + (ids[it] >> 5)], 1u << (ids[it] & 31));
+    __syncthreads();
+    int wcount = 0;
+    unsigned keepm[kUnionItems];
+#pragma unroll
+    for (int it = 0; it < kUnionItems; ++it) {
+      bool keep = ids[it] != kEmpty;
+      if (keep)
+        for (int j2 = 0; j2 < lst[it]; ++j2)
+          keep = keep && !((S.areaA[j2 * p.bitmap_words + (ids[it] >> 5)] >> (ids[it] & 31)) & 1u);
+      keepm[it] = __ballot_sync(0xffffffffu, keep);
+      wcount += __popc(keepm[it]);
+    }
+    int* wtot = reinterpret_cast<int*>(S.scratch);
+    if (lane == 0) wtot[warp] = wcount;
+    __syncthreads();
+    int base = 0;
+    for (int w = 0; w < warp; ++w) base += wtot[w];
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < kU2Warps; ++w) t += wtot[w];
+      wtot[kU2Warps] = t;
+    }
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int it = 0; it < kUnionItems; ++it) {
+      if ((keepm[it] >> lane) & 1u) S.rec[base + __popc(keepm[it] & lt)] = ids[it];
+      base += __popc(keepm[it]);
     }
     __syncthreads();
-    const int per = (n + blockDim.x - 1) / blockDim.x;
-    const int o0 = tid * per;
-    int cnt = 0;
-    uint64_t keep = 0;   // per <= 64: n = C' * rho <= 8 * 4096
-    for (int e = 0; e < per; ++e) {
-      const int o = o0 + e;
-      if (o >= n) break;
-      const int j = o / p.rho;
-      const int id = p.lists[((int64_t)u * p.C + S.sel[j]) * p.rho + (o - j * p.rho)];
-      if (id == kEmpty || id < 0 || id >= total) continue;
-      bool dup = false;
-      for (int j2 = 0; j2 < j; ++j2) dup |= (S.areaA[j2 * p.bitmap_words + (id >> 5)] >> (id & 31)) & 1u;
-      if (!dup) { keep |= 1ull << e; ++cnt; }
-    }
-    int tot;
-    int pos = block_exclusive_scan(cnt, &tot, S.scratch);
-    for (int e = 0; e < per; ++e)
-      if (keep & (1ull << e)) {
-        const int o = o0 + e, j = o / p.rho;
-        S.rec[pos++] = p.lists[((int64_t)u * p.C + S.sel[j]) * p.rho + (o - j * p.rho)];
-      }
-    L = tot;
+    L = wtot[kU2Warps];
     __syncthreads();
   } else {
     uint32_t* bitmap = S.areaA;
@@ -1201,7 +1256,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
   if (rank == 0)
     for (int i = tid; i < p.ns * gs * D; i += blockDim.x) spo[i] = p.po[pbase * gs * D + i];
 
-  // ---- 3. rerank logits for this rank's half (row per thread) ------------
+  // ---- 3. rerank logits for this rank's half -------------------------------
+  // 8 lanes per key row (each lane two 16-byte chunks, so a lane group reads
+  // one contiguous 128-byte line per load), f32 chunk partials from exact
+  // bf16 products, f64 across chunks and lanes.
   double* lg = p.logits + (int64_t)u * gs * p.lmax;
   uint64_t* peer_skey = cl.map_shared_rank(S.skey, rank ^ 1);
   {
@@ -1209,44 +1267,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
     const int lo = rank ? half : 0, hi = rank ? L : half;
     const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
     const double scale = 1.0 / sqrt((double)D);
-    constexpr int VPR = D * int(sizeof(T)) / 16;
-    for (int t = lo + tid; t < hi; t += blockDim.x) {
-      const uint4* r4 = reinterpret_cast<const uint4*>(keys + (int64_t)S.rec[t] * D);
-      constexpr int KC = VPR < 8 ? VPR : 8;
-      double gmax = -INFINITY;
-#pragma unroll 1
-      for (int h0 = 0; h0 < gs; h0 += 8) {
-        double acc[8];
+    constexpr int VPR = D * int(sizeof(T)) / 16;     // 16 for d=128 bf16
+    constexpr int LPRL = 8;                          // lanes per row
+    constexpr int CPL = VPR / LPRL;                  // chunks per lane
+    constexpr int RPWL = 32 / LPRL;                  // rows per warp pass
+    constexpr int UNL = 2;                           // passes in flight
+    const int sub = lane % LPRL, rw = lane / LPRL;
+    const int stepw = kU2Warps * RPWL;
+    for (int base = lo + warp * RPWL; base < hi; base += stepw * UNL) {
+      uint4 raw[UNL][CPL];
+      int tt[UNL];
 #pragma unroll
-        for (int hh = 0; hh < 8; ++hh) acc[hh] = 0.0;
-#pragma unroll 1
-        for (int k0 = 0; k0 < VPR; k0 += KC) {
-          uint4 raw[KC];
+      for (int u2 = 0; u2 < UNL; ++u2) {
+        tt[u2] = base + u2 * stepw + rw;
+        if (tt[u2] < hi) {
+          const uint4* r4 = reinterpret_cast<const uint4*>(keys + (int64_t)S.rec[tt[u2]] * D);
 #pragma unroll
-          for (int k = 0; k < KC; ++k) raw[k] = ldg16(r4 + k0 + k);
+          for (int c = 0; c < CPL; ++c) raw[u2][c] = ldg16(r4 + c * LPRL + sub);
+        } else {
 #pragma unroll
-          for (int k = 0; k < KC; ++k) {
-#pragma unroll
-            for (int hh = 0; hh < 8; ++hh) {
-              if (h0 + hh < gs) {
-                const uint4 qq = reinterpret_cast<const uint4*>(qs + (h0 + hh) * D)[k0 + k];
-                acc[hh] += (double)bf16x8_dot(qq, raw[k], 0.f);
-              }
-            }
-          }
-        }
-#pragma unroll
-        for (int hh = 0; hh < 8; ++hh) {
-          if (h0 + hh < gs) {
-            const double a = acc[hh] * scale;
-            lg[(int64_t)(h0 + hh) * p.lmax + t] = a;
-            gmax = fmax(gmax, a);
-          }
+          for (int c = 0; c < CPL; ++c) raw[u2][c] = make_uint4(0, 0, 0, 0);
         }
       }
-      const uint64_t key = ((uint64_t)(~okey32((float)gmax)) << 32) | (uint32_t)t;
-      S.skey[t] = key;
-      peer_skey[t] = key;
+#pragma unroll
+      for (int u2 = 0; u2 < UNL; ++u2) {
+        double gmax = -INFINITY;
+        for (int hh = 0; hh < gs; ++hh) {
+          const uint4* q4 = reinterpret_cast<const uint4*>(qs + hh * D);
+          double a = 0.0;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) a += (double)bf16x8_dot(q4[c * LPRL + sub], raw[u2][c], 0.f);
+#pragma unroll
+          for (int o = 1; o < LPRL; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+          a *= scale;
+          if (sub == 0 && tt[u2] < hi) lg[(int64_t)hh * p.lmax + tt[u2]] = a;
+          gmax = fmax(gmax, a);
+        }
+        if (sub == 0 && tt[u2] < hi) {
+          const uint64_t key = ((uint64_t)(~okey32((float)gmax)) << 32) | (uint32_t)tt[u2];
+          S.skey[tt[u2]] = key;
+          peer_skey[tt[u2]] = key;
+        }
+      }
     }
     for (int t = L + tid; t < npad; t += blockDim.x) S.skey[t] = ~0ull;
   }
@@ -1361,29 +1423,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
       __syncthreads();
     }
     phase_mark(7);
-    // exact merge with the static partials
+    // exact merge with the static partials: per head the running max M and
+    // the split weights exp(m_j - M) once, then a weighted sum per element
+    double* wj = S.scratch;   // [gs][ns + 1]: w_static_j ..., w_sparse ; Ls at [gs*(ns+1)+hh]
+    const int ns = p.ns;
+    __syncthreads();
+    if (tid < gs) {
+      const int hh = tid;
+      double M = ls[hh] > 0.0 ? ms[hh] : -INFINITY;
+      for (int j = 0; j < ns; ++j)
+        if (S.spml[ns * gs + j * gs + hh] > 0.0) M = fmax(M, S.spml[j * gs + hh]);
+      double Ls = 0.0;
+      for (int j = 0; j < ns; ++j) {
+        const double lj = S.spml[ns * gs + j * gs + hh];
+        const double w = lj > 0.0 ? exp(S.spml[j * gs + hh] - M) : 0.0;
+        wj[hh * (ns + 1) + j] = w;
+        Ls += w * lj;
+      }
+      const double wsp = ls[hh] > 0.0 ? exp(ms[hh] - M) : 0.0;
+      wj[hh * (ns + 1) + ns] = wsp;
+      Ls += wsp * ls[hh];
+      ms[hh] = M;          // reuse: merged statistics
+      ls[hh] = Ls;
+    }
+    __syncthreads();
     bool none = false;
     for (int i = tid; i < gs * D; i += blockDim.x) {
       const int hh = i / D, e = i % D;
       float o0 = 0.f;
       for (int w = 0; w < kU2Warps; ++w) o0 += red[(int64_t)w * gs * D + i];
-      double M = ls[hh] > 0.0 ? ms[hh] : -INFINITY;
-      for (int j = 0; j < p.ns; ++j)
-        if (S.spml[p.ns * gs + j * gs + hh] > 0.0) M = fmax(M, S.spml[j * gs + hh]);
-      double Ls = 0.0, O = 0.0;
-      if (ls[hh] > 0.0) {
-        const double w = exp(ms[hh] - M);
-        Ls += w * ls[hh];
-        O += w * (double)o0;
-      }
-      for (int j = 0; j < p.ns; ++j) {
-        const double lj = S.spml[p.ns * gs + j * gs + hh];
-        if (lj > 0.0) {
-          const double w = exp(S.spml[j * gs + hh] - M);
-          Ls += w * lj;
-          O += w * (double)spo[(j * gs + hh) * D + e];
-        }
-      }
+      const double* wh = wj + hh * (ns + 1);
+      double O = wh[ns] * (double)o0;
+      for (int j = 0; j < ns; ++j) O += wh[j] * (double)spo[(j * gs + hh) * D + e];
+      const double Ls = ls[hh];
       const int64_t oh = (int64_t)bi * p.h + gi * gs + hh;
       if (Ls > 0.0) {
         p.out[oh * D + e] = (float)(O / Ls);
@@ -1392,7 +1464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
         none = true;
       }
       if (e == 0) {
-        if (p.row_max) p.row_max[oh] = M;
+        if (p.row_max) p.row_max[oh] = ms[hh];
         if (p.denom) p.denom[oh] = Ls;
       }
     }
