@@ -531,6 +531,299 @@ __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
   }
 }
 
+// ------------------------------------------------------------------------
+// v3 scan: persistent and warp-specialised.  One CTA per SM; warp 0 (one
+// lane) is a TMA-bulk producer that keeps kScanStages x 64 KB of the CTA's
+// next tasks in flight; warps 1..8 consume: cosine tasks (256 centroid rows,
+// one row per thread, + chunk-local top-C' candidates) and static-attention
+// tasks (128 tokens of K and V).  Tasks are dealt round-robin
+// (task = blockIdx.x + k * gridDim.x), cosine tasks first.
+// ------------------------------------------------------------------------
+
+constexpr int kScanStages = 3;
+constexpr int kStageBytes = 64 * 1024 + 2048;   // rows/K+V + the unit's query heads (gs<=8)
+constexpr int kScan3Threads = 32 + kScanRowsV2;  // producer warp + 8 consumer warps
+
+__device__ __forceinline__ void bar_arrive_local(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(bar)) : "memory");
+}
+__device__ __forceinline__ void cons_sync() {   // consumer warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(kScanRowsV2) : "memory");
+}
+
+template <typename T, int D>
+__device__ void scan3_issue(const DecodeParams& p, int task, int64_t t0, int64_t total,
+                            unsigned char* stage, uint64_t* full) {
+  constexpr int RB = D * int(sizeof(T));
+  const int ncos = p.U * p.cos_blocks_per_unit;
+  const int gs = p.gs;
+  const T* qsrc;
+  uint32_t bytes = 0;
+  unsigned char* qdst = stage + 64 * 1024;
+  if (task < ncos) {
+    const int CC = kScanRowsV2 / gs, cpu = p.cos_blocks_per_unit;
+    const int u = task / cpu, chunk = task % cpu;
+    const int bi = u / p.g, gi = u % p.g;
+    const int c0 = chunk * CC, nc = min(CC, p.C - c0);
+    qsrc = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
+    bytes = (uint32_t)(gs * nc * RB + gs * RB);
+    bar_expect(full, bytes);
+    const T* cent = static_cast<const T*>(p.cent);
+    for (int j = 0; j < gs; ++j)
+      bulk_g2s(stage + (size_t)j * CC * RB, cent + (((int64_t)bi * p.h + gi * gs + j) * p.C + c0) * D,
+               (uint32_t)(nc * RB), full);
+  } else {
+    constexpr int ST = static_tok<T>();
+    const int st = task - ncos;
+    const int u = st / p.ns, split = st % p.ns;
+    const int bi = u / p.g, gi = u % p.g;
+    qsrc = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
+    const StaticSpan span(total, p.init_len, p.local_len);
+    const int64_t i0 = (int64_t)split * ST;
+    const int nt = (int)max((int64_t)0, min((int64_t)ST, span.n_static - i0));
+    bytes = (uint32_t)(2 * nt * RB + gs * RB);
+    bar_expect(full, bytes);
+    const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
+    const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
+    T* Ks = reinterpret_cast<T*>(stage);
+    T* Vs = Ks + (size_t)ST * D;
+    const bool appending = p.k_new != nullptr;
+    int64_t i = i0;
+    const int64_t i1 = i0 + nt;
+    while (i < i1) {
+      const int64_t id = span.id(i);
+      const int64_t run_end = (i < span.n_init) ? min(i1, span.n_init) : i1;
+      int64_t n = run_end - i;
+      const bool has_new = appending && id <= t0 && t0 < id + n;
+      if (has_new) n = t0 - id;
+      if (n > 0) {
+        bulk_g2s(Ks + (size_t)(i - i0) * D, keys + id * D, (uint32_t)(n * RB), full);
+        bulk_g2s(Vs + (size_t)(i - i0) * D, vals + id * D, (uint32_t)(n * RB), full);
+      }
+      if (has_new) {
+        const int64_t at = i + n - i0;
+        bulk_g2s(Ks + (size_t)at * D, static_cast<const T*>(p.k_new) + (int64_t)u * D, RB, full);
+        bulk_g2s(Vs + (size_t)at * D, static_cast<const T*>(p.v_new) + (int64_t)u * D, RB, full);
+        n += 1;
+      }
+      i += n;
+    }
+  }
+  bulk_g2s(qdst, qsrc, (uint32_t)(gs * RB), full);
+}
+
+// consumer side of a cosine task (256 threads; rows already in `stage`)
+template <typename T, int D>
+__device__ void scan3_cos(const DecodeParams& p, int task, const unsigned char* stage,
+                          double* cosv, double* qn) {
+  const int ct = threadIdx.x - 32;            // consumer thread 0..255
+  const int gs = p.gs, CC = kScanRowsV2 / gs;
+  const int cpu = p.cos_blocks_per_unit;
+  const int u = task / cpu, chunk = task % cpu;
+  const int c0 = chunk * CC, nc = min(CC, p.C - c0);
+  const T* rows = reinterpret_cast<const T*>(stage);
+  const T* qs = reinterpret_cast<const T*>(stage + 64 * 1024);
+  if (ct < gs) {
+    double s = 0.0;
+    for (int e = 0; e < D; ++e) {
+      const double x = (double)to_f(qs[ct * D + e]);
+      s = fma(x, x, s);
+    }
+    qn[ct] = sqrt(s);
+  }
+  double dot = 0.0, nrm = 0.0;
+  const int j = ct / CC, c = ct % CC;
+  const bool live = j < gs && c < nc;
+  if (live) row_dot<T, D, true>(qs + j * D, rows + (size_t)ct * D, ct, dot, nrm);
+  cons_sync();
+  if (live) {
+    const double den = qn[j] * sqrt(nrm);
+    double cv;
+    if (den == 0.0) {
+      cv = 0.0;
+      set_flag(p.flags, kFlagDegenerate);
+    } else {
+      cv = fmin(fmax(dot / den, -1.0), 1.0);
+    }
+    cosv[ct] = cv;
+  }
+  cons_sync();
+  double* gv = cosv + kScanRowsV2;
+  if (ct < nc) {
+    double m = cosv[ct];
+    for (int jj = 1; jj < gs; ++jj) m = fmax(m, cosv[jj * CC + ct]);
+    p.gcos[(int64_t)u * p.C + c0 + ct] = m;
+    gv[ct] = m;
+  }
+  if (p.cval != nullptr) {
+    cons_sync();
+    if (ct < 32) {
+      const int lane = ct;
+      uint64_t prev_key = ~0ull;
+      int prev_idx = -1;
+      const int64_t base = ((int64_t)u * cpu + chunk) * p.ncand;
+      for (int r = 0; r < p.ncand; ++r) {
+        uint64_t bk = 0;
+        int bidx = INT32_MAX;
+        for (int cc = lane; cc < nc; cc += 32) {
+          const uint64_t k = okey64(gv[cc]);
+          const int i = c0 + cc;
+          const bool below = k < prev_key || (k == prev_key && i > prev_idx);
+          if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+          const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
+          if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
+        }
+        if (lane == 0) {
+          p.cval[base + r] = bidx == INT32_MAX ? -INFINITY : gv[bidx - c0];
+          p.cidx[base + r] = bidx;
+        }
+        prev_key = bk;
+        prev_idx = bidx;
+      }
+    }
+  }
+}
+
+// consumer side of a static-attention task
+template <typename T, int D>
+__device__ void scan3_static(const DecodeParams& p, int st, int64_t total,
+                             const unsigned char* stage, double* lg, float* w, double* ml) {
+  constexpr int ST = static_tok<T>();
+  const int ct = threadIdx.x - 32;
+  const int gs = p.gs;
+  const int u = st / p.ns, split = st % p.ns;
+  const StaticSpan span(total, p.init_len, p.local_len);
+  const int64_t i0 = (int64_t)split * ST;
+  const int nt = (int)max((int64_t)0, min((int64_t)ST, span.n_static - i0));
+  const int64_t slot = (int64_t)u * p.ns + split;
+  double* pm = p.pm + slot * gs;
+  double* pl = p.pl + slot * gs;
+  float* po = p.po + slot * gs * D;
+  if (nt == 0) {
+    for (int i = ct; i < gs * D; i += kScanRowsV2) po[i] = 0.f;
+    if (ct < gs) { pm[ct] = -INFINITY; pl[ct] = 0.0; }
+    return;
+  }
+  const T* Ks = reinterpret_cast<const T*>(stage);
+  const T* Vs = Ks + (size_t)ST * D;
+  const T* qs = reinterpret_cast<const T*>(stage + 64 * 1024);
+  const double scale = 1.0 / sqrt((double)D);
+  for (int pr = ct; pr < nt * gs; pr += kScanRowsV2) {
+    const int t = pr % nt, j = pr / nt;
+    double dot, nrm;
+    row_dot<T, D, false>(qs + j * D, Ks + (size_t)t * D, t, dot, nrm);
+    lg[j * ST + t] = dot * scale;
+  }
+  cons_sync();
+  const int warp = ct >> 5, lane = ct & 31;
+  for (int j = warp; j < gs; j += kScanRowsV2 / 32) {
+    double m = -INFINITY;
+    for (int t = lane; t < nt; t += 32) m = fmax(m, lg[j * ST + t]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    double l = 0.0;
+    for (int t = lane; t < nt; t += 32) {
+      const double e = exp(lg[j * ST + t] - m);
+      w[j * ST + t] = (float)e;
+      l += e;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) { ml[j] = m; ml[gs + j] = l; }
+  }
+  cons_sync();
+  for (int pr = ct; pr < gs * (D / 2); pr += kScanRowsV2) {
+    const int j = pr / (D / 2), e = 2 * (pr % (D / 2));
+    float a0 = 0.f, a1 = 0.f;
+    const float* wj = w + j * ST;
+    for (int t = 0; t < nt; ++t) {
+      const T* vr = Vs + (size_t)t * D + e;
+      a0 = fmaf(wj[t], to_f(vr[0]), a0);
+      a1 = fmaf(wj[t], to_f(vr[1]), a1);
+    }
+    po[j * D + e] = a0;
+    po[j * D + e + 1] = a1;
+  }
+  if (ct < gs) {
+    pm[ct] = ml[ct];
+    pl[ct] = ml[gs + ct];
+  }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kScan3Threads, 1) scan3_kernel(DecodeParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint64_t full[kScanStages], empty[kScanStages];
+  const int64_t t0 = p.total ? *p.total : p.id_bound;
+  const bool appending = p.k_new != nullptr;
+  const int64_t total = t0 + (appending ? 1 : 0);
+  const int ncos = p.do_cos ? p.U * p.cos_blocks_per_unit : 0;
+  const int ntasks = ncos + p.U * p.ns;
+  // per-task scratch after the stage ring
+  unsigned char* scratch = smem + (size_t)kScanStages * kStageBytes;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kScanStages; ++s) {
+      bar_init(&full[s], 1);
+      bar_init(&empty[s], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
+        bar_wait(&empty[stage], phase ^ 1);
+        scan3_issue<T, D>(p, task, t0, total, smem + (size_t)stage * kStageBytes, &full[stage]);
+        if (++stage == kScanStages) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    int stage = 0;
+    uint32_t phase = 0;
+    constexpr int ST = static_tok<T>();
+    double* cosv = reinterpret_cast<double*>(scratch);                 // [2 * 256]
+    double* qn = cosv + 2 * kScanRowsV2;                               // [8]
+    double* lg = qn + 8;                                               // [gs<=8][ST]
+    float* w = reinterpret_cast<float*>(lg + 8 * ST);                  // [gs][ST]
+    double* ml = reinterpret_cast<double*>(w + 8 * ST);                // [2][gs]
+    for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
+      bar_wait(&full[stage], phase);
+      const unsigned char* st = smem + (size_t)stage * kStageBytes;
+      if (task < ncos)
+        scan3_cos<T, D>(p, task, st, cosv, qn);
+      else
+        scan3_static<T, D>(p, task - ncos, total, st, lg, w, ml);
+      cons_sync();   // every consumer is done with the stage (and the scratch)
+      if (threadIdx.x == 32) bar_arrive_local(&empty[stage]);
+      if (++stage == kScanStages) { stage = 0; phase ^= 1; }
+    }
+  }
+  if (appending && blockIdx.x == 0) {
+    __syncthreads();
+    T* keys = static_cast<T*>(const_cast<void*>(p.keys));
+    T* vals = static_cast<T*>(const_cast<void*>(p.values));
+    const T* kn = static_cast<const T*>(p.k_new);
+    const T* vn = static_cast<const T*>(p.v_new);
+    for (int64_t i = threadIdx.x; i < (int64_t)p.U * D; i += blockDim.x) {
+      const int64_t uu = i / D, e = i % D;
+      keys[(uu * p.cap + t0) * D + e] = kn[i];
+      vals[(uu * p.cap + t0) * D + e] = vn[i];
+    }
+  }
+}
+
+template <typename T, int D>
+size_t scan3_smem() {
+  constexpr int ST = static_tok<T>();
+  return (size_t)kScanStages * kStageBytes + sizeof(double) * (2 * kScanRowsV2 + 8) +
+         sizeof(double) * 8 * ST + sizeof(float) * 8 * ST + sizeof(double) * 2 * 8;
+}
+
 template <typename T, int D>
 size_t scan2_smem(int gs) {
   constexpr int RB = D * int(sizeof(T));
@@ -1602,8 +1895,31 @@ size_t scan_smem_bytes(const DecodeParams& p, int D) {
   return std::max(cosb, attb);
 }
 
+static int num_sms_dev() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
 template <typename T, int D>
 static int launch_scan_t(const DecodeParams& p, int nblocks, cudaStream_t st) {
+  if (sizeof(T) == 2 && D <= 128 && p.gs <= 8) {
+    // persistent warp-specialised scan: one CTA per SM streaming its tasks
+    const size_t sm3 = scan3_smem<T, D>();
+    auto k3 = scan3_kernel<T, D>;
+    static bool set3 = false;
+    if (!set3) {
+      cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+      set3 = true;
+    }
+    const int grid = nblocks < num_sms_dev() ? nblocks : num_sms_dev();
+    if (grid > 0) k3<<<grid, kScan3Threads, sm3, st>>>(p);
+    return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+  }
   const size_t sm = scan2_smem<T, D>(p.gs);
   auto k = scan2_kernel<T, D>;
   static size_t configured = 0;
