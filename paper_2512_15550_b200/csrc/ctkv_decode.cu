@@ -26,6 +26,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -299,6 +300,24 @@ __device__ __forceinline__ void row_dot(const T* q, const T* row, int rot, doubl
   }
 }
 
+// |q_j| for the gs query heads staged in shared memory: one warp per head,
+// lanes stride over d, f64 squares reduced by shuffles (the reference's
+// np.linalg.norm, ck/tensor_ops.py:199-200)
+template <typename T, int D>
+__device__ __forceinline__ void query_norms(const T* qs, int gs, double* qn, int wid, int nw) {
+  const int lane = threadIdx.x & 31;
+  for (int j = wid; j < gs; j += nw) {
+    double s = 0.0;
+    for (int e = lane; e < D; e += 32) {
+      const double x = (double)to_f(qs[j * D + e]);
+      s = fma(x, x, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) qn[j] = sqrt(s);
+  }
+}
+
 template <typename T>
 __host__ __device__ constexpr int static_tok() { return sizeof(T) == 2 ? 128 : 64; }
 
@@ -328,14 +347,7 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = q[i];
   __syncthreads();
-  if (threadIdx.x < gs) {
-    double s = 0.0;
-    for (int e = 0; e < D; ++e) {
-      const double x = (double)to_f(qs[threadIdx.x * D + e]);
-      s = fma(x, x, s);
-    }
-    qn[threadIdx.x] = sqrt(s);
-  }
+  query_norms<T, D>(qs, gs, qn, threadIdx.x >> 5, blockDim.x >> 5);
   __syncthreads();
   for (int r = threadIdx.x; r < gs * CC; r += blockDim.x) {
     const int j = r / CC, c = r % CC;
@@ -623,14 +635,7 @@ __device__ void scan3_cos(const DecodeParams& p, int task, const unsigned char* 
   const int c0 = chunk * CC, nc = min(CC, p.C - c0);
   const T* rows = reinterpret_cast<const T*>(stage);
   const T* qs = reinterpret_cast<const T*>(stage + 64 * 1024);
-  if (ct < gs) {
-    double s = 0.0;
-    for (int e = 0; e < D; ++e) {
-      const double x = (double)to_f(qs[ct * D + e]);
-      s = fma(x, x, s);
-    }
-    qn[ct] = sqrt(s);
-  }
+  query_norms<T, D>(qs, gs, qn, ct >> 5, kScanRowsV2 / 32);
   double dot = 0.0, nrm = 0.0;
   const int j = ct / CC, c = ct % CC;
   const bool live = j < gs && c < nc;
@@ -1905,9 +1910,18 @@ static int num_sms_dev() {
   return n;
 }
 
+static int scan_variant() {   // CTKV_SCAN=2 forces the per-task scan (A/B testing)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CTKV_SCAN");
+    v = (e && e[0] == '2') ? 2 : 3;
+  }
+  return v;
+}
+
 template <typename T, int D>
 static int launch_scan_t(const DecodeParams& p, int nblocks, cudaStream_t st) {
-  if (sizeof(T) == 2 && D <= 128 && p.gs <= 8) {
+  if (sizeof(T) == 2 && D <= 128 && p.gs <= 8 && scan_variant() == 3) {
     // persistent warp-specialised scan: one CTA per SM streaming its tasks
     const size_t sm3 = scan3_smem<T, D>();
     auto k3 = scan3_kernel<T, D>;
