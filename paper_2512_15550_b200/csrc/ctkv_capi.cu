@@ -49,6 +49,10 @@ struct DecodeWs {
   double* logits;
   double* cval;
   int32_t* cidx;
+  int* ctr;
+  int32_t* recg;
+  int32_t* Lg;
+  uint64_t* keyg;
   size_t bytes;
 };
 
@@ -79,6 +83,11 @@ DecodeWs carve_decode(const ctkv_layout* L, int C, int lmax, int ns, void* base,
       c_prime > 0 ? (size_t)U * ((std::max(C, 1) + cc - 1) / cc) * ncand_for(L, c_prime) : 1;
   w.cval = reinterpret_cast<double*>(take(sizeof(double) * ncand_total));
   w.cidx = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * ncand_total));
+  const size_t lm = (size_t)std::max(lmax, 1);
+  w.ctr = reinterpret_cast<int*>(take(sizeof(int) * (3 + 4 * (size_t)U)));
+  w.recg = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U * lm));
+  w.Lg = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U));
+  w.keyg = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (size_t)U * lm));
   w.bytes = off;
   return w;
 }
@@ -242,6 +251,10 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.cval = w.cval;
   p.cidx = w.cidx;
   p.ncand = ncand_for(L, A->c_prime);
+  p.ctr = w.ctr;
+  p.recg = w.recg;
+  p.Lg = w.Lg;
+  p.keyg = w.keyg;
   p.out = A->out;
   p.row_max = A->row_max;
   p.denom = A->denom;
@@ -257,6 +270,13 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   if (!v2) p.cval = nullptr;   // the f64 unit kernel selects from gcos directly
   if (!v2 && unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // v4: one persistent layer kernel with a dependency-ordered task queue
+  const bool v4 = v2 && L->head_dim <= 128 && A->c_prime <= 64 && lmax <= 8192 &&
+                  ctkv::decode_variant() == 4;
+  if (v4) {
+    if (phase & 1) return launch_layer(p, L->dtype, L->head_dim, st);
+    return CTKV_OK;
+  }
   const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
   if (phase & 1)
     if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;

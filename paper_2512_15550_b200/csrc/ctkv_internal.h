@@ -58,6 +58,11 @@ struct DecodeParams {
   double* cval;     // [U][cos_blocks_per_unit][ncand] chunk top-C' cosines
   int32_t* cidx;    // [U][cos_blocks_per_unit][ncand] their centroid slots
   int ncand;        // min(C', centroids per cos chunk)
+  // layer kernel (v4) task-queue state
+  int* ctr;         // [3 + 4U] claim, started, dcu_done, cos/union/static/logit done per unit
+  int32_t* recg;    // [U][lmax] recalled ids, first-occurrence order
+  int32_t* Lg;      // [U] recall lengths
+  uint64_t* keyg;   // [U][lmax] packed (score, position) rerank keys
   // staged io
   const int32_t* rec_in;
   const int32_t* len_in;
@@ -85,6 +90,8 @@ int launch_unit2(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 size_t unit2_smem_bytes(const DecodeParams& p, int D);
 int static_tok_for(int dtype);
 int phase_timing(int on, unsigned long long* out, int n);
+int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st);
+int decode_variant();
 int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const double* la,
                   const float* ob, const double* mb, const double* lb, float* out, double* mo,
