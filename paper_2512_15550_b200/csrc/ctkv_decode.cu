@@ -2633,11 +2633,11 @@ static int num_sms_dev() {
   return n;
 }
 
-static int scan_variant() {   // CTKV_SCAN=2 forces the per-task scan (A/B testing)
+static int scan_variant() {   // CTKV_SCAN=3 selects the persistent scan3 (A/B testing)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("CTKV_SCAN");
-    v = (e && e[0] == '2') ? 2 : 3;
+    v = (e && e[0] == '3') ? 3 : 2;
   }
   return v;
 }
