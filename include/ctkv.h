@@ -82,6 +82,8 @@ typedef struct ctkv_index {
   int32_t* lists;       /* [b,g,C,rho] int32, -1 = empty */
   int64_t* fifo_head;   /* [b] FIFO cursor (ck/index.py:55,121,133) */
   int32_t* sync;        /* [1+b] int32 scratch, zero-initialised once, owned by the index */
+  float* cnorm;         /* [b,h,C] |centroid| (f32 of the exact f64 norm) or NULL; kept
+                           current by ctkv_centroid_norms and every DCU write */
   int32_t capacity;     /* C */
   int32_t rho;          /* list length */
 } ctkv_index;
@@ -143,6 +145,12 @@ int ctkv_build_lists(const ctkv_layout* L, const void* centroids, const void* ke
                      int64_t off_begin, int64_t n_off, int32_t capacity, int32_t rho,
                      int32_t mode, int32_t* lists, int32_t* flags, void* workspace,
                      size_t workspace_bytes, void* stream);
+
+/* |c| for every centroid row (the recall cosine's denominator,
+ * ck/tensor_ops.py:199-200), exact f64 from the stored values, rounded to
+ * f32: cnorm [b,h,C]. */
+int ctkv_centroid_norms(const ctkv_layout* L, const void* centroids, int32_t capacity,
+                        float* cnorm, void* stream);
 
 /* ---- decode (ck/retrieval.py) --------------------------------------------- */
 

@@ -231,6 +231,7 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.lists = I.lists;
   p.fifo = I.fifo_head;
   p.sync = I.sync;
+  p.cnorm = I.cnorm;
   p.C = I.capacity;
   p.rho = I.rho;
   p.q = A->query;
@@ -303,6 +304,7 @@ int ctkv_recall(const ctkv_layout* L, ctkv_index I, int64_t id_bound, const void
   p.bitmap_words = (int)((id_bound + 31) / 32);
   p.cent = I.centroids;
   p.lists = I.lists;
+  p.cnorm = I.cnorm;
   p.C = I.capacity;
   p.rho = I.rho;
   p.q = query;
@@ -366,6 +368,7 @@ int ctkv_fifo_update(const ctkv_layout* L, ctkv_index I, const void* query,
   p.lists = I.lists;
   p.fifo = I.fifo_head;
   p.sync = I.sync;
+  p.cnorm = I.cnorm;
   p.C = I.capacity;
   p.rho = I.rho;
   p.q = query;
@@ -455,6 +458,15 @@ int ctkv_topk_rows(const float* values, int64_t rows, int64_t n, int32_t k, int3
   if (k > 8192) return CTKV_ECONFIG;
   return launch_topk_rows(values, rows, n, k, idx, workspace, workspace_bytes,
                           static_cast<cudaStream_t>(stream));
+}
+
+int ctkv_centroid_norms(const ctkv_layout* L, const void* centroids, int32_t capacity,
+                        float* cnorm, void* stream) {
+  if (int rc = check_layout(L)) return rc;
+  if (!centroids || !cnorm || capacity < 0) return CTKV_ECONFIG;
+  const int64_t rows = (int64_t)L->batch * L->query_heads * capacity;
+  return launch_centroid_norms(L->dtype, L->head_dim, centroids, rows, cnorm,
+                               static_cast<cudaStream_t>(stream));
 }
 
 int ctkv_debug_phase_timing(int32_t on, uint64_t* host_out, int32_t n) {

@@ -318,6 +318,23 @@ __device__ __forceinline__ void query_norms(const T* qs, int gs, double* qn, int
   }
 }
 
+// DCU helper: |q_h| of the gs query heads written next to their centroid rows
+template <typename T, int D>
+__device__ void write_slot_norms(const DecodeParams& p, const T* q, int bi, int gi, int64_t slot) {
+  if (p.cnorm == nullptr) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int hh = warp; hh < p.gs; hh += nw) {
+    double s = 0.0;
+    for (int e = lane; e < D; e += 32) {
+      const double v = (double)to_f(q[hh * D + e]);
+      s = fma(v, v, s);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) p.cnorm[((int64_t)bi * p.h + gi * p.gs + hh) * p.C + slot] = (float)sqrt(s);
+  }
+}
+
 template <typename T>
 __host__ __device__ constexpr int static_tok() { return sizeof(T) == 2 ? 128 : 64; }
 
@@ -354,8 +371,15 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
     if (c >= nc) continue;
     bar_wait(&bars[j], 0);
     double dot, nrm;
-    row_dot<T, D, true>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
-    const double den = qn[j] * sqrt(nrm);
+    double cn;
+    if (p.cnorm != nullptr) {
+      row_dot<T, D, false>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
+      cn = (double)__ldg(p.cnorm + ((int64_t)bi * p.h + gi * gs + j) * p.C + c0 + c);
+    } else {
+      row_dot<T, D, true>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
+      cn = sqrt(nrm);
+    }
+    const double den = qn[j] * cn;
     double cv;
     if (den == 0.0) {
       cv = 0.0;
@@ -639,7 +663,16 @@ __device__ void scan3_cos(const DecodeParams& p, int task, const unsigned char* 
   double dot = 0.0, nrm = 0.0;
   const int j = ct / CC, c = ct % CC;
   const bool live = j < gs && c < nc;
-  if (live) row_dot<T, D, true>(qs + j * D, rows + (size_t)ct * D, ct, dot, nrm);
+  const int bi3 = u / p.g, gi3 = u % p.g;
+  if (live) {
+    if (p.cnorm != nullptr) {
+      row_dot<T, D, false>(qs + j * D, rows + (size_t)ct * D, ct, dot, nrm);
+      nrm = (double)__ldg(p.cnorm + ((int64_t)bi3 * p.h + gi3 * gs + j) * p.C + c0 + c);
+      nrm *= nrm;
+    } else {
+      row_dot<T, D, true>(qs + j * D, rows + (size_t)ct * D, ct, dot, nrm);
+    }
+  }
   cons_sync();
   if (live) {
     const double den = qn[j] * sqrt(nrm);
@@ -1134,6 +1167,7 @@ __global__ void __launch_bounds__(kUnitThreads, 1) unit_kernel(DecodeParams p) {
       const int hh = i / D, e = i % D;
       cent[(((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D + e] = q[i];
     }
+    write_slot_norms<T, D>(p, q, bi, gi, slot);
   }
 
   // ---- 6. sparse attention over the top rho' (or the whole recall set) ---
@@ -1639,6 +1673,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
         const int hh = i / D, e = i % D;
         cent[(((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D + e] = q[i];
       }
+      write_slot_norms<T, D>(p, q, bi, gi, slot);
     }
     if (p.sparse_ids)
       for (int i = tid; i < p.sparse_cap; i += blockDim.x)
@@ -1891,8 +1926,15 @@ __device__ void l_cos(const DecodeParams& p, int task, unsigned char* smem, uint
     if (c >= nc) continue;
     bar_wait(&bars[j], (ph >> j) & 1u);
     double dot, nrm;
-    row_dot<T, D, true>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
-    const double den = qn[j] * sqrt(nrm);
+    double cn;
+    if (p.cnorm != nullptr) {
+      row_dot<T, D, false>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
+      cn = (double)__ldcg(p.cnorm + ((int64_t)bi * p.h + gi * gs + j) * p.C + c0 + c);
+    } else {
+      row_dot<T, D, true>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
+      cn = sqrt(nrm);
+    }
+    const double den = qn[j] * cn;
     double cv;
     if (den == 0.0) {
       cv = 0.0;
@@ -2407,6 +2449,7 @@ __device__ void l_dcu(const DecodeParams& p, int u, int64_t t0, const LayerPlan&
       const int hh = i / D, e = i % D;
       cent[(((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D + e] = q[i];
     }
+    write_slot_norms<T, D>(p, q, bi, gi, slot);
   }
   if (p.sparse_ids)
     for (int i = tid; i < p.sparse_cap; i += blockDim.x)
@@ -2785,6 +2828,38 @@ int decode_variant() {   // CTKV_DECODE=2 forces the two-kernel path (A/B testin
     v = (e && e[0] == '2') ? 2 : 4;
   }
   return v;
+}
+
+// |row| for rows of D elements: one warp per row, f64 squares (exact for
+// bf16 and f32 inputs), rounded to f32
+template <typename T, int D>
+__global__ void row_norms_kernel(const T* __restrict__ rows, int64_t n, float* __restrict__ out) {
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const T* x = rows + r * D;
+  double s = 0.0;
+  for (int e = lane; e < D; e += 32) {
+    const double v = (double)to_f(x[e]);
+    s = fma(v, v, s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[r] = (float)sqrt(s);
+}
+
+template <typename T, int D>
+static int launch_norms_t(const void* cent, int64_t rows, float* out, cudaStream_t st) {
+  if (rows == 0) return 0;
+  const int64_t threads = rows * 32;
+  row_norms_kernel<T, D><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(
+      static_cast<const T*>(cent), rows, out);
+  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+}
+
+int launch_centroid_norms(int dtype, int D, const void* cent, int64_t rows, float* out,
+                          cudaStream_t st) {
+  return CTKV_DISPATCH(dtype, D, launch_norms_t, cent, rows, out, st);
 }
 
 int static_tok_for(int dtype) { return dtype == CTKV_BF16 ? static_tok<__nv_bfloat16>() : static_tok<float>(); }

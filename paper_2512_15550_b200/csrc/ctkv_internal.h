@@ -37,6 +37,7 @@ struct DecodeParams {
   int32_t* lists;
   int64_t* fifo;
   int32_t* sync;
+  float* cnorm;       // [b,h,C] centroid norms (nullable)
   int C, rho;
   // step
   const void* q;
@@ -92,6 +93,7 @@ int static_tok_for(int dtype);
 int phase_timing(int on, unsigned long long* out, int n);
 int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int decode_variant();
+int launch_centroid_norms(int dtype, int D, const void* cent, int64_t rows, float* out, cudaStream_t st);
 int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const double* la,
                   const float* ob, const double* mb, const double* lb, float* out, double* mo,

@@ -53,6 +53,7 @@ class QueryCentroidIndex:
         if id_bound is None:
             id_bound = int(self.lists_dev.max().item()) + 1 if self.lists_dev.numel() else 0
         self.id_bound = max(int(id_bound), 0)
+        self._compute_norms()
 
     # -- views -----------------------------------------------------------------
 
@@ -73,7 +74,16 @@ class QueryCentroidIndex:
 
     def desc(self) -> N.IndexDesc:
         return N.IndexDesc(self.cent.data_ptr(), self.lists_dev.data_ptr(),
-                           self.fifo_dev.data_ptr(), self.sync.data_ptr(), self.capacity, self.rho)
+                           self.fifo_dev.data_ptr(), self.sync.data_ptr(), self.cnorm.data_ptr(),
+                           self.capacity, self.rho)
+
+    def _compute_norms(self) -> None:
+        """|c| per centroid row (f64-exact, stored f32); kept current by the DCU."""
+        lay = self.layout
+        self.cnorm = torch.empty((lay.batch, lay.query_heads, self.capacity), dtype=torch.float32,
+                                 device=self.cent.device)
+        N.check(N.lib().ctkv_centroid_norms(self.ctkv_layout(), self.cent.data_ptr(), self.capacity,
+                                            self.cnorm.data_ptr(), N.stream_ptr()), "centroid norms")
 
     def ctkv_layout(self, store_capacity: int = 0, init_len: int = 0, local_len: int = 0):
         lay = self.layout
@@ -125,6 +135,7 @@ class QueryCentroidIndex:
         idx.fifo_dev = torch.zeros(b, dtype=torch.int64, device=cent.device)
         idx.sync = torch.zeros(1 + b, dtype=torch.int32, device=cent.device)
         idx.id_bound = store.total_tokens
+        idx._compute_norms()
         return idx
 
     # -- DCU (ck/index.py:103-133) -------------------------------------------------

@@ -42,7 +42,7 @@ def test_struct_layouts():
     # offsets of the C structs (x86-64 SysV): see include/ctkv.h
     assert ctypes.sizeof(N.Layout) == 40 and N.Layout.capacity.offset == 16
     assert ctypes.sizeof(N.StoreDesc) == 24
-    assert ctypes.sizeof(N.IndexDesc) == 40
+    assert ctypes.sizeof(N.IndexDesc) == 48
     assert N.StepArgs.out.offset == 40 and ctypes.sizeof(N.StepArgs) == 112
 
 

@@ -108,6 +108,9 @@ def test_fused_decode_matches_reference(name):
     np.testing.assert_array_equal(index.lists, arr["lists_final"])
     np.testing.assert_array_equal(index.centroid_queries, arr["centroids_final"])
     np.testing.assert_array_equal(index.fifo_head, arr["step_fifo_head"][-1])
+    # the cached centroid norms follow every DCU write
+    ref_norm = torch.linalg.norm(index.cent.double(), dim=-1).float()
+    torch.testing.assert_close(index.cnorm, ref_norm, rtol=1e-6, atol=0)
 
 
 # ---------------------------------------------------------------------------
@@ -364,6 +367,8 @@ def test_96k_unit_properties_bf16():
     assert torch.isfinite(outs).all()
     store.check_partition()
     index.check_lists(store)
+    torch.testing.assert_close(index.cnorm, torch.linalg.norm(index.cent.double(), dim=-1).float(),
+                               rtol=1e-6, atol=0)
 
 
 def test_96k_tensor_core_build_matches_exact_within_tie_window():
