@@ -62,6 +62,16 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu summary
+    (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)[kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -415,12 +425,13 @@ def main():
                                                     "retrieve, attend, DCU)",
                           "achieved": layer_bytes / (scan_ms * 1e-3) / 1e9, "peak": hbm,
                           "peak_kind": peak_kind, "unit": "GB/s",
-                          "frac": layer_bytes / (scan_ms * 1e-3) / 1e9 / hbm, "traffic": None,
+                          "frac": layer_bytes / (scan_ms * 1e-3) / 1e9 / hbm,
+                          "traffic": ncu_traffic("ctkv::layer_kernel"),
                           "bytes_per_launch": layer_bytes, "ms_per_launch": scan_ms}
                          if fused else
                          {"bound": "hbm", "kernel": "scan_kernel (centroid cosine + static attention)",
                           "achieved": scan_gbs, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                          "frac": scan_gbs / hbm, "traffic": None,
+                          "frac": scan_gbs / hbm, "traffic": ncu_traffic("ctkv::scan2_kernel"),
                           "bytes_per_launch": scan_bytes, "ms_per_launch": scan_ms}),
             "kernels": {
                 ("layer_kernel" if fused else "scan_kernel"):

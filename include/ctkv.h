@@ -162,11 +162,17 @@ size_t ctkv_decode_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32
 int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctkv_step_args* A,
                      void* workspace, size_t workspace_bytes, void* stream);
 
-/* Same step split by kernel: phase 1 = scan kernel (cosine vs all
- * centroids + static-partition attention partials + append), phase 2 =
- * unit kernel (select, union, rerank, order, DCU, sparse attention,
- * merge), 3 = both.  Lets a caller time each kernel with events or place
- * other work between them; phase 2 must follow phase 1 of the same step. */
+/* Same step split by kernel.  `phase` is a bit set: 1 = scan kernel
+ * (cosine vs all centroids + static-partition attention partials +
+ * append); 2 = unit kernels (select, union, rerank, sparse attention,
+ * merge) followed by the tail (ordering, FIFO DCU, sparse ids, cursor and
+ * total advance); 8 = with 2, leave the tail out; 4 = the tail only.  3 is
+ * the whole step.  Phase 2 must follow phase 1 of the same step; a
+ * deferred tail (4) must follow that step's phase 2 and precede the next
+ * step's phase 1 for the same layer, and may run on another stream
+ * concurrently with other layers' work (it writes only this layer's index,
+ * total and outputs, and reads this call's workspace).  Paths without a
+ * separate tail run it inside phase 2 and treat 4 as a no-op. */
 int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
                            const ctkv_step_args* A, int32_t phase, void* workspace,
                            size_t workspace_bytes, void* stream);

@@ -53,6 +53,11 @@ struct DecodeWs {
   int32_t* recg;
   int32_t* Lg;
   uint64_t* keyg;
+  int* uctr;
+  int32_t* wsel;
+  float* apo;
+  double* apl;
+  double* wmax;
   size_t bytes;
 };
 
@@ -88,6 +93,11 @@ DecodeWs carve_decode(const ctkv_layout* L, int C, int lmax, int ns, void* base,
   w.recg = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U * lm));
   w.Lg = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U));
   w.keyg = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (size_t)U * lm));
+  w.uctr = reinterpret_cast<int*>(take(sizeof(int) * 4 * (size_t)U));
+  w.wsel = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U * lm));
+  w.apo = reinterpret_cast<float*>(take(sizeof(float) * (size_t)U * 8 * gs * d));
+  w.apl = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * 8 * gs));
+  w.wmax = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * gs));
   w.bytes = off;
   return w;
 }
@@ -206,7 +216,7 @@ int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctk
 int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
                            const ctkv_step_args* A, int32_t phase, void* workspace,
                            size_t workspace_bytes, void* stream) {
-  if (phase < 1 || phase > 3) return CTKV_ECONFIG;
+  if (phase < 1 || phase > 15) return CTKV_ECONFIG;
   if (int rc = check_layout(L)) return rc;
   if (!A || !A->query || !A->out || !S.keys || !S.values || !S.total) return CTKV_ECONFIG;
   if (I.capacity < 1) return CTKV_ECONFIG;                            // "recall: empty index"
@@ -256,6 +266,11 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.recg = w.recg;
   p.Lg = w.Lg;
   p.keyg = w.keyg;
+  p.uctr = w.uctr;
+  p.wsel = w.wsel;
+  p.apo = w.apo;
+  p.apl = w.apl;
+  p.wmax = w.wmax;
   p.out = A->out;
   p.row_max = A->row_max;
   p.denom = A->denom;
@@ -271,6 +286,17 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   if (!v2) p.cval = nullptr;   // the f64 unit kernel selects from gcos directly
   if (!v2 && unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // v5: wide unit pipeline; its tail (DCU, sparse ids, cursor/total) can be
+  // deferred (phase bit 8) and enqueued separately (phase 4) on another stream
+  if (v2 && ctkv::decode_variant() == 5 && wide_supported(p, L->dtype, L->head_dim)) {
+    const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
+    if (phase & 1)
+      if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;
+    const bool tail = (phase & 4) || ((phase & 2) && !(phase & 8));
+    const int what = ((phase & 2) ? 1 : 0) | (tail ? 2 : 0);
+    return what ? launch_wide(p, L->dtype, L->head_dim, what, st) : CTKV_OK;
+  }
+  p.uctr = nullptr;
   // v4: one persistent layer kernel with a dependency-ordered task queue
   const bool v4 = v2 && L->head_dim <= 128 && A->c_prime <= 64 && lmax <= 8192 &&
                   ctkv::decode_variant() == 4;

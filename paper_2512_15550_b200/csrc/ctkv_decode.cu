@@ -33,6 +33,7 @@
 #include "ctkv.h"
 #include "ctkv_common.cuh"
 #include "ctkv_internal.h"
+#include "ctkv_decode_dev.cuh"
 
 namespace ctkv {
 
@@ -59,14 +60,6 @@ constexpr int kUnitWarps = kUnitThreads / 32;
 constexpr int kAttnChunk = 512;     // sparse tokens per weight chunk
 constexpr int kAttnSplit = 64;      // tokens per attn_split_kernel CTA
 
-template <typename T>
-__device__ __forceinline__ const T* kv_row(const T* base, const T* fresh, int64_t cap, int unit,
-                                           int64_t id, int64_t t_new, int D) {
-  // the token appended by this very step is read from the caller's buffer
-  // (the store copy is written concurrently by scan block 0)
-  if (fresh != nullptr && id == t_new) return fresh + (int64_t)unit * D;
-  return base + ((int64_t)unit * cap + id) * D;
-}
 
 // this lane's partial of q_hh . row in f64 (products of f32-representable
 // values are exact in f64; only the summation order differs from numpy)
@@ -90,88 +83,11 @@ __device__ __forceinline__ double lane_dot(const float* qs, int hh, const float*
   return a;
 }
 
-// Per-warp weighted row sums: red_warp[hh][:] += sum_t w(hh,t) * row(t)[:]
-// for t in [0,n) strided over the block's warps.  Heads are processed four
-// at a time so the accumulators stay in registers for any group size; UN
-// row passes are loaded before any is consumed (memory-level parallelism).
-template <typename T, int D, typename RowFn, typename WFn>
-__device__ void accum_weighted_rows(int n, int gs, RowFn rowfn, WFn wfn, float* red_warp) {
-  using R = Row<T, D>;
-  constexpr int UN = 4;
-  const int nwarps = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sub = lane % R::LPR, rw = lane / R::LPR;
-  const int step = nwarps * R::RPW;
-  for (int h0 = 0; h0 < gs; h0 += 4) {
-    float acc[4][R::EPL];
-#pragma unroll
-    for (int hh = 0; hh < 4; ++hh)
-#pragma unroll
-      for (int j = 0; j < R::EPL; ++j) acc[hh][j] = 0.f;
-    for (int base = warp * R::RPW; base < n; base += step * UN) {
-      float vv[UN][R::EPL];
-      bool ok[UN];
-#pragma unroll
-      for (int u2 = 0; u2 < UN; ++u2) {
-        const int t = base + u2 * step + rw;
-        const T* row = t < n ? rowfn(t) : nullptr;
-        ok[u2] = row != nullptr;
-        if (ok[u2]) {
-          load_row_slice<T, D>(row, sub, vv[u2]);
-        } else {
-#pragma unroll
-          for (int j = 0; j < R::EPL; ++j) vv[u2][j] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int u2 = 0; u2 < UN; ++u2) {
-        if (!ok[u2]) continue;
-        const int t = base + u2 * step + rw;
-#pragma unroll
-        for (int hh = 0; hh < 4; ++hh) {
-          if (h0 + hh < gs) {
-            const float w = wfn(h0 + hh, t);
-#pragma unroll
-            for (int j = 0; j < R::EPL; ++j) acc[hh][j] = fmaf(w, vv[u2][j], acc[hh][j]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int hh = 0; hh < 4; ++hh)
-#pragma unroll
-      for (int j = 0; j < R::EPL; ++j) {
-        float x = acc[hh][j];
-#pragma unroll
-        for (int o = R::LPR; o < 32; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        acc[hh][j] = x;
-      }
-    if (rw == 0) {
-#pragma unroll
-      for (int hh = 0; hh < 4; ++hh)
-        if (h0 + hh < gs)
-#pragma unroll
-          for (int v = 0; v < R::VPL; ++v)
-#pragma unroll
-            for (int j = 0; j < R::EPV; ++j)
-              red_warp[(h0 + hh) * D + R::elem(sub, v) + j] += acc[hh][v * R::EPV + j];
-    }
-  }
-}
 
 // ------------------------------------------------------------------------
 // scan kernel: cosine chunks + static attention splits (+ append)
 // ------------------------------------------------------------------------
 
-struct StaticSpan {
-  int64_t n_init, ring_start, n_static;
-  __device__ StaticSpan(int64_t total, int init_len, int local_len) {
-    n_init = min((int64_t)init_len, total);
-    ring_start = max((int64_t)init_len, total - local_len);
-    n_static = n_init + (total - ring_start);
-  }
-  __device__ int64_t id(int64_t i) const { return i < n_init ? i : ring_start + (i - n_init); }
-};
 
 // softmax partial (m, l, unnormalised o) of the gs heads over up to
 // kAttnSplit tokens whose ids come from `idf(i)`; written to slot `part`.
@@ -318,22 +234,6 @@ __device__ __forceinline__ void query_norms(const T* qs, int gs, double* qn, int
   }
 }
 
-// DCU helper: |q_h| of the gs query heads written next to their centroid rows
-template <typename T, int D>
-__device__ void write_slot_norms(const DecodeParams& p, const T* q, int bi, int gi, int64_t slot) {
-  if (p.cnorm == nullptr) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int hh = warp; hh < p.gs; hh += nw) {
-    double s = 0.0;
-    for (int e = lane; e < D; e += 32) {
-      const double v = (double)to_f(q[hh * D + e]);
-      s = fma(v, v, s);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) p.cnorm[((int64_t)bi * p.h + gi * p.gs + hh) * p.C + slot] = (float)sqrt(s);
-  }
-}
 
 template <typename T>
 __host__ __device__ constexpr int static_tok() { return sizeof(T) == 2 ? 128 : 64; }
@@ -554,6 +454,8 @@ __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
     cos_task<T, D>(p, blockIdx.x, smem, bars);
   else
     static_task<T, D>(p, blockIdx.x - ncos, t0, total, smem, bars);
+  if (p.uctr != nullptr && blockIdx.x == gridDim.x - 1)
+    for (int i = threadIdx.x; i < 4 * p.U; i += blockDim.x) p.uctr[i] = 0;
   if (appending && blockIdx.x == 0) {
     T* keys = static_cast<T*>(const_cast<void*>(p.keys));
     T* vals = static_cast<T*>(const_cast<void*>(p.values));
@@ -887,7 +789,6 @@ struct UnitSmem {
   double* scratch;   // [64] reductions
 };
 
-__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 __host__ __device__ inline size_t unit_smem_layout(const DecodeParams& p, int D, UnitSmem* s,
                                                    unsigned char* base) {
@@ -950,33 +851,6 @@ __device__ int block_argmax(uint64_t key, int idx, double* scratch) {
   return si[32];
 }
 
-__device__ int block_exclusive_scan(int x, int* total, double* scratch) {
-  int* ws = reinterpret_cast<int*>(scratch);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int incl = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  __syncthreads();
-  if (lane == 31) ws[warp] = incl;
-  __syncthreads();
-  const int nw = blockDim.x >> 5;
-  if (warp == 0) {
-    int v = lane < nw ? ws[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += y;
-    }
-    if (lane < nw) ws[lane] = v;  // inclusive prefix of warp totals
-  }
-  __syncthreads();
-  const int warp_prefix = warp ? ws[warp - 1] : 0;
-  *total = ws[nw - 1];
-  return warp_prefix + incl - x;
-}
 
 __device__ double block_max_f64(double x, double* scratch) {
 #pragma unroll
@@ -1340,77 +1214,7 @@ __host__ __device__ inline size_t u2_layout(const DecodeParams& p, int D, U2Smem
 
 size_t unit2_smem_bytes(const DecodeParams& p, int D) { return u2_layout(p, D, nullptr, nullptr); }
 
-template <int IPT>
-__device__ void sort_keys(uint64_t* skey) {
-  uint64_t k[IPT];
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) k[i] = skey[threadIdx.x * IPT + i];
-  bitonic_regs<IPT>(k, skey);
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) skey[threadIdx.x * IPT + i] = k[i];
-  __syncthreads();
-}
 
-// positions of the R smallest of the (unique) keys key[0..L) -> spos (any order)
-__device__ int select_smallest(const uint64_t* key, int L, int R, int* spos, int* hist,
-                               int* s_state) {
-  if (R >= L) {
-    for (int i = threadIdx.x; i < L; i += blockDim.x) spos[i] = i;
-    __syncthreads();
-    return L;
-  }
-  uint64_t prefix = 0;
-  int need = R, shift = 56;
-  while (true) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < L; i += blockDim.x) {
-      const uint64_t k = key[i];
-      if (shift == 56 || ((k ^ prefix) >> (shift + 8)) == 0) atomicAdd(&hist[(k >> shift) & 255], 1);
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      int sum = 0;
-      for (int b = 8 * lane; b < 8 * lane + 8; ++b) sum += hist[b];
-      int incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int excl = incl - sum;
-      const unsigned bal = __ballot_sync(0xffffffffu, incl >= need && excl < need);
-      if (lane == __ffs(bal) - 1) {
-        int run = excl;
-        for (int b = 8 * lane; b < 8 * lane + 8; ++b) {
-          if (run + hist[b] >= need) {
-            s_state[0] = b;
-            s_state[1] = run;
-            s_state[2] = hist[b];
-            break;
-          }
-          run += hist[b];
-        }
-      }
-    }
-    __syncthreads();
-    const int b = s_state[0], below = s_state[1], cnt = s_state[2];
-    prefix |= (uint64_t)b << shift;
-    need -= below;
-    if (cnt == need || shift == 0) break;
-    shift -= 8;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) s_state[3] = 0;
-  __syncthreads();
-  const uint64_t lim = prefix >> shift;
-  for (int i = threadIdx.x; i < L; i += blockDim.x)
-    if ((key[i] >> shift) <= lim) spos[atomicAdd(&s_state[3], 1)] = i;
-  __syncthreads();
-  return s_state[3];
-}
 
 template <typename T, int D>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
@@ -2821,11 +2625,13 @@ int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
   return CTKV_ESHAPE;
 }
 
-int decode_variant() {   // CTKV_DECODE=2 forces the two-kernel path (A/B testing)
+// Decode path for bf16 (A/B switch CTKV_DECODE): 5 = wide unit pipeline
+// (default), 2 = 2-CTA cluster unit kernel, 4 = persistent layer kernel.
+int decode_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("CTKV_DECODE");
-    v = (e && e[0] == '2') ? 2 : 4;
+    v = (e && (e[0] == '2' || e[0] == '4')) ? e[0] - '0' : 5;
   }
   return v;
 }

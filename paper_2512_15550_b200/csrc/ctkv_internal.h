@@ -64,6 +64,13 @@ struct DecodeParams {
   int32_t* recg;    // [U][lmax] recalled ids, first-occurrence order
   int32_t* Lg;      // [U] recall lengths
   uint64_t* keyg;   // [U][lmax] packed (score, position) rerank keys
+  // wide unit pipeline (v5, ctkv_unit_wide.cu)
+  int* uctr;        // [U][4] recall done, attend done, L, Rn (zeroed by the scan)
+  int32_t* wsel;    // [U][lmax] selected recall positions, ascending
+  float* apo;       // [U][8][gs][D] sparse attention partials
+  double* apl;      // [U][8][gs]
+  double* wmax;     // [U][gs] per-head max of the selected logits
+  int wparts_b, wparts_c;
   // staged io
   const int32_t* rec_in;
   const int32_t* len_in;
@@ -93,6 +100,9 @@ int static_tok_for(int dtype);
 int phase_timing(int on, unsigned long long* out, int n);
 int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int decode_variant();
+bool wide_supported(const DecodeParams& p, int dtype, int D);
+// what: 1 = recall + attend kernels, 2 = tail (DCU, sparse ids, cursor/total)
+int launch_wide(const DecodeParams& p, int dtype, int D, int what, cudaStream_t st);
 int launch_centroid_norms(int dtype, int D, const void* cent, int64_t rows, float* out, cudaStream_t st);
 int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const double* la,

@@ -1,10 +1,12 @@
 """Multi-layer decode engine: the serving-shaped entry point.
 
 One (KvStore, QueryCentroidIndex) pair per layer lives in HBM; a decode
-step walks the layers in order and, per layer, enqueues the fused kernel
-pair (scan + unit: append, recall, rerank, sparse/static attention, merge,
-DCU) -- two launches per layer, no host synchronisation, so the whole step
-is captured once as a CUDA graph and replayed per token.  Under a ShardPlan
+step walks the layers in order and, per layer, enqueues the scan kernel
+(append, centroid cosines, static partials) and the unit kernels (recall,
+rerank, sparse attention, merge) on the main stream, and the layer's tail
+(FIFO DCU, cursor/total advance) on a side stream that overlaps the next
+layers.  No host synchronisation, so the whole step is captured once as a
+CUDA graph and replayed per token.  Under a ShardPlan
 each rank owns a (batch x kv-head) shard and all-gathers the head-sharded
 outputs after every layer (captured in the same graph).
 """
@@ -43,17 +45,14 @@ class DecodeEngine:
         self.b, self.h, self.g, self.d = lay.batch, lay.query_heads, lay.kv_heads, lay.head_dim
         self.dtype = st0.dtype
         dev = st0.keys.device
-        shared_ws = None
+        # one workspace per layer: a layer's deferred tail (DCU, cursor/total
+        # advance) reads its workspace while later layers already run
         self.layers: list[Layer] = []
         for store, index in layers:
-            bufs = StepBuffers.allocate(store, index, cfg)
-            # layers run back to back on one stream: one workspace serves all
-            if shared_ws is None or shared_ws.numel() < bufs.ws.numel():
-                shared_ws = bufs.ws
-            self.layers.append(Layer(store, index, bufs))
-        for layer in self.layers:
-            layer.bufs.ws = shared_ws
+            self.layers.append(Layer(store, index, StepBuffers.allocate(store, index, cfg)))
         nl = len(self.layers)
+        self._side = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
+        self._tail_ev = [torch.cuda.Event() for _ in range(nl)] if self._side is not None else []
         # step inputs (device): q [L,b,h,d], k/v [L,b,g,d]
         self.q = torch.zeros((nl, self.b, self.h, self.d), dtype=self.dtype, device=dev)
         self.k = torch.zeros((nl, self.b, self.g, self.d), dtype=self.dtype, device=dev)
@@ -98,18 +97,27 @@ class DecodeEngine:
         if self.layers[0].call is None:
             self._prepare()
             self._fn = N.lib().ctkv_decode_step_phase
+        main = torch.cuda.current_stream()
         for li, layer in enumerate(self.layers):
+            # phase bits: 1 scan, 2 unit, 8 defer the tail, 4 tail only
             if events is not None:
                 events[li][0].record()
                 self._launch(layer, 1)
                 events[li][1].record()
-                self._launch(layer, 2)
+                self._launch(layer, 2 | 8)
                 events[li][2].record()
             else:
-                self._launch(layer, 3)
+                self._launch(layer, 1 | 2 | 8)
+            # the tail (DCU write, sparse ids, cursor/total advance) is only
+            # read by this layer's next step: run it beside the next layers
+            self._tail_ev[li].record(main)
+            self._side.wait_event(self._tail_ev[li])
+            with torch.cuda.stream(self._side):
+                self._launch(layer, 4)
             if self._gbuf is not None:
                 self.gathered[li].copy_(all_gather_outputs(self.plan, self.out[li], self.group,
                                                            self._gbuf))
+        main.wait_stream(self._side)
 
     def _note(self) -> None:
         for layer in self.layers:
