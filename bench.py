@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--build-mode", type=int, default=1, help="0 exact f64, 1 fast")
+    ap.add_argument("--lanes", type=int, default=4,
+                    help="micro-batch lanes per GPU (sequence groups on their own streams)")
     return ap.parse_args()
 
 
@@ -206,7 +208,7 @@ def _config(a, n):
             "model": "llama3-8b-geometry", "global_batch": a.batch * n, "seq_len": a.seq,
             "layers": a.layers, "C": a.capacity, "rho": a.rho, "rho_prime": a.rho_prime,
             "c_prime": a.c_prime, "init_len": a.init_len, "local_len": a.local_len,
-            "parallelism": f"kvhead x batch shards over {n} GPU(s)", "l2": "inputs > L2 (no flush)"}
+            "parallelism": f"kvhead x batch shards over {n} GPU(s), {a.lanes} micro-batch lanes per GPU", "l2": "inputs > L2 (no flush)"}
 
 
 # ---------------------------------------------------------------------------
@@ -270,7 +272,7 @@ def main():
         build_ms.append(ev0.elapsed_time(ev1))
         layers.append((store, index))
         del q
-    engine = DecodeEngine(layers, cfg, plan=plan, group=group)
+    engine = DecodeEngine(layers, cfg, plan=plan, group=group, lanes=a.lanes)
     nl = a.layers
     # all step inputs, device resident: [T, L, b, heads, d]
     Qall = torch.stack([t[0].permute(2, 0, 1, 3) for t in tails], dim=1).contiguous()
@@ -327,7 +329,7 @@ def main():
 
     # ---- per-kernel timing (events on the launching stream, eager) ----
     nmeas = 3
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(nl)]
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(nl * a.lanes)]
            for _ in range(nmeas)]
     rl_tot = 0
     for m in range(nmeas):
@@ -340,7 +342,7 @@ def main():
     Lbar = rl_tot / (nmeas * nl * b * g)      # mean recall length per (b, g) unit
     e = 2
     gs = h // g
-    U = b * g
+    U = b * g // a.lanes                       # units per kernel launch (one lane)
     n_static = a.init_len + a.local_len
     C = a.capacity
     scan_bytes = U * (gs * C * d * e + 2 * n_static * d * e + gs * d * e + 2 * d * e) \
@@ -348,7 +350,7 @@ def main():
     unit_bytes = U * (C * 8 + 4 * a.c_prime * a.rho + e * d * Lbar + e * d * a.rho_prime
                       + 8 * gs * Lbar * 2 + e * gs * d + 4 * a.rho + 4 * gs * d
                       + math.ceil(n_static / 64) * gs * (d * 4 + 16))
-    algo_bytes = U * (h // g * C * d * e + 4 * a.c_prime * a.rho + e * d * Lbar
+    algo_bytes = b * g * (h // g * C * d * e + 4 * a.c_prime * a.rho + e * d * Lbar
                       + e * d * a.rho_prime + 2 * e * d * n_static + e * gs * d + 4 * gs * d
                       + e * gs * d + 4 * a.rho + 2 * e * d) * nl
     scan_gbs = scan_bytes / (scan_ms * 1e-3) / 1e9
@@ -448,7 +450,7 @@ def main():
                       "mode": "fast" if a.build_mode else "exact-f64"},
             "e2e": {"value": e2e_tok_s, "unit": "tok/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": (1 if fused else 2) * nl * a.steps,
+            "gpu_launches": (1 if fused else 2) * nl * a.lanes * a.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "graph": use_graph,

@@ -154,6 +154,9 @@ int ctkv_centroid_norms(const ctkv_layout* L, const void* centroids, int32_t cap
 
 /* ---- decode (ck/retrieval.py) --------------------------------------------- */
 
+/* The decode workspace must be zero-filled before its first use; the
+ * kernels' completion counters are left at zero by the CTAs that consume
+ * them, so a workspace is reusable across steps without clearing. */
 size_t ctkv_decode_workspace_bytes(const ctkv_layout* L, int32_t capacity, int32_t rho,
                                    int32_t c_prime, int32_t rho_prime);
 

@@ -58,6 +58,8 @@ struct DecodeWs {
   float* apo;
   double* apl;
   double* wmax;
+  int32_t* selg;
+  int* selctr;
   size_t bytes;
 };
 
@@ -98,6 +100,8 @@ DecodeWs carve_decode(const ctkv_layout* L, int C, int lmax, int ns, void* base,
   w.apo = reinterpret_cast<float*>(take(sizeof(float) * (size_t)U * 8 * gs * d));
   w.apl = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * 8 * gs));
   w.wmax = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * gs));
+  w.selg = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U * std::max(c_prime, 1)));
+  w.selctr = reinterpret_cast<int*>(take(sizeof(int) * (size_t)U));
   w.bytes = off;
   return w;
 }
@@ -286,6 +290,20 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   if (!v2) p.cval = nullptr;   // the f64 unit kernel selects from gcos directly
   if (!v2 && unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // v6: scan, then the 4-CTA cluster chain kernel; its tail (DCU, sparse
+  // ids, cursor/total) can be deferred (phase bit 8) and enqueued separately
+  // (phase 4) on another stream
+  if (v2 && ctkv::decode_variant() == 6 && chain_supported(p, L->dtype, L->head_dim)) {
+    p.selg = w.selg;
+    p.selctr = w.selctr;
+    const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
+    if (phase & 1)
+      if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;
+    if (phase & 2)
+      if (int rc = launch_chain(p, L->dtype, L->head_dim, st)) return rc;
+    const bool tail = (phase & 4) || ((phase & 2) && !(phase & 8));
+    return tail ? launch_wide(p, L->dtype, L->head_dim, 2, st) : CTKV_OK;
+  }
   // v5: wide unit pipeline; its tail (DCU, sparse ids, cursor/total) can be
   // deferred (phase bit 8) and enqueued separately (phase 4) on another stream
   if (v2 && ctkv::decode_variant() == 5 && wide_supported(p, L->dtype, L->head_dim)) {
@@ -496,6 +514,9 @@ int ctkv_centroid_norms(const ctkv_layout* L, const void* centroids, int32_t cap
 }
 
 int ctkv_debug_phase_timing(int32_t on, uint64_t* host_out, int32_t n) {
+  // v6 decode: the chain kernel's marks; otherwise the unit kernels'
+  if (ctkv::decode_variant() == 6)
+    return ctkv::chain_phase_timing(on, reinterpret_cast<unsigned long long*>(host_out), n);
   return ctkv::phase_timing(on, reinterpret_cast<unsigned long long*>(host_out), n);
 }
 

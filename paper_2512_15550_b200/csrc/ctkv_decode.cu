@@ -328,6 +328,21 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
         prev_idx = bidx;
       }
     }
+    // the unit's last cosine chunk turns the candidates into its top-C' slots
+    if (p.selg != nullptr) {
+      __shared__ int s_last;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&p.selctr[u], 1) == cpu - 1;
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        if (threadIdx.x < 32) warp_top_slots(p, u, p.selg + (int64_t)u * p.c_prime);
+        if (threadIdx.x == 0) p.selctr[u] = 0;
+      }
+    }
   }
 }
 
@@ -623,6 +638,21 @@ __device__ void scan3_cos(const DecodeParams& p, int task, const unsigned char* 
         }
         prev_key = bk;
         prev_idx = bidx;
+      }
+    }
+    // the unit's last cosine chunk turns the candidates into its top-C' slots
+    if (p.selg != nullptr) {
+      __shared__ int s_last;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&p.selctr[u], 1) == cpu - 1;
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        if (threadIdx.x < 32) warp_top_slots(p, u, p.selg + (int64_t)u * p.c_prime);
+        if (threadIdx.x == 0) p.selctr[u] = 0;
       }
     }
   }
@@ -2625,13 +2655,14 @@ int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
   return CTKV_ESHAPE;
 }
 
-// Decode path for bf16 (A/B switch CTKV_DECODE): 5 = wide unit pipeline
-// (default), 2 = 2-CTA cluster unit kernel, 4 = persistent layer kernel.
+// Decode path for bf16 (A/B switch CTKV_DECODE): 6 = 4-CTA cluster chain
+// kernel + deferred tail (default), 2 = 2-CTA cluster unit kernel, 5 = wide
+// unit pipeline, 4 = persistent layer kernel.
 int decode_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("CTKV_DECODE");
-    v = (e && (e[0] == '2' || e[0] == '4')) ? e[0] - '0' : 5;
+    v = (e && (e[0] == '5' || e[0] == '4' || e[0] == '2')) ? e[0] - '0' : 6;
   }
   return v;
 }

@@ -168,9 +168,14 @@ static __device__ int select_smallest(const uint64_t* key, int L, int R, int* sp
   while (true) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    for (int i = threadIdx.x; i < L; i += blockDim.x) {
-      const uint64_t k = key[i];
-      if (shift == 56 || ((k ^ prefix) >> (shift + 8)) == 0) atomicAdd(&hist[(k >> shift) & 255], 1);
+    // warp-aggregated (similar scores share their leading digits)
+    for (int i0 = threadIdx.x & ~31; i0 < L; i0 += blockDim.x) {
+      const int i = i0 + (threadIdx.x & 31);
+      const uint64_t k = i < L ? key[i] : 0ull;
+      const bool in = i < L && (shift == 56 || ((k ^ prefix) >> (shift + 8)) == 0);
+      const int bin = in ? (int)((k >> shift) & 255) : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      if (in && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -213,6 +218,51 @@ static __device__ int select_smallest(const uint64_t* key, int L, int R, int* sp
     if ((key[i] >> shift) <= lim) spos[atomicAdd(&s_state[3], 1)] = i;
   __syncthreads();
   return s_state[3];
+}
+
+// top-C' centroid slots of unit u from the scan's chunk candidates (value
+// desc, slot asc; ck/tensor_ops.py:88-92 on the group-max cosines) -> sel.
+// One warp.
+static __device__ void warp_top_slots(const DecodeParams& p, int u, int32_t* sel) {
+  const int lane = threadIdx.x & 31;
+  const int M = p.cos_blocks_per_unit * p.ncand;
+  const double* cv = p.cval + (int64_t)u * M;
+  const int32_t* ci = p.cidx + (int64_t)u * M;
+  constexpr int KR = 8;
+  uint64_t rk[KR];
+  int ri[KR];
+#pragma unroll
+  for (int r = 0; r < KR; ++r) {
+    const int m = lane + 32 * r;
+    rk[r] = m < M ? okey64(__ldcg(cv + m)) : 0ull;
+    ri[r] = m < M ? __ldcg(ci + m) : INT32_MAX;
+  }
+  uint64_t prev_key = ~0ull;
+  int prev_idx = -1;
+  for (int r = 0; r < p.c_prime; ++r) {
+    uint64_t bk = 0;
+    int bidx = INT32_MAX;
+#pragma unroll
+    for (int x = 0; x < KR; ++x) {
+      const bool below = rk[x] < prev_key || (rk[x] == prev_key && ri[x] > prev_idx);
+      if (below && (rk[x] > bk || (rk[x] == bk && ri[x] < bidx))) { bk = rk[x]; bidx = ri[x]; }
+    }
+    for (int m = lane + 32 * KR; m < M; m += 32) {
+      const uint64_t k = okey64(__ldcg(cv + m));
+      const int i = __ldcg(ci + m);
+      const bool below = k < prev_key || (k == prev_key && i > prev_idx);
+      if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
+    }
+    if (lane == 0) sel[r] = bidx;
+    prev_key = bk;
+    prev_idx = bidx;
+  }
 }
 
 }  // namespace ctkv

@@ -71,6 +71,9 @@ struct DecodeParams {
   double* apl;      // [U][8][gs]
   double* wmax;     // [U][gs] per-head max of the selected logits
   int wparts_b, wparts_c;
+  // v6 chain: the scan's last cosine CTA of a unit writes its top-C' slots
+  int32_t* selg;    // [U][c'] top-C' slots (ties -> smaller slot)
+  int* selctr;      // [U] cosine-chunk completion counters (reset by the last CTA)
   // staged io
   const int32_t* rec_in;
   const int32_t* len_in;
@@ -103,6 +106,10 @@ int decode_variant();
 bool wide_supported(const DecodeParams& p, int dtype, int D);
 // what: 1 = recall + attend kernels, 2 = tail (DCU, sparse ids, cursor/total)
 int launch_wide(const DecodeParams& p, int dtype, int D, int what, cudaStream_t st);
+bool chain_supported(const DecodeParams& p, int dtype, int D);
+// v6: the unit chain on a 4-CTA cluster per unit (ctkv_chain.cu)
+int chain_phase_timing(int on, unsigned long long* out, int n);
+int launch_chain(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_centroid_norms(int dtype, int D, const void* cent, int64_t rows, float* out, cudaStream_t st);
 int launch_attn(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const double* la,

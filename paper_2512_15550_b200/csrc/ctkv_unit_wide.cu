@@ -110,51 +110,6 @@ __host__ __device__ inline int wide_tail_npad(int lmax) {
   return n < kTailT ? kTailT : n;
 }
 
-// top-C' centroid slots of unit u from the scan's chunk candidates (value
-// desc, slot asc; ck/tensor_ops.py:88-92 on the group-max cosines) -> sel.
-// One warp.
-__device__ void warp_top_slots(const DecodeParams& p, int u, int32_t* sel) {
-  const int lane = threadIdx.x & 31;
-  const int M = p.cos_blocks_per_unit * p.ncand;
-  const double* cv = p.cval + (int64_t)u * M;
-  const int32_t* ci = p.cidx + (int64_t)u * M;
-  constexpr int KR = 8;
-  uint64_t rk[KR];
-  int ri[KR];
-#pragma unroll
-  for (int r = 0; r < KR; ++r) {
-    const int m = lane + 32 * r;
-    rk[r] = m < M ? okey64(cv[m]) : 0ull;
-    ri[r] = m < M ? ci[m] : INT32_MAX;
-  }
-  uint64_t prev_key = ~0ull;
-  int prev_idx = -1;
-  for (int r = 0; r < p.c_prime; ++r) {
-    uint64_t bk = 0;
-    int bidx = INT32_MAX;
-#pragma unroll
-    for (int x = 0; x < KR; ++x) {
-      const bool below = rk[x] < prev_key || (rk[x] == prev_key && ri[x] > prev_idx);
-      if (below && (rk[x] > bk || (rk[x] == bk && ri[x] < bidx))) { bk = rk[x]; bidx = ri[x]; }
-    }
-    for (int m = lane + 32 * KR; m < M; m += 32) {
-      const uint64_t k = okey64(cv[m]);
-      const int i = ci[m];
-      const bool below = k < prev_key || (k == prev_key && i > prev_idx);
-      if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
-      if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
-    }
-    if (lane == 0) sel[r] = bidx;
-    prev_key = bk;
-    prev_idx = bidx;
-  }
-}
-
 template <typename T, int D>
 __global__ void __launch_bounds__(kWT) recall_wide_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];

@@ -3,12 +3,26 @@
 One (KvStore, QueryCentroidIndex) pair per layer lives in HBM; a decode
 step walks the layers in order and, per layer, enqueues the scan kernel
 (append, centroid cosines, static partials) and the unit kernels (recall,
-rerank, sparse attention, merge) on the main stream, and the layer's tail
-(FIFO DCU, cursor/total advance) on a side stream that overlaps the next
-layers.  No host synchronisation, so the whole step is captured once as a
-CUDA graph and replayed per token.  Under a ShardPlan
-each rank owns a (batch x kv-head) shard and all-gathers the head-sharded
-outputs after every layer (captured in the same graph).
+rerank, sparse attention, merge), and the layer's tail (FIFO DCU,
+cursor/total advance) on a side stream that overlaps the next layers.  No
+host synchronisation, so the whole step is captured once as a CUDA graph
+and replayed per token.
+
+Lanes (micro-batches).  The sequences of a batch are independent through
+every layer (ck/retrieval.py:151-167 loops over (b, g) units with no
+cross-sequence state except the per-sequence FIFO cursor), so the batch is
+split into `lanes` groups of sequences, each walking the layers on its own
+stream.  Per lane the layer order is kept (layer l+1 of a sequence starts
+after its layer l), but while one lane runs the latency-bound part of a
+layer (top-C' -> union -> rerank -> top-rho' -> attention) another lane's
+bandwidth-bound centroid scan fills the GPU.  No data dependency is
+relaxed; this is the two-batch-overlap of serving engines.
+
+Under a ShardPlan each rank owns a (batch x kv-head) shard and all-gathers
+the head-sharded outputs after every layer (captured in the same graph) on
+one communication stream in a fixed (layer, lane) order, so every rank
+issues the collectives identically; lane k's layer l+1 waits for its layer-l
+gather.
 """
 
 from __future__ import annotations
@@ -19,7 +33,7 @@ import torch
 
 from . import _native as N
 from .index import QueryCentroidIndex
-from .parallel import ShardPlan, all_gather_outputs
+from .parallel import ShardPlan
 from .retrieval import DecodeConfig, StepBuffers
 from .store import KvStore
 
@@ -29,105 +43,173 @@ class Layer:
     store: KvStore
     index: QueryCentroidIndex
     bufs: StepBuffers
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
     call: tuple | None = None   # cached ctypes arguments of ctkv_decode_step_phase
 
 
 class DecodeEngine:
     def __init__(self, layers: list[tuple[KvStore, QueryCentroidIndex]], cfg: DecodeConfig, *,
-                 plan: ShardPlan | None = None, group=None):
+                 plan: ShardPlan | None = None, group=None, lanes: int = 1):
         if not layers:
             raise ValueError("DecodeEngine needs at least one layer")
         self.cfg = cfg
         self.plan = plan
         self.group = group
+        self.parents = list(layers)
         st0 = layers[0][0]
         lay = st0.layout
         self.b, self.h, self.g, self.d = lay.batch, lay.query_heads, lay.kv_heads, lay.head_dim
+        if lanes < 1 or self.b % lanes:
+            raise ValueError(f"lanes={lanes} must divide the batch {self.b}")
+        self.nlanes = lanes
+        self.bl = self.b // lanes
         self.dtype = st0.dtype
         dev = st0.keys.device
-        # one workspace per layer: a layer's deferred tail (DCU, cursor/total
-        # advance) reads its workspace while later layers already run
-        self.layers: list[Layer] = []
-        for store, index in layers:
-            self.layers.append(Layer(store, index, StepBuffers.allocate(store, index, cfg)))
-        nl = len(self.layers)
-        self._side = torch.cuda.Stream(device=dev) if dev.type == "cuda" else None
-        self._tail_ev = [torch.cuda.Event() for _ in range(nl)] if self._side is not None else []
-        # step inputs (device): q [L,b,h,d], k/v [L,b,g,d]
+        nl = len(layers)
+        self.nl = nl
+        # step inputs (device): q [L,b,h,d], k/v [L,b,g,d]; outputs [L,b,h,d] f32
         self.q = torch.zeros((nl, self.b, self.h, self.d), dtype=self.dtype, device=dev)
         self.k = torch.zeros((nl, self.b, self.g, self.d), dtype=self.dtype, device=dev)
         self.v = torch.zeros((nl, self.b, self.g, self.d), dtype=self.dtype, device=dev)
         self.out = torch.zeros((nl, self.b, self.h, self.d), dtype=torch.float32, device=dev)
-        for li, layer in enumerate(self.layers):
-            layer.bufs.out = self.out[li]          # kernels write the layer output in place
+        # lane_layers[k][l]: lane k's view of layer l.  One workspace per
+        # (lane, layer): a layer's deferred tail reads its workspace while
+        # later layers already run.
+        self.lane_layers: list[list[Layer]] = []
+        for k in range(lanes):
+            b0, b1 = k * self.bl, (k + 1) * self.bl
+            row = []
+            for li, (store, index) in enumerate(layers):
+                if lanes > 1:
+                    store, index = store.batch_view(b0, b1), index.batch_view(b0, b1)
+                bufs = StepBuffers.allocate(store, index, cfg)
+                bufs.out = self.out[li, b0:b1]      # kernels write the layer output in place
+                row.append(Layer(store, index, bufs, self.q[li, b0:b1], self.k[li, b0:b1],
+                                 self.v[li, b0:b1]))
+            self.lane_layers.append(row)
+        self.layers = [L for row in self.lane_layers for L in row]
+        cuda = dev.type == "cuda"
+        self._lane_st = [torch.cuda.Stream(device=dev) for _ in range(lanes)] if cuda else []
+        self._tail_st = [torch.cuda.Stream(device=dev) for _ in range(lanes)] if cuda else []
+        self._ev = ([[torch.cuda.Event() for _ in range(nl)] for _ in range(lanes)] if cuda else [])
         world = plan.world if plan else 1
+        self.world = world
+        self._comm = torch.cuda.Stream(device=dev) if (cuda and world > 1) else None
+        self._gev = ([[torch.cuda.Event() for _ in range(nl)] for _ in range(lanes)]
+                     if self._comm is not None else [])
         self.gathered = (torch.zeros((nl, plan.batch, plan.query_heads, self.d), dtype=torch.float32,
                                      device=dev) if world > 1 else self.out)
-        self._gbuf = (torch.empty((world, self.b, self.h, self.d), dtype=torch.float32, device=dev)
-                      if world > 1 else None)
+        self._gbuf = ([torch.empty((world, self.bl, self.h, self.d), dtype=torch.float32, device=dev)
+                       for _ in range(lanes)] if world > 1 else None)
         self.graph: torch.cuda.CUDAGraph | None = None
         self.steps_done = 0
 
     # -- one step -------------------------------------------------------------
 
     def _prepare(self) -> None:
-        """Build every layer's ctypes argument block once (pointers are fixed
-        for the engine's lifetime), so a launch costs one foreign call."""
+        """Build every (lane, layer) ctypes argument block once (pointers are
+        fixed for the engine's lifetime), so a launch costs one foreign call."""
         cfg = self.cfg
-        for li, layer in enumerate(self.layers):
-            st, ix, bf = layer.store, layer.index, layer.bufs
+        for L in self.layers:
+            st, ix, bf = L.store, L.index, L.bufs
             if cfg.c_prime > ix.capacity:
                 raise ValueError("c_prime exceeds the index capacity")
-            args = N.StepArgs(self.q[li].data_ptr(), self.k[li].data_ptr(), self.v[li].data_ptr(),
+            args = N.StepArgs(L.q.data_ptr(), L.k.data_ptr(), L.v.data_ptr(),
                               cfg.c_prime, cfg.rho_prime, int(cfg.use_dcu), int(cfg.use_rerank),
                               bf.out.data_ptr(), bf.row_max.data_ptr(), bf.denom.data_ptr(),
                               bf.selected.data_ptr(), bf.recall_len.data_ptr(),
                               bf.sparse_ids.data_ptr(), bf.sparse_len.data_ptr(), bf.sparse_cap,
                               bf.flags.data_ptr())
-            layer.call = (st.ctkv_layout(), st.desc(), ix.desc(), args, bf.ws.data_ptr(),
-                          bf.ws.numel())
+            L.call = (st.ctkv_layout(), st.desc(), ix.desc(), args, bf.ws.data_ptr(), bf.ws.numel())
+        self._fn = N.lib().ctkv_decode_step_phase
 
-    def _launch(self, layer: Layer, phase: int) -> None:
+    def _launch(self, layer: Layer, phase: int, stream=None) -> None:
         lay, sd, idd, args, ws, wsn = layer.call
-        rc = self._fn(lay, sd, idd, args, phase, ws, wsn, torch.cuda.current_stream().cuda_stream)
+        s = stream if stream is not None else torch.cuda.current_stream()
+        rc = self._fn(lay, sd, idd, args, phase, ws, wsn, s.cuda_stream)
         if rc:
             N.check(rc, "decode_step")
+
+    def _gather(self, k: int, li: int) -> None:
+        """All-gather lane k's layer-li output slice [bl, h_loc, d] and place
+        it into the global [B, H, d] view (rank-major, ShardPlan.assemble)."""
+        import torch.distributed as dist
+        plan, buf = self.plan, self._gbuf[k]
+        local = self.out[li, k * self.bl:(k + 1) * self.bl]
+        dist.all_gather_into_tensor(buf.view((-1,) + tuple(local.shape[1:])), local,
+                                    group=self.group)
+        for r in range(plan.world):
+            b0 = plan.batch_range(r)[0] + k * self.bl
+            h0, h1 = plan.q_range(r)
+            self.gathered[li, b0:b0 + self.bl, h0:h1].copy_(buf[r])
+
+    def _enqueue_timed(self, events) -> None:
+        """Serial eager step on the current stream with CUDA events around
+        each launch: events[i] = (start, after scan, after unit) for
+        i = layer * lanes + lane."""
+        for li in range(self.nl):
+            for k in range(self.nlanes):
+                L = self.lane_layers[k][li]
+                ev = events[li * self.nlanes + k]
+                ev[0].record()
+                self._launch(L, 1)
+                ev[1].record()
+                self._launch(L, 2 | 8)
+                ev[2].record()
+                self._launch(L, 4)
+                if self.world > 1:
+                    self._gather(k, li)
 
     def _enqueue(self, events=None) -> None:
         if self.layers[0].call is None:
             self._prepare()
-            self._fn = N.lib().ctkv_decode_step_phase
+        if events is not None:
+            self._enqueue_timed(events)
+            return
         main = torch.cuda.current_stream()
-        for li, layer in enumerate(self.layers):
-            # phase bits: 1 scan, 2 unit, 8 defer the tail, 4 tail only
-            if events is not None:
-                events[li][0].record()
-                self._launch(layer, 1)
-                events[li][1].record()
-                self._launch(layer, 2 | 8)
-                events[li][2].record()
-            else:
-                self._launch(layer, 1 | 2 | 8)
-            # the tail (DCU write, sparse ids, cursor/total advance) is only
-            # read by this layer's next step: run it beside the next layers
-            self._tail_ev[li].record(main)
-            self._side.wait_event(self._tail_ev[li])
-            with torch.cuda.stream(self._side):
-                self._launch(layer, 4)
-            if self._gbuf is not None:
-                self.gathered[li].copy_(all_gather_outputs(self.plan, self.out[li], self.group,
-                                                           self._gbuf))
-        main.wait_stream(self._side)
+        fork = torch.cuda.Event()
+        fork.record(main)
+        streams = self._lane_st + self._tail_st + ([self._comm] if self._comm is not None else [])
+        for s in streams:
+            s.wait_event(fork)
+        for li in range(self.nl):
+            for k in range(self.nlanes):
+                L = self.lane_layers[k][li]
+                ls, ts = self._lane_st[k], self._tail_st[k]
+                if self._comm is not None and li > 0:
+                    ls.wait_event(self._gev[k][li - 1])
+                # phase bits: 1 scan, 2 unit, 8 defer the tail, 4 tail only
+                self._launch(L, 1 | 2 | 8, ls)
+                ev = self._ev[k][li]
+                ev.record(ls)
+                # the tail (DCU write, sparse ids, cursor/total advance) is only
+                # read by this layer's next step: run it beside the next layers
+                ts.wait_event(ev)
+                self._launch(L, 4, ts)
+                if self._comm is not None:
+                    self._comm.wait_event(ev)
+                    with torch.cuda.stream(self._comm):
+                        self._gather(k, li)
+                    self._gev[k][li].record(self._comm)
+        for s in streams:
+            main.wait_stream(s)
 
     def _note(self) -> None:
-        for layer in self.layers:
-            layer.store.note_device_append()
+        for L in self.layers:
+            L.store.note_device_append()
+        if self.nlanes > 1:
+            for li, (store, _) in enumerate(self.parents):
+                store.note_device_append()
         self.steps_done += 1
 
     def reserve(self, steps: int) -> None:
-        for layer in self.layers:
-            layer.store.ensure_room(steps)
-            layer.call = None   # storage may have moved
+        if self.nlanes > 1:
+            raise RuntimeError("reserve() before splitting into lanes (lane views share storage)")
+        for L in self.layers:
+            L.store.ensure_room(steps)
+            L.call = None   # storage may have moved
 
     def step(self, events=None) -> None:
         """Enqueue one decode step (all layers) eagerly."""
@@ -140,8 +222,6 @@ class DecodeEngine:
         steps).  Call after at least one eager warm-up step."""
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        # the capture itself must not run the kernels: snapshot nothing, the
-        # graph records launches only
         with torch.cuda.graph(g):
             self._enqueue()
         self.graph = g
@@ -154,9 +234,17 @@ class DecodeEngine:
 
     def flags(self) -> int:
         f = 0
-        for layer in self.layers:
-            f |= int(layer.bufs.flags.item())
+        for L in self.layers:
+            f |= int(L.bufs.flags.item())
         return f
+
+    def sync_parents(self) -> None:
+        """Copy the lanes' token counters back into the layers' stores (the
+        lanes share K/V, centroids, lists and cursors with them already)."""
+        if self.nlanes > 1:
+            for li, (store, _) in enumerate(self.parents):
+                store.adopt_total(self.lane_layers[0][li].store)
 
     def check(self) -> None:
         N.raise_flags(self.flags(), "decode step")
+        self.sync_parents()

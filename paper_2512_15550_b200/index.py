@@ -77,6 +77,24 @@ class QueryCentroidIndex:
                            self.fifo_dev.data_ptr(), self.sync.data_ptr(), self.cnorm.data_ptr(),
                            self.capacity, self.rho)
 
+    def batch_view(self, b0: int, b1: int) -> "QueryCentroidIndex":
+        """Sequences [b0, b1) sharing this index's centroids, lists, norms and
+        FIFO cursors (all updated in place by the DCU), with a private
+        completion word array (a decode lane of DecodeEngine)."""
+        lay = self.layout
+        if not 0 <= b0 < b1 <= lay.batch:
+            raise ConfigError(f"batch_view: [{b0}, {b1}) outside [0, {lay.batch})")
+        v = QueryCentroidIndex.__new__(QueryCentroidIndex)
+        v.layout = HeadLayout(b1 - b0, lay.query_heads, lay.kv_heads, lay.seq_len, lay.head_dim)
+        v.capacity, v.rho, v.host_api, v.dtype, v.id_bound = (self.capacity, self.rho, self.host_api,
+                                                              self.dtype, self.id_bound)
+        v.cent = self.cent[b0:b1]
+        v.lists_dev = self.lists_dev[b0:b1]
+        v.fifo_dev = self.fifo_dev[b0:b1]
+        v.cnorm = self.cnorm[b0:b1]
+        v.sync = torch.zeros(1 + b1 - b0, dtype=torch.int32, device=self.cent.device)
+        return v
+
     def _compute_norms(self) -> None:
         """|c| per centroid row (f64-exact, stored f32); kept current by the DCU."""
         lay = self.layout

@@ -130,7 +130,9 @@ def _flags_check(flags: torch.Tensor, what: str, **kw) -> int:
 
 
 def _ws(nbytes: int, device) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    # zero-filled: the decode kernels' completion counters start at 0 and
+    # are left at 0 by the CTA that consumes them (include/ctkv.h)
+    return torch.zeros(max(int(nbytes), 1), dtype=torch.uint8, device=device)
 
 
 def _pad_per_head(per_head, b, g):

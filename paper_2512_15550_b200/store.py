@@ -72,6 +72,29 @@ class KvStore:
         store._set_total(s)
         return store
 
+    def batch_view(self, b0: int, b1: int) -> "KvStore":
+        """Sequences [b0, b1) as a store sharing this one's K/V memory, with
+        its own token counter (a decode lane of DecodeEngine).  Every lane
+        appends once per step, so the counters stay equal; `adopt_total`
+        copies one back."""
+        lay = self.layout
+        if not 0 <= b0 < b1 <= lay.batch:
+            raise ConfigError(f"batch_view: [{b0}, {b1}) outside [0, {lay.batch})")
+        v = KvStore.__new__(KvStore)
+        v.layout = HeadLayout(b1 - b0, lay.query_heads, lay.kv_heads, lay.seq_len, lay.head_dim)
+        v.init_len, v.local_len, v.dtype, v.host_api = (self.init_len, self.local_len, self.dtype,
+                                                        self.host_api)
+        v.keys = self.keys[b0:b1]
+        v.values = self.values[b0:b1]
+        v.total_dev = self.total_dev.clone()
+        v._total = self._total
+        return v
+
+    def adopt_total(self, other: "KvStore") -> None:
+        """Take over the token counter of a batch view (device and host)."""
+        self._total = other._total
+        self.total_dev.copy_(other.total_dev)
+
     def _set_total(self, t: int) -> None:
         self._total = int(t)
         self.total_dev.fill_(int(t))

@@ -1,0 +1,63 @@
+"""Phase breakdown of the v6 chain kernel (4-CTA cluster per unit) on a
+cfg2-sized layer: one eager step with device phase timestamps on, printed
+as per-phase medians over the units' CTAs."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2512_15550_b200 as P  # noqa: E402
+from paper_2512_15550_b200 import _native as N  # noqa: E402
+from paper_2512_15550_b200.engine import DecodeEngine  # noqa: E402
+from paper_2512_15550_b200.index import QueryCentroidIndex  # noqa: E402
+from paper_2512_15550_b200.store import KvStore  # noqa: E402
+
+lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+b, h, g, d, s, C, T = 8, 32, 8, 128, 98304, 2048, 16
+lay = P.HeadLayout(b, h, g, s + T, d)
+q, k, v, _ = P.generate(P.DriftConfig(seed=42, s=s, decode_steps=T), lay, dtype=torch.bfloat16,
+                        q_rows=(s - C, s + T))
+st = KvStore(P.HeadLayout(b, h, g, s, d), 128, 1024, dtype=torch.bfloat16, capacity=s + T,
+             host_api=False)
+st.keys[:, :, :s].copy_(k[:, :, :s])
+st.values[:, :, :s].copy_(v[:, :, :s])
+st._set_total(s)
+ix = QueryCentroidIndex.build(q[:, :, :C].contiguous(), st, C, 1280)
+eng = DecodeEngine([(st, ix)], P.DecodeConfig(4, 512), lanes=lanes)
+lib = N.lib()
+names = ["start", "topC'", "bitmaps+sync1", "survivors+sync2", "pull ids", "logits+sync3",
+         "pull keys", "threshold", "attention", "sync4", "merge"]
+for t in range(4):
+    eng.q[0].copy_(q[:, :, C + t])
+    eng.k[0].copy_(k[:, :, s + t])
+    eng.v[0].copy_(v[:, :, s + t])
+    if t == 3:
+        torch.cuda.synchronize()
+        lib.ctkv_debug_phase_timing(1, None, 0)
+        L0 = eng.lane_layers[0][0]
+        eng._launch(L0, 1)
+        torch.cuda.synchronize()
+        eng._launch(L0, 2 | 8)
+        torch.cuda.synchronize()
+        n = 512 * 12
+        buf = (ctypes.c_uint64 * n)()
+        lib.ctkv_debug_phase_timing(0, buf, n)
+        a = np.frombuffer(buf, dtype=np.uint64).reshape(512, 12).astype(np.int64)
+        nct = eng.bl * g * 4
+        a = a[:nct]
+        t0 = a[:, 0].min()
+        print(f"lanes={lanes}: {nct} CTAs; start spread {(a[:, 0].max() - t0) / 1e3:.2f} us")
+        for kk in range(1, 11):
+            rows = a[:, kk] > 0
+            dd = (a[rows, kk] - a[rows, kk - 1]) / 1e3
+            if len(dd):
+                print(f"  {kk:2d} {names[kk]:18s} median {np.median(dd):7.2f} us  max {dd.max():7.2f}")
+        r0 = a[0::4]
+        print(f"  end-to-end (rank 0, mark 10 - mark 0): median {np.median(r0[:, 10] - r0[:, 0]) / 1e3:.2f} us")
+        print(f"  kernel span: {(a[:, 10].max() - t0) / 1e3:.2f} us")
+    else:
+        eng.step()
+    torch.cuda.synchronize()

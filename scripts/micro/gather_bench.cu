@@ -6,6 +6,7 @@
 //  3: TMA bulk copies of every row into smem (one mbarrier), then read
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __device__ __forceinline__ uint32_t sa(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -46,6 +47,16 @@ __global__ void __launch_bounds__(512, 1) gather(const uint4* __restrict__ base,
 #pragma unroll
       for (int u = 0; u < UN; ++u) acc += __uint_as_float(x[u][0].x) + __uint_as_float(x[u][1].w);
     }
+  } else if (V == 4) {
+    // cp.async (LDGSTS) 16 B per lane into smem, 16 lanes per row, all in flight
+    for (int i = tid; i < nr * 16; i += 512) {
+      const int t = i >> 4, c = i & 15;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(smem + t * 256 + c * 16)),
+                   "l"(base + (int64_t)my[t] * 16 + c) : "memory");
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int t = tid; t < nr; t += 512) acc += reinterpret_cast<float*>(smem + t * 256)[lane];
   } else {
     // TMA bulk copy of every row (nr * 256 B must fit smem)
     if (tid == 0) {
@@ -63,12 +74,12 @@ __global__ void __launch_bounds__(512, 1) gather(const uint4* __restrict__ base,
   if (acc == 12345.f) out[0] = acc;
 }
 
-int main() {
+int main(int argc, char** argv) {
   const int64_t rows = 64LL * 98304;   // a layer's K rows, 1.6 GB
   uint4* base;
   cudaMalloc(&base, rows * 256);
   cudaMemset(base, 1, rows * 256);
-  const int ctas = 128, nr = 750;
+  const int ctas = argc > 1 ? atoi(argv[1]) : 128, nr = argc > 2 ? atoi(argv[2]) : 750;
   int* ids;
   cudaMalloc(&ids, ctas * nr * sizeof(int));
   int* h = new int[ctas * nr];
@@ -88,7 +99,8 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaFuncSetAttribute(gather<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  for (int v = 0; v < 4; ++v) {
+  cudaFuncSetAttribute(gather<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  for (int v = 0; v < 5; ++v) {
     float best = 1e9;
     for (int rep = 0; rep < 5; ++rep) {
       cudaMemset(flush, rep, 256 << 20);
@@ -97,6 +109,7 @@ int main() {
       if (v == 1) gather<1><<<ctas, 512>>>(base, ids, nr, out);
       if (v == 2) gather<2><<<ctas, 512>>>(base, ids, nr, out);
       if (v == 3) gather<3><<<ctas, 512, nr * 256>>>(base, ids, nr, out);
+      if (v == 4) gather<4><<<ctas, 512, nr * 256>>>(base, ids, nr, out);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
