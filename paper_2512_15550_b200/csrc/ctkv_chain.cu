@@ -1,29 +1,34 @@
-// v6 decode: the per-(b,g) unit chain after the scan, on a 4-CTA cluster.
+// v6 decode: the per-(b,g) unit chain after the scan, on a CL-CTA cluster.
 //
 // After the scan kernel (ctkv_decode.cu) each unit is a dependency chain:
 // top-C' slots -> first-occurrence union of their lists -> rerank logits of
 // the recalled keys -> top-rho' -> attention over the selected V rows ->
-// merge with the static partials.  On one SM every link is a latency-bound
-// gather; here the four CTAs of a cluster split every link and exchange
-// the small cross-CTA state through distributed shared memory:
+// merge with the static partials.  Its gathers are random 256-byte rows,
+// which one SM pulls at only ~27 GB/s (measured, scripts/micro), so the CL
+// CTAs of a cluster split every gather and exchange the small cross-CTA
+// state through distributed shared memory.  Each CTA is small (~64 KB of
+// shared memory, <= 80 registers) so three fit an SM next to other work:
+// the engine's micro-batch lanes overlap one lane's chains with another
+// lane's bandwidth-bound scan.
 //
-//   1. every CTA: top-C' slots from the scan's chunk candidates
-//      (ck/retrieval.py:144-154, ties -> smaller slot)
-//   2. CTA r owns lists r, r+4, ...: loads them, marks a bitmap over token
+//   1. the scan's last cosine CTA of the unit already wrote its top-C'
+//      slots (ck/retrieval.py:144-154, ties -> smaller slot)
+//   2. CTA r owns lists r, r+CL, ...: loads them, marks a bitmap over token
 //      ids; cluster barrier; an entry of list j survives iff no list j' < j
 //      holds it (bits read from the owners' shared memory) -- the
 //      np.unique(return_index) first-occurrence order of
 //      ck/retrieval.py:156-162; per-list survivor counts are broadcast
 //   3. the recall positions [0, L) are split evenly over the CTAs; each
-//      pulls its slice's ids from the owners and gathers the K rows with
-//      TMA bulk copies, then computes the gs-head rerank logits (f32 sums of
-//      exact bf16 products per 8-element chunk, f64 across chunks, x 1/sqrt(d);
-//      ck/retrieval.py:171-193) and the packed key (~f32(group max), pos)
-//   4. every CTA pulls all L keys and radix-selects the rho'-th smallest:
-//      the top-rho' set by (score desc, position asc) (ck/retrieval.py:210-216)
-//   5. each CTA attends over its slice's selected tokens (V rows by TMA bulk
-//      copy; f64 softmax statistics, f32 weighted sums; ck/retrieval.py:221-246)
-//      and sends its partial (m, l, o) to CTA 0
+//      pulls its slice's ids from the owners and gathers the K rows into
+//      registers (8 lanes x 32 B per row, 128 rows in flight), computing the
+//      gs-head rerank logits (f32 sums of exact bf16 products per 8-element
+//      chunk, f64 across chunks, x 1/sqrt(d); ck/retrieval.py:171-193)
+//   4. every CTA pulls all L score keys and radix-selects the top-rho' set
+//      by (score desc, position asc) (ck/retrieval.py:210-216)
+//   5. the selected tokens, in position order, are split evenly over the
+//      CTAs; each gathers its V rows into registers and accumulates an
+//      online-softmax partial (f64 statistics, f32 weighted sums;
+//      ck/retrieval.py:221-246) that goes to CTA 0
 //   6. CTA 0 merges the sparse partials with the static partials exactly
 //      (ck/retrieval.py:275-284) and writes out / row_max / denom.
 //
@@ -32,6 +37,7 @@
 // tail_wide_kernel in ctkv_unit_wide.cu), which runs on a side stream.
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -56,9 +62,8 @@ __device__ __forceinline__ void cmark(int k) {
   }
 }
 
-// generic-proxy accesses of shared memory before later async-proxy (TMA) writes
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa(dst)), "l"(src) : "memory");
@@ -66,33 +71,49 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-constexpr int kCL = 4;           // CTAs per unit (cluster size)
+// f64 exp out of line: one copy of its ~200 instructions per kernel
+__device__ __noinline__ double dexp(double x) { return exp(x); }
+__device__ __forceinline__ double warp_max_f64(double m) {
+#pragma unroll 1
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  return m;
+}
+__device__ __forceinline__ double warp_sum_f64(double m) {
+#pragma unroll 1
+  for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+  return m;
+}
+
 constexpr int kCT = 256;         // threads per CTA
-constexpr int kCB = 256;         // rows per gather batch
-constexpr int kCMaxGs = 8;       // query heads per kv head
+constexpr int kCW = kCT / 32;
+constexpr int kCB = 128;         // selected rows per attention batch
 constexpr int kCMaxLists = 8;    // c' <= 8
-constexpr int kCMaxOwn = 32;     // list entries per thread held in registers
+constexpr int kCMaxPer = 32;     // list entries per thread (keep mask bits)
+constexpr int kKUn = 4;          // K-row passes in flight per warp (4 rows each)
+constexpr int kVUn = 4;          // V-row passes in flight per warp (2 rows each)
 
 struct ChainSmem {
-  unsigned char* rows;   // [kCB][D] gathered K (then V) rows; later the row-group sums
-  uint32_t* bm;          // [nlo][words] bitmaps of this CTA's lists  } area A; CTA 0 reuses it
-  int32_t* recl;         // [nlo][rho] this CTA's lists, survivors    } for the static partials
-  uint64_t* keys;        // [lmax] packed keys of all recall positions
+  uint32_t* bm;          // [nlo][words] bitmaps of this CTA's lists   } area A; CTA 0
+  int32_t* recl;         // [nlo][rho] this CTA's lists, survivors     } later: static partials
+  float* spo;            // CTA 0, after the union: [ns][gs][D] static o
+  double* spml;          //                          [2][ns][gs] static (m, l)
+  uint32_t* keys;        // [lmax] score keys ~f32(group max) by position } area B: later the
+  float* red;            // [kCW][gs][D] per-warp partial sums           } per-warp V sums
   int32_t* sid;          // [scap] ids of this CTA's slice
-  double* slg;           // [gs][scap] rerank logits of the slice
-  int32_t* spos;         // [scap] selected slice offsets, ascending
-  float* wts;            // [gs][kCB] attention weights of a batch
-  float* cpo;            // CTA 0: [kCL][gs][D] sparse partial sums from the cluster
-  double* cpml;          // CTA 0: [2][kCL][gs] their (m, l)
+  int32_t* spos;         // [scap] this CTA's selected positions, in position order
+  int32_t* vid;          // [kCB] ids of an attention batch
+  float* wts;            // [gs][kCB] weights of an attention batch
+  double* lgs;           // [gs][kCB] logits / f64 weights of an attention batch
+  float* cpo;            // CTA 0: [CL][gs][D] sparse partial sums from the cluster
+  double* cpml;          // CTA 0: [2][CL][gs] their (m, l)
   int* hist;             // [256]
-  double* scratch;       // [128]
-  size_t area_a;
+  double* scratch;       // [max(128, gs * (ns + CL))]
 };
 
-__host__ __device__ inline int chain_nlo(int c_prime) { return (c_prime + kCL - 1) / kCL; }
-__host__ __device__ inline int chain_scap(int lmax) { return (lmax + kCL - 1) / kCL + 1; }
+__host__ __device__ inline int chain_nlo(int c_prime, int CL) { return (c_prime + CL - 1) / CL; }
+__host__ __device__ inline int chain_scap(int lmax, int CL) { return (lmax + CL - 1) / CL + 1; }
 
-__host__ __device__ inline size_t chain_layout(const DecodeParams& p, int D, int esize, ChainSmem* s,
+__host__ __device__ inline size_t chain_layout(const DecodeParams& p, int D, int CL, ChainSmem* s,
                                                unsigned char* base) {
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -100,48 +121,53 @@ __host__ __device__ inline size_t chain_layout(const DecodeParams& p, int D, int
     off += align16(bytes);
     return ptr;
   };
-  const int nlo = chain_nlo(p.c_prime);
-  const int scap = chain_scap(p.lmax);
+  const int nlo = chain_nlo(p.c_prime, CL);
+  const int scap = chain_scap(p.lmax, CL);
   const int lmax = p.lmax > 1 ? p.lmax : 1;
-  const size_t a_lists = (size_t)nlo * p.bitmap_words * 4 + align16((size_t)nlo * p.rho * 4);
-  const size_t a_static = (size_t)p.ns * p.gs * D * 4 + align16((size_t)2 * p.ns * p.gs * 8);
+  const size_t bm_b = align16((size_t)nlo * p.bitmap_words * 4);
+  const size_t a_lists = bm_b + align16((size_t)nlo * p.rho * 4);
+  const size_t spo_b = align16((size_t)p.ns * p.gs * D * 4);
+  const size_t a_static = spo_b + align16((size_t)2 * p.ns * p.gs * 8);
+  const size_t keys_b = (size_t)lmax * 4, red_b = (size_t)kCW * p.gs * D * 4;
   ChainSmem t;
-  t.area_a = a_lists > a_static ? a_lists : a_static;
-  const size_t rows = (size_t)kCB * D * esize;
-  const size_t red = (size_t)(kCT / (D / 4)) * p.gs * D * 4;
-  t.rows = take(rows > red ? rows : red);
-  unsigned char* a = take(t.area_a);
+  unsigned char* a = take(a_lists > a_static ? a_lists : a_static);
   t.bm = reinterpret_cast<uint32_t*>(a);
-  t.recl = a ? reinterpret_cast<int32_t*>(a + align16((size_t)nlo * p.bitmap_words * 4)) : nullptr;
-  t.keys = reinterpret_cast<uint64_t*>(take((size_t)lmax * 8));
+  t.recl = a ? reinterpret_cast<int32_t*>(a + bm_b) : nullptr;
+  t.spo = reinterpret_cast<float*>(a);
+  t.spml = a ? reinterpret_cast<double*>(a + spo_b) : nullptr;
+  unsigned char* b = take(keys_b > red_b ? keys_b : red_b);
+  t.keys = reinterpret_cast<uint32_t*>(b);
+  t.red = reinterpret_cast<float*>(b);
   t.sid = reinterpret_cast<int32_t*>(take((size_t)scap * 4));
-  t.slg = reinterpret_cast<double*>(take((size_t)p.gs * scap * 8));
   t.spos = reinterpret_cast<int32_t*>(take((size_t)scap * 4));
+  t.vid = reinterpret_cast<int32_t*>(take((size_t)kCB * 4));
   t.wts = reinterpret_cast<float*>(take((size_t)p.gs * kCB * 4));
-  t.cpo = reinterpret_cast<float*>(take((size_t)kCL * p.gs * D * 4));
-  t.cpml = reinterpret_cast<double*>(take((size_t)2 * kCL * p.gs * 8));
+  t.lgs = reinterpret_cast<double*>(take((size_t)p.gs * kCB * 8));
+  t.cpo = reinterpret_cast<float*>(take((size_t)CL * p.gs * D * 4));
+  t.cpml = reinterpret_cast<double*>(take((size_t)2 * CL * p.gs * 8));
   t.hist = reinterpret_cast<int*>(take(256 * 4));
-  const int nscr = p.gs * (p.ns + kCL) > 128 ? p.gs * (p.ns + kCL) : 128;
+  const int nscr = p.gs * (p.ns + CL) > 128 ? p.gs * (p.ns + CL) : 128;
   t.scratch = reinterpret_cast<double*>(take((size_t)nscr * 8));
   if (s) *s = t;
   return off;
 }
 
-// the R-th smallest of the unique keys key[0..L): on return every selected
-// key satisfies (key >> st[1]) <= lim (st[0..1] = lim lo/hi word, shift)
-__device__ void chain_threshold(const uint64_t* key, int L, int R, int* hist, int* st,
-                                uint64_t* lim_out, int* shift_out) {
-  uint64_t prefix = 0;
-  int need = R, shift = 56;
-  while (true) {
+// Boundary of the R smallest 64-bit keys (key[i] << 32 | i), i < L, i.e. the
+// top-R by (score desc, position asc): returns v and need such that the
+// selected positions are {i : key[i] < v} plus the first `need` positions
+// (in position order) with key[i] == v.  Radix over the 32-bit score keys,
+// warp-aggregated histogram (similar scores share leading digits).
+__device__ void chain_boundary(const uint32_t* key, int L, int R, int* hist, int* st, uint32_t* v_out,
+                               int* need_out) {
+  uint32_t prefix = 0;
+  int need = R;
+  for (int shift = 24; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    // warp-aggregated: the leading digits of similar scores coincide, so
-    // per-key atomics would serialise on a few bins
     for (int i0 = threadIdx.x & ~31; i0 < L; i0 += blockDim.x) {
       const int i = i0 + (threadIdx.x & 31);
-      const uint64_t k = i < L ? key[i] : 0ull;
-      const bool in = i < L && (shift == 56 || ((k ^ prefix) >> (shift + 8)) == 0);
+      const uint32_t k = i < L ? key[i] : 0u;
+      const bool in = i < L && (shift == 24 || ((k ^ prefix) >> (shift + 8)) == 0);
       const int bin = in ? (int)((k >> shift) & 255) : -1;
       const unsigned peers = __match_any_sync(0xffffffffu, bin);
       if (in && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
@@ -165,7 +191,6 @@ __device__ void chain_threshold(const uint64_t* key, int L, int R, int* hist, in
           if (run + hist[b] >= need) {
             st[0] = b;
             st[1] = run;
-            st[2] = hist[b];
             break;
           }
           run += hist[b];
@@ -173,101 +198,111 @@ __device__ void chain_threshold(const uint64_t* key, int L, int R, int* hist, in
       }
     }
     __syncthreads();
-    const int b = st[0], below = st[1], cnt = st[2];
-    prefix |= (uint64_t)b << shift;
-    need -= below;
+    prefix |= (uint32_t)st[0] << shift;
+    need -= st[1];
     __syncthreads();
-    if (cnt == need || shift == 0) break;
-    shift -= 8;
   }
-  *lim_out = prefix >> shift;
-  *shift_out = shift;
+  *v_out = prefix;
+  *need_out = need;
 }
 
-template <typename T, int D>
-__global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 1) chain_kernel(DecodeParams p) {
+template <typename T, int D, int CL, int GS>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 3) chain_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cl = cg::this_cluster();
   const int r = (int)cl.block_rank();
   ChainSmem S;
-  chain_layout(p, D, sizeof(T), &S, smem);
-  const int u = blockIdx.x / kCL;
-  const int bi = u / p.g, gi = u % p.g, gs = p.gs;
+  chain_layout(p, D, CL, &S, smem);
+  const int u = blockIdx.x / CL;
+  const int bi = u / p.g, gi = u % p.g;
+  constexpr int gs = GS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int RB = D * int(sizeof(T));
-  constexpr int CH = RB / 16;                 // 16-byte chunks per row
+  constexpr int CH = D * int(sizeof(T)) / 16;   // 16-byte chunks per row (16 at d=128)
+  static_assert(CH == 16 || CH == 8, "d = 64 or 128 (bf16)");
   const int64_t total = *p.total + (p.k_new != nullptr ? 1 : 0);
-  const int scap = chain_scap(p.lmax);
-  __shared__ __align__(16) T qs[kCMaxGs * D];
+  const int ns = p.ns;
+  __shared__ __align__(16) T qs[GS * D];
   __shared__ int32_t sel[kCMaxLists];
   __shared__ int lcnt[kCMaxLists];
   __shared__ int sbase[kCMaxLists + 1];
   __shared__ int s_state[4];
-  __shared__ uint64_t bar_rows, bar_st;
-  __shared__ double hm[kCMaxGs], hl[kCMaxGs];
+  __shared__ double hm[GS], hl[GS], hnew[GS], hresc[GS];
 
   cmark(0);
-  if (tid == 0) {
-    bar_init(&bar_rows, 1);
-    bar_init(&bar_st, 1);
-  }
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = tid; i < gs * D; i += kCT) qs[i] = q[i];
-
-  // ---- 1. top-C' slots (every CTA) ------------------------------------------
-  if (warp == 0) warp_top_slots(p, u, sel);
+  if (tid < p.c_prime) sel[tid] = __ldcg(p.selg + (int64_t)u * p.c_prime + tid);
+  __syncthreads();
+  cmark(1);
 
   // ---- 2. own lists: load, bitmap, first-occurrence test ----------------------
-  const int nlo = chain_nlo(p.c_prime);
-  const int nown = (p.c_prime - r + kCL - 1) / kCL;     // lists r, r + kCL, ... < c'
-  const int per = (p.rho + kCT - 1) / kCT;              // entries per thread per list
-  __syncthreads();                                      // sel, bar init
-  cmark(1);
-  // entry x of this thread: list slot x / per, position tid * per + x % per
-  int ids[kCMaxOwn];
+  // (compact loops, not unrolled code: this phase runs once per kernel and a
+  // cold instruction cache costs more than the loop overhead)
+  const int nlo = chain_nlo(p.c_prime, CL);
+  const int nown = (p.c_prime - r + CL - 1) / CL;      // lists r, r + CL, ... < c'
+  int32_t* raw = reinterpret_cast<int32_t*>(S.keys);   // area B: [nown][rho] raw ids
+  {
+    constexpr int LU = 8;
+    for (int sl = 0; sl < nown; ++sl) {
+      const int32_t* row = p.lists + ((int64_t)u * p.C + sel[r + CL * sl]) * p.rho;
+      int32_t* dst = raw + sl * p.rho;
+      for (int i0 = tid; i0 < p.rho; i0 += kCT * LU) {
+        int v[LU];
 #pragma unroll
-  for (int x = 0; x < kCMaxOwn; ++x) {
-    ids[x] = kEmpty;
-    const int sl = x / per, i = tid * per + x % per;
-    if (sl < nown && i < p.rho) {
-      int id = __ldg(p.lists + ((int64_t)u * p.C + sel[r + kCL * sl]) * p.rho + i);
-      if (id != kEmpty && (id < 0 || id >= total)) { set_flag(p.flags, kFlagIdRange); id = kEmpty; }
-      ids[x] = id;
+        for (int x = 0; x < LU; ++x) v[x] = i0 + x * kCT < p.rho ? __ldg(row + i0 + x * kCT) : kEmpty;
+#pragma unroll
+        for (int x = 0; x < LU; ++x) {
+          int id = v[x];
+          if (id != kEmpty && (id < 0 || id >= total)) { set_flag(p.flags, kFlagIdRange); id = kEmpty; }
+          if (i0 + x * kCT < p.rho) dst[i0 + x * kCT] = id;
+        }
+      }
+    }
+    for (int i = tid; i < nlo * p.bitmap_words; i += kCT) S.bm[i] = 0u;
+    __syncthreads();
+    for (int sl = 0; sl < nown; ++sl) {
+      uint32_t* bm = S.bm + sl * p.bitmap_words;
+#pragma unroll 4
+      for (int i = tid; i < p.rho; i += kCT) {
+        const int id = raw[sl * p.rho + i];
+        if (id != kEmpty) atomicOr(&bm[id >> 5], 1u << (id & 31));
+      }
     }
   }
-  for (int i = tid; i < nlo * p.bitmap_words; i += kCT) S.bm[i] = 0u;
-  __syncthreads();
-#pragma unroll
-  for (int x = 0; x < kCMaxOwn; ++x)
-    if (ids[x] != kEmpty) atomicOr(&S.bm[(x / per) * p.bitmap_words + (ids[x] >> 5)], 1u << (ids[x] & 31));
   cl.sync();   // #1: every list's bitmap is complete
   cmark(2);
-  // survivors, compacted in position order per list
+  // survivors, compacted in position order per list (thread t owns entries
+  // [t*per, (t+1)*per)); the earlier lists' bits are read with independent
+  // remote loads
+  const int per = (p.rho + kCT - 1) / kCT;
   for (int sl = 0; sl < nown; ++sl) {
-    const int j = r + kCL * sl;
+    const int j = r + CL * sl;
+    const int32_t* rl = raw + sl * p.rho;
     unsigned keepm = 0;
     int cnt = 0;
+#pragma unroll 4
+    for (int e = 0; e < per; ++e) {
+      const int i = tid * per + e;
+      const int id = i < p.rho ? rl[i] : kEmpty;
+      uint32_t hit = 0;
+      if (id != kEmpty) {
+        uint32_t w[kCMaxLists - 1];
 #pragma unroll
-    for (int x = 0; x < kCMaxOwn; ++x) {
-      if (x / per != sl) continue;
-      const int id = ids[x];
-      bool keep = id != kEmpty;
-      for (int j2 = 0; keep && j2 < j; ++j2) {
-        const uint32_t* obm = cl.map_shared_rank(S.bm, j2 % kCL) + (j2 / kCL) * p.bitmap_words;
-        keep = !((obm[id >> 5] >> (id & 31)) & 1u);
+        for (int j2 = 0; j2 < kCMaxLists - 1; ++j2)
+          w[j2] = j2 < j ? (cl.map_shared_rank(S.bm, j2 % CL) + (j2 / CL) * p.bitmap_words)[id >> 5] : 0u;
+#pragma unroll
+        for (int j2 = 0; j2 < kCMaxLists - 1; ++j2) hit |= w[j2] >> (id & 31);
       }
-      keepm |= (keep ? 1u : 0u) << x;
+      const bool keep = id != kEmpty && !(hit & 1u);
+      keepm |= (keep ? 1u : 0u) << e;
       cnt += keep;
     }
     int tot;
     int o = block_exclusive_scan(cnt, &tot, S.scratch);
-#pragma unroll
-    for (int x = 0; x < kCMaxOwn; ++x)
-      if ((keepm >> x) & 1u) S.recl[sl * p.rho + o++] = ids[x];
-    if (tid < kCL) {
-      int* peer = cl.map_shared_rank(lcnt, tid);
-      peer[j] = tot;
-    }
+#pragma unroll 1
+    for (int e = 0; e < per; ++e)
+      if ((keepm >> e) & 1u) S.recl[sl * p.rho + o++] = rl[tid * per + e];
+    if (tid < CL) cl.map_shared_rank(lcnt, tid)[j] = tot;
   }
   cl.sync();   // #2: survivor counts everywhere, survivors compacted
   cmark(3);
@@ -278,267 +313,296 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 1) chain_kern
   }
   __syncthreads();
   const int L = sbase[kCMaxLists];
-  const int lo = (int)((int64_t)r * L / kCL), hi = (int)((int64_t)(r + 1) * L / kCL);
+  const int lo = (int)((int64_t)r * L / CL), hi = (int)((int64_t)(r + 1) * L / CL);
   const int n_sl = hi - lo;
   int32_t* recg = p.recg + (int64_t)u * p.lmax;
   uint64_t* kg = p.keyg + (int64_t)u * p.lmax;
+  double* lgg = p.logits + (int64_t)u * gs * p.lmax;
   for (int i = tid; i < n_sl; i += kCT) {
     const int pos = lo + i;
     int j = 0;
     while (j + 1 < p.c_prime && pos >= sbase[j + 1]) ++j;
-    const int32_t* orecl = cl.map_shared_rank(S.recl, j % kCL);
-    const int id = orecl[(j / kCL) * p.rho + (pos - sbase[j])];
+    const int id = cl.map_shared_rank(S.recl, j % CL)[(j / CL) * p.rho + (pos - sbase[j])];
     S.sid[i] = id;
     recg[pos] = id;
   }
   __syncthreads();
-
   cmark(4);
-  // ---- 3. rerank logits of the slice ---------------------------------------------
-  const double scale = 1.0 / sqrt((double)D);
-  const T* keys_g = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
-  T* rows = reinterpret_cast<T*>(S.rows);
-  uint32_t ph = 0;
-  for (int b0 = 0; b0 < n_sl; b0 += kCB) {
-    const int n = min(kCB, n_sl - b0);
-    if (tid == 0) bar_expect(&bar_rows, (uint32_t)(n * RB));
-    fence_proxy_async();
-    __syncthreads();
-    if (tid < n) bulk_g2s(rows + (size_t)tid * D, keys_g + (int64_t)S.sid[b0 + tid] * D, RB, &bar_rows);
-    bar_wait(&bar_rows, ph);
-    ph ^= 1u;
-    if (tid < n) {
-      double acc[kCMaxGs];
+
+  // ---- 3. rerank logits of the slice (K rows gathered into registers) ----------
+  {
+    const double scale = 1.0 / sqrt((double)D);
+    const T* keys_g = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
+    constexpr int LPR = 8;                 // lanes per row
+    constexpr int CPL = CH / LPR;          // 16-byte chunks per lane (2 at d=128)
+    const int sub = lane % LPR, rw = lane / LPR;
+    constexpr int RPW = 32 / LPR;          // rows per warp pass
+    const uint4* q4 = reinterpret_cast<const uint4*>(qs);
+    for (int b0 = warp * RPW; b0 < n_sl; b0 += kCW * RPW * kKUn) {
+      uint4 raw[kKUn][CPL];
 #pragma unroll
-      for (int hh = 0; hh < kCMaxGs; ++hh) acc[hh] = 0.0;
-      const uint4* r4 = reinterpret_cast<const uint4*>(rows + (size_t)tid * D);
-      const uint4* q4 = reinterpret_cast<const uint4*>(qs);
-#pragma unroll 4
-      for (int c = 0; c < CH; ++c) {
-        const int cc = (c + tid) & (CH - 1);
-        const uint4 x = r4[cc];
+      for (int x = 0; x < kKUn; ++x) {
+        const int t = b0 + x * kCW * RPW + rw;
+        if (t < n_sl) {
+          const uint4* r4 = reinterpret_cast<const uint4*>(keys_g + (int64_t)S.sid[t] * D);
 #pragma unroll
-        for (int hh = 0; hh < kCMaxGs; ++hh)
-          if (hh < gs) acc[hh] += (double)bf16x8_dot(q4[hh * CH + cc], x, 0.f);
+          for (int c = 0; c < CPL; ++c) raw[x][c] = ldg16(r4 + c * LPR + sub);
+        } else {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) raw[x][c] = make_uint4(0, 0, 0, 0);
+        }
       }
-      double gmax = -INFINITY;
 #pragma unroll
-      for (int hh = 0; hh < kCMaxGs; ++hh)
-        if (hh < gs) {
-          const double a = acc[hh] * scale;
-          S.slg[hh * scap + b0 + tid] = a;
+      for (int x = 0; x < kKUn; ++x) {
+        const int t = b0 + x * kCW * RPW + rw;
+        double gmax = -INFINITY;
+#pragma unroll
+        for (int hh = 0; hh < GS; ++hh) {
+          double a = 0.0;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) a += (double)bf16x8_dot(q4[hh * CH + c * LPR + sub], raw[x][c], 0.f);
+#pragma unroll
+          for (int o = 1; o < LPR; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+          a *= scale;
+          if (sub == 0 && t < n_sl) lgg[(int64_t)hh * p.lmax + lo + t] = a;
           gmax = fmax(gmax, a);
         }
-      const int pos = lo + b0 + tid;
-      const uint64_t key = ((uint64_t)(~okey32((float)gmax)) << 32) | (uint32_t)pos;
-      S.keys[pos] = key;
-      kg[pos] = key;
+        if (sub == 0 && t < n_sl) {
+          const uint32_t k32 = ~okey32((float)gmax);
+          S.keys[lo + t] = k32;
+          kg[lo + t] = ((uint64_t)k32 << 32) | (uint32_t)(lo + t);
+        }
+      }
     }
-    __syncthreads();   // rows reused by the next batch
   }
-  cl.sync();   // #3: every slice's keys are complete
+  cl.sync();   // #3: every slice's keys are complete (and its logits/ids in L2)
   cmark(5);
 
   // CTA 0: prefetch the static partials into area A (its lists are dead)
-  const int ns = p.ns;
-  float* spo = reinterpret_cast<float*>(S.bm);
-  double* spml = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(S.bm) +
-                                           align16((size_t)ns * gs * D * 4));
-  const int64_t pbase = (int64_t)u * ns;
   if (r == 0) {
-    fence_proxy_async();
-    if (tid == 0) {
-      const uint32_t ob = (uint32_t)(ns * gs * D * 4);
-      bar_expect(&bar_st, ob);
-      bulk_g2s(spo, p.po + pbase * gs * D, ob, &bar_st);
-    }
+    for (int i = tid; i < ns * gs * D / 4; i += kCT)
+      cp_async16(S.spo + 4 * i, p.po + (int64_t)u * ns * gs * D + 4 * i);
     for (int i = tid; i < ns * gs; i += kCT) {
-      cp_async8(spml + i, p.pm + pbase * gs + i);
-      cp_async8(spml + ns * gs + i, p.pl + pbase * gs + i);
+      cp_async8(S.spml + i, p.pm + (int64_t)u * ns * gs + i);
+      cp_async8(S.spml + ns * gs + i, p.pl + (int64_t)u * ns * gs + i);
     }
     cp_async_commit();
   }
 
-  // ---- 4. top-rho' threshold over all L keys ----------------------------------------
+  // ---- 4. top-rho' boundary over all L keys --------------------------------------
   for (int pos = tid; pos < L; pos += kCT) {
     if (pos >= lo && pos < hi) continue;
     int o = 0;
-    while ((int)((int64_t)(o + 1) * L / kCL) <= pos) ++o;
+    while ((int)((int64_t)(o + 1) * L / CL) <= pos) ++o;
     S.keys[pos] = cl.map_shared_rank(S.keys, o)[pos];
   }
   __syncthreads();
   cmark(6);
   const int Rn = L > 0 ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
-  uint64_t lim = ~0ull;
-  int shift = 0;
-  if (Rn > 0 && Rn < L) chain_threshold(S.keys, L, Rn, S.hist, s_state, &lim, &shift);
-
+  uint32_t vb = 0xffffffffu;
+  int need = L;
+  if (Rn > 0 && Rn < L) chain_boundary(S.keys, L, Rn, S.hist, s_state, &vb, &need);
   cmark(7);
-  // ---- 5. attention over this slice's selected tokens --------------------------------
-  // ordered compaction of the selected slice offsets
+  // this CTA's share of the selected positions: ranks [Rn*r/CL, Rn*(r+1)/CL)
+  // in position order (ordered compaction, two block scans)
+  const int rlo = (int)((int64_t)Rn * r / CL), rhi = (int)((int64_t)Rn * (r + 1) / CL);
   {
-    const int pt = (n_sl + kCT - 1) / kCT;
-    int cnt = 0;
+    const int pt = (L + kCT - 1) / kCT;
+    int neq = 0;
     for (int e = 0; e < pt; ++e) {
       const int i = tid * pt + e;
-      cnt += (i < n_sl && (S.keys[lo + i] >> shift) <= lim);
+      neq += (i < L && S.keys[i] == vb);
     }
     int tot;
-    int o = block_exclusive_scan(cnt, &tot, S.scratch);
+    int eq0 = block_exclusive_scan(neq, &tot, S.scratch);
+    int nsel = 0;
+    int eqr = eq0;
     for (int e = 0; e < pt; ++e) {
       const int i = tid * pt + e;
-      if (i < n_sl && (S.keys[lo + i] >> shift) <= lim) S.spos[o++] = i;
+      if (i < L) {
+        const uint32_t k = S.keys[i];
+        nsel += (k < vb) || (k == vb && eqr < need);
+        eqr += (k == vb);
+      }
     }
-    if (tid == 0) s_state[3] = tot;
-    __syncthreads();
+    int rk = block_exclusive_scan(nsel, &tot, S.scratch);
+    eqr = eq0;
+    for (int e = 0; e < pt; ++e) {
+      const int i = tid * pt + e;
+      if (i < L) {
+        const uint32_t k = S.keys[i];
+        const bool s = (k < vb) || (k == vb && eqr < need);
+        eqr += (k == vb);
+        if (s) {
+          if (rk >= rlo && rk < rhi) S.spos[rk - rlo] = i;
+          ++rk;
+        }
+      }
+    }
   }
-  const int nsel = s_state[3];
-  // per-head max of the selected logits
-  {
-    double m8[kCMaxGs];
+  __syncthreads();   // keys dead from here: area B becomes the per-warp V sums
+  const int nmy = rhi - rlo;
+  cmark(8);
+
+  // ---- 5. attention over this CTA's selected tokens (online softmax) ------------
+  constexpr int VL = CH;                     // lanes per V row (one 16-byte chunk each)
+  constexpr int VR = 32 / VL;                // rows per warp pass
+  const int vsub = lane % VL, vrw = lane / VL;
+  float acc[GS][8];
 #pragma unroll
-    for (int hh = 0; hh < kCMaxGs; ++hh) m8[hh] = -INFINITY;
-    for (int k = tid; k < nsel; k += kCT) {
-      const int i = S.spos[k];
+  for (int hh = 0; hh < GS; ++hh)
 #pragma unroll
-      for (int hh = 0; hh < kCMaxGs; ++hh)
-        if (hh < gs) m8[hh] = fmax(m8[hh], S.slg[hh * scap + i]);
-    }
-#pragma unroll
-    for (int hh = 0; hh < kCMaxGs; ++hh)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m8[hh] = fmax(m8[hh], __shfl_xor_sync(0xffffffffu, m8[hh], o));
-    if (lane == 0)
-#pragma unroll
-      for (int hh = 0; hh < kCMaxGs; ++hh) S.scratch[warp * kCMaxGs + hh] = m8[hh];
-    __syncthreads();
-    if (tid < gs) {
-      double m = -INFINITY;
-      for (int w = 0; w < kCT / 32; ++w) m = fmax(m, S.scratch[w * kCMaxGs + tid]);
-      hm[tid] = m;
-      hl[tid] = 0.0;
-    }
-    __syncthreads();
+    for (int e = 0; e < 8; ++e) acc[hh][e] = 0.f;
+  if (tid < GS) {
+    hm[tid] = -INFINITY;
+    hl[tid] = 0.0;
   }
-  constexpr int DQ = D / 4;              // 4-element column groups
-  constexpr int RG = kCT / DQ;           // row groups
-  const int dq = tid % DQ, rg = tid / DQ;
-  float acc[kCMaxGs][4];
-#pragma unroll
-  for (int hh = 0; hh < kCMaxGs; ++hh)
-#pragma unroll
-    for (int e = 0; e < 4; ++e) acc[hh][e] = 0.f;
   const T* vals_g = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
-  double l8[kCMaxGs];
+  for (int b0 = 0; b0 < nmy; b0 += kCB) {
+    const int n = min(kCB, nmy - b0);
+    __syncthreads();   // previous batch's weights and ids consumed; hm/hl current
+    double* lgs = S.lgs;   // [GS][kCB] this batch's logits, then their exp weights
+    for (int i = tid; i < n; i += kCT) {
+      const int pos = S.spos[b0 + i];
+      S.vid[i] = __ldcg(recg + pos);
 #pragma unroll
-  for (int hh = 0; hh < kCMaxGs; ++hh) l8[hh] = 0.0;
-  for (int b0 = 0; b0 < nsel; b0 += kCB) {
-    const int n = min(kCB, nsel - b0);
-    if (tid == 0) bar_expect(&bar_rows, (uint32_t)(n * RB));
-    fence_proxy_async();
+      for (int hh = 0; hh < GS; ++hh) lgs[hh * kCB + i] = __ldcg(lgg + (int64_t)hh * p.lmax + pos);
+    }
     __syncthreads();
-    if (tid < n)
-      bulk_g2s(rows + (size_t)tid * D, vals_g + (int64_t)S.sid[S.spos[b0 + tid]] * D, RB, &bar_rows);
-    if (tid < n) {
-      const int i = S.spos[b0 + tid];
-#pragma unroll
-      for (int hh = 0; hh < kCMaxGs; ++hh)
-        if (hh < gs) {
-          const double e = exp(S.slg[hh * scap + i] - hm[hh]);
-          S.wts[hh * kCB + tid] = (float)e;
-          l8[hh] += e;
-        }
+    // running max per head (warp hh), then one exp per (head, token)
+    for (int hh = warp; hh < GS; hh += kCW) {
+      double m = -INFINITY;
+      for (int i = lane; i < n; i += 32) m = fmax(m, lgs[hh * kCB + i]);
+      m = warp_max_f64(m);
+      if (lane == 0) {
+        const double mn = fmax(m, hm[hh]);
+        hresc[hh] = hm[hh] == -INFINITY ? 0.0 : dexp(hm[hh] - mn);
+        hnew[hh] = mn;
+      }
     }
-    bar_wait(&bar_rows, ph);
-    ph ^= 1u;
-    __syncthreads();   // weights visible
-    for (int k = rg; k < n; k += RG) {
-      const uint2 raw = *reinterpret_cast<const uint2*>(rows + (size_t)k * D + 4 * dq);
-      const float v0 = __uint_as_float(raw.x << 16), v1 = __uint_as_float(raw.x & 0xffff0000u);
-      const float v2 = __uint_as_float(raw.y << 16), v3 = __uint_as_float(raw.y & 0xffff0000u);
-#pragma unroll
-      for (int hh = 0; hh < kCMaxGs; ++hh)
-        if (hh < gs) {
-          const float w = S.wts[hh * kCB + k];
-          acc[hh][0] = fmaf(w, v0, acc[hh][0]);
-          acc[hh][1] = fmaf(w, v1, acc[hh][1]);
-          acc[hh][2] = fmaf(w, v2, acc[hh][2]);
-          acc[hh][3] = fmaf(w, v3, acc[hh][3]);
-        }
+    __syncthreads();
+#pragma unroll 1
+    for (int i = tid; i < GS * n; i += kCT) {
+      const int hh = i / n, k = i - hh * n;
+      const double e = dexp(lgs[hh * kCB + k] - hnew[hh]);
+      lgs[hh * kCB + k] = e;
+      S.wts[hh * kCB + k] = (float)e;
     }
-    __syncthreads();   // rows and weights reused by the next batch
+    __syncthreads();
+    for (int hh = warp; hh < GS; hh += kCW) {
+      double l = 0.0;
+      for (int i = lane; i < n; i += 32) l += lgs[hh * kCB + i];
+      l = warp_sum_f64(l);
+      if (lane == 0) {
+        hl[hh] = hl[hh] * hresc[hh] + l;
+        hm[hh] = hnew[hh];
+      }
+    }
+    float resc[GS];
+#pragma unroll
+    for (int hh = 0; hh < GS; ++hh) resc[hh] = (float)hresc[hh];
+#pragma unroll
+    for (int hh = 0; hh < GS; ++hh)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[hh][e] *= resc[hh];
+    // weighted V rows: VL lanes per row, kVUn passes in flight
+    for (int t0 = warp * VR; t0 < n; t0 += kCW * VR * kVUn) {
+      uint4 raw[kVUn];
+#pragma unroll
+      for (int x = 0; x < kVUn; ++x) {
+        const int t = t0 + x * kCW * VR + vrw;
+        raw[x] = t < n ? ldg16(reinterpret_cast<const uint4*>(vals_g + (int64_t)S.vid[t] * D) + vsub)
+                       : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int x = 0; x < kVUn; ++x) {
+        const int t = t0 + x * kCW * VR + vrw;
+        if (t >= n) continue;
+        float f[8];
+        unpack16<T>(raw[x], f);
+#pragma unroll
+        for (int hh = 0; hh < GS; ++hh)
+          if (hh < gs) {
+            const float w = S.wts[hh * kCB + t];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[hh][e] = fmaf(w, f[e], acc[hh][e]);
+          }
+      }
+    }
   }
-  // l per head: block reduce
+  // rows of a warp pass -> one partial per warp, then over the warps
 #pragma unroll
-  for (int hh = 0; hh < kCMaxGs; ++hh)
+  for (int hh = 0; hh < GS; ++hh)
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l8[hh] += __shfl_xor_sync(0xffffffffu, l8[hh], o);
-  if (lane == 0)
+    for (int e = 0; e < 8; ++e)
 #pragma unroll
-    for (int hh = 0; hh < kCMaxGs; ++hh) S.scratch[warp * kCMaxGs + hh] = l8[hh];
-  // row-group partial sums -> rows area, then reduce over the row groups
-  float* red = reinterpret_cast<float*>(S.rows);
+      for (int o = VL; o < 32; o <<= 1) acc[hh][e] += __shfl_xor_sync(0xffffffffu, acc[hh][e], o);
+  __syncthreads();
+  if (vrw == 0)
 #pragma unroll
-  for (int hh = 0; hh < kCMaxGs; ++hh)
-    if (hh < gs)
-      *reinterpret_cast<float4*>(red + ((size_t)rg * gs + hh) * D + 4 * dq) =
-          make_float4(acc[hh][0], acc[hh][1], acc[hh][2], acc[hh][3]);
+    for (int hh = 0; hh < GS; ++hh)
+      if (hh < gs) {
+        float4* dst = reinterpret_cast<float4*>(S.red + ((size_t)warp * gs + hh) * D + 8 * vsub);
+        dst[0] = make_float4(acc[hh][0], acc[hh][1], acc[hh][2], acc[hh][3]);
+        dst[1] = make_float4(acc[hh][4], acc[hh][5], acc[hh][6], acc[hh][7]);
+      }
   __syncthreads();
   float* cpo0 = cl.map_shared_rank(S.cpo, 0);
   double* cpml0 = cl.map_shared_rank(S.cpml, 0);
   for (int i = tid; i < gs * D; i += kCT) {
     float s = 0.f;
-    for (int g2 = 0; g2 < RG; ++g2) s += red[(size_t)g2 * gs * D + i];
+    for (int w = 0; w < kCW; ++w) s += S.red[(size_t)w * gs * D + i];
     cpo0[(size_t)r * gs * D + i] = s;
   }
   if (tid < gs) {
-    double l = 0.0;
-    for (int w = 0; w < kCT / 32; ++w) l += S.scratch[w * kCMaxGs + tid];
-    cpml0[r * gs + tid] = nsel > 0 ? hm[tid] : -INFINITY;
-    cpml0[kCL * gs + r * gs + tid] = nsel > 0 ? l : 0.0;
+    cpml0[r * gs + tid] = nmy > 0 ? hm[tid] : -INFINITY;
+    cpml0[CL * gs + r * gs + tid] = nmy > 0 ? hl[tid] : 0.0;
   }
-  cmark(8);
-  cl.sync();   // #4: all sparse partials are in CTA 0
   cmark(9);
+  cl.sync();   // #4: all sparse partials are in CTA 0
   if (r != 0) return;
 
   // ---- 6. CTA 0: exact merge with the static partials ---------------------------------
-  bar_wait(&bar_st, 0);
   cp_async_wait_all();
   __syncthreads();
-  double* wj = S.scratch;   // [gs][ns + kCL] split weights
-  const int nsp = ns + kCL;
+  double* wj = S.scratch;   // [gs][ns + CL] split weights
+  const int nsp = ns + CL;
   if (tid < gs) {
     const int hh = tid;
     double M = -INFINITY;
+#pragma unroll 1
     for (int j = 0; j < ns; ++j)
-      if (spml[ns * gs + j * gs + hh] > 0.0) M = fmax(M, spml[j * gs + hh]);
-    for (int k = 0; k < kCL; ++k)
-      if (S.cpml[kCL * gs + k * gs + hh] > 0.0) M = fmax(M, S.cpml[k * gs + hh]);
-    double Ls = 0.0;
-    for (int j = 0; j < ns; ++j) {
-      const double lj = spml[ns * gs + j * gs + hh];
-      const double w = lj > 0.0 ? exp(spml[j * gs + hh] - M) : 0.0;
-      wj[hh * nsp + j] = w;
-      Ls += w * lj;
-    }
-    for (int k = 0; k < kCL; ++k) {
-      const double lk = S.cpml[kCL * gs + k * gs + hh];
-      const double w = lk > 0.0 ? exp(S.cpml[k * gs + hh] - M) : 0.0;
-      wj[hh * nsp + ns + k] = w;
-      Ls += w * lk;
-    }
+      if (S.spml[ns * gs + j * gs + hh] > 0.0) M = fmax(M, S.spml[j * gs + hh]);
+    for (int c = 0; c < CL; ++c)
+      if (S.cpml[CL * gs + c * gs + hh] > 0.0) M = fmax(M, S.cpml[c * gs + hh]);
     hm[hh] = M;
+  }
+  __syncthreads();
+  for (int i = tid; i < gs * nsp; i += kCT) {   // one exp per (head, split), in parallel
+    const int hh = i / nsp, j = i % nsp;
+    const double mj = j < ns ? S.spml[j * gs + hh] : S.cpml[(j - ns) * gs + hh];
+    const double lj = j < ns ? S.spml[ns * gs + j * gs + hh] : S.cpml[CL * gs + (j - ns) * gs + hh];
+    wj[i] = lj > 0.0 ? dexp(mj - hm[hh]) : 0.0;
+  }
+  __syncthreads();
+  if (tid < gs) {
+    const int hh = tid;
+    double Ls = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < ns; ++j) Ls += wj[hh * nsp + j] * S.spml[ns * gs + j * gs + hh];
+    for (int c = 0; c < CL; ++c) Ls += wj[hh * nsp + ns + c] * S.cpml[CL * gs + c * gs + hh];
     hl[hh] = Ls;
   }
   __syncthreads();
   bool none = false;
+#pragma unroll 1
   for (int i = tid; i < gs * D; i += kCT) {
     const int hh = i / D, e = i % D;
     const double* wh = wj + hh * nsp;
     double O = 0.0;
-    for (int j = 0; j < ns; ++j) O += wh[j] * (double)spo[(j * gs + hh) * D + e];
-    for (int k = 0; k < kCL; ++k) O += wh[ns + k] * (double)S.cpo[((size_t)k * gs + hh) * D + e];
+#pragma unroll 1
+    for (int j = 0; j < ns; ++j) O += wh[j] * (double)S.spo[(j * gs + hh) * D + e];
+    for (int c = 0; c < CL; ++c) O += wh[ns + c] * (double)S.cpo[((size_t)c * gs + hh) * D + e];
     const double Ls = hl[hh];
     const int64_t oh = (int64_t)bi * p.h + gi * gs + hh;
     if (Ls > 0.0) {
@@ -561,7 +625,7 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 1) chain_kern
     set_flag(p.flags, L > 0 ? kFlagNonEmptyRecall : kFlagEmptyRecall);
   }
   if (p.selected)
-    for (int k = tid; k < p.c_prime; k += kCT) p.selected[(int64_t)u * p.c_prime + k] = sel[k];
+    for (int k2 = tid; k2 < p.c_prime; k2 += kCT) p.selected[(int64_t)u * p.c_prime + k2] = sel[k2];
   cmark(10);
 }
 
@@ -569,17 +633,26 @@ __global__ void __cluster_dims__(kCL, 1, 1) __launch_bounds__(kCT, 1) chain_kern
 // launcher
 // ------------------------------------------------------------------------
 
-template <typename T, int D>
+static int chain_cl() {   // CTKV_CHAIN_CL=8 selects 8-CTA clusters (A/B)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CTKV_CHAIN_CL");
+    v = (e && e[0] == '8') ? 8 : 4;
+  }
+  return v;
+}
+
+template <typename T, int D, int CL, int GS>
 static int launch_chain_t(const DecodeParams& p, cudaStream_t st) {
-  const size_t sm = chain_layout(p, D, sizeof(T), nullptr, nullptr);
-  auto k = chain_kernel<T, D>;
+  const size_t sm = chain_layout(p, D, CL, nullptr, nullptr);
+  auto k = chain_kernel<T, D, CL, GS>;
   static size_t configured = 0;
   if (sm > configured) {
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))
       return CTKV_ECUDA;
     configured = sm;
   }
-  k<<<p.U * kCL, kCT, sm, st>>>(p);
+  k<<<p.U * CL, kCT, sm, st>>>(p);
   return cudaGetLastError() == cudaSuccess ? CTKV_OK : CTKV_ECUDA;
 }
 
@@ -595,16 +668,32 @@ int chain_phase_timing(int on, unsigned long long* out, int n) {
 
 bool chain_supported(const DecodeParams& p, int dtype, int D) {
   if (dtype != CTKV_BF16 || (D != 64 && D != 128)) return false;
-  if (p.gs > kCMaxGs || p.c_prime > kCMaxLists) return false;
-  const int per = (p.rho + kCT - 1) / kCT;
-  if (chain_nlo(p.c_prime) * per > kCMaxOwn) return false;
-  return chain_layout(p, D, 2, nullptr, nullptr) <= 220 * 1024;
+  if ((p.gs != 1 && p.gs != 2 && p.gs != 4 && p.gs != 8) || p.c_prime > kCMaxLists) return false;
+  const int CL = chain_cl();
+  if ((p.rho + kCT - 1) / kCT > kCMaxPer) return false;
+  return chain_layout(p, D, CL, nullptr, nullptr) <= 200 * 1024;
+}
+
+template <int D, int CL>
+static int launch_chain_g(const DecodeParams& p, cudaStream_t st) {
+  switch (p.gs) {
+    case 1: return launch_chain_t<__nv_bfloat16, D, CL, 1>(p, st);
+    case 2: return launch_chain_t<__nv_bfloat16, D, CL, 2>(p, st);
+    case 4: return launch_chain_t<__nv_bfloat16, D, CL, 4>(p, st);
+    case 8: return launch_chain_t<__nv_bfloat16, D, CL, 8>(p, st);
+  }
+  return CTKV_ESHAPE;
+}
+
+template <int D>
+static int launch_chain_d(const DecodeParams& p, cudaStream_t st) {
+  return chain_cl() == 8 ? launch_chain_g<D, 8>(p, st) : launch_chain_g<D, 4>(p, st);
 }
 
 int launch_chain(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
   if (dtype != CTKV_BF16) return CTKV_ECONFIG;
-  if (D == 128) return launch_chain_t<__nv_bfloat16, 128>(p, st);
-  if (D == 64) return launch_chain_t<__nv_bfloat16, 64>(p, st);
+  if (D == 128) return launch_chain_d<128>(p, st);
+  if (D == 64) return launch_chain_d<64>(p, st);
   return CTKV_ESHAPE;
 }
 

@@ -251,14 +251,21 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
   double* qn = reinterpret_cast<double*>(qs + gs * D);                    // [gs]
   double* cosv = qn + gs;                                                 // [gs*CC]
   double* gv = cosv + kScanRowsV2;                                        // [CC] group max
+  float* cns = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(gv + CC) + 15) &
+                                        ~uintptr_t(15));                  // [gs][CC] |c|
   const T* cent = static_cast<const T*>(p.cent);
+  // cached centroid norms ride with the rows when 16-byte aligned
+  const bool cn_bulk = p.cnorm != nullptr && (p.C & 3) == 0 && (nc & 3) == 0;
   if (threadIdx.x == 0) {
     // one barrier per head block: rows of head j are computed as soon as they land
     for (int j = 0; j < gs; ++j) {
       bar_init(&bars[j], 1);
-      bar_expect(&bars[j], (uint32_t)(nc * RB));
+      bar_expect(&bars[j], (uint32_t)(nc * RB) + (cn_bulk ? (uint32_t)(nc * 4) : 0u));
       bulk_g2s(rows + (size_t)j * CC * D, cent + (((int64_t)bi * p.h + gi * gs + j) * p.C + c0) * D,
                (uint32_t)(nc * RB), &bars[j]);
+      if (cn_bulk)
+        bulk_g2s(cns + j * CC, p.cnorm + ((int64_t)bi * p.h + gi * gs + j) * p.C + c0,
+                 (uint32_t)(nc * 4), &bars[j]);
     }
   }
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
@@ -274,7 +281,8 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
     double cn;
     if (p.cnorm != nullptr) {
       row_dot<T, D, false>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
-      cn = (double)__ldg(p.cnorm + ((int64_t)bi * p.h + gi * gs + j) * p.C + c0 + c);
+      cn = cn_bulk ? (double)cns[j * CC + c]
+                   : (double)__ldg(p.cnorm + ((int64_t)bi * p.h + gi * gs + j) * p.C + c0 + c);
     } else {
       row_dot<T, D, true>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
       cn = sqrt(nrm);
@@ -295,6 +303,23 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
     for (int j = 1; j < gs; ++j) m = fmax(m, cosv[j * CC + c]);
     p.gcos[(int64_t)u * p.C + c0 + c] = m;
     gv[c] = m;
+  }
+  // v6: the unit's last cosine chunk takes the top-C' of all C group maxima
+  if (p.selg != nullptr) {
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(&p.selctr[u], 1) == cpu - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      block_top_slots(p.gcos + (int64_t)u * p.C, p.C, p.c_prime, p.selg + (int64_t)u * p.c_prime,
+                      cosv, reinterpret_cast<int*>(cosv + 64));
+      if (threadIdx.x == 0) p.selctr[u] = 0;
+    }
+    return;
   }
   // chunk-local top-C' candidates (value desc, slot asc): the global top-C'
   // is contained in the union of the chunks' candidates
@@ -326,21 +351,6 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
         }
         prev_key = bk;
         prev_idx = bidx;
-      }
-    }
-    // the unit's last cosine chunk turns the candidates into its top-C' slots
-    if (p.selg != nullptr) {
-      __shared__ int s_last;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&p.selctr[u], 1) == cpu - 1;
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        if (threadIdx.x < 32) warp_top_slots(p, u, p.selg + (int64_t)u * p.c_prime);
-        if (threadIdx.x == 0) p.selctr[u] = 0;
       }
     }
   }
@@ -640,21 +650,6 @@ __device__ void scan3_cos(const DecodeParams& p, int task, const unsigned char* 
         prev_idx = bidx;
       }
     }
-    // the unit's last cosine chunk turns the candidates into its top-C' slots
-    if (p.selg != nullptr) {
-      __shared__ int s_last;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&p.selctr[u], 1) == cpu - 1;
-      }
-      __syncthreads();
-      if (s_last) {
-        __threadfence();
-        if (threadIdx.x < 32) warp_top_slots(p, u, p.selg + (int64_t)u * p.c_prime);
-        if (threadIdx.x == 0) p.selctr[u] = 0;
-      }
-    }
   }
 }
 
@@ -799,7 +794,7 @@ size_t scan2_smem(int gs) {
   constexpr int RB = D * int(sizeof(T));
   constexpr int ST = static_tok<T>();
   const size_t cosb = (size_t)kScanRowsV2 * RB + sizeof(float) * gs * D + sizeof(double) * gs +
-                      sizeof(double) * 2 * kScanRowsV2;
+                      sizeof(double) * 2 * kScanRowsV2 + sizeof(float) * kScanRowsV2 + 16;
   const size_t stb = (size_t)2 * ST * RB + sizeof(float) * gs * D + sizeof(double) * gs * ST +
                      sizeof(float) * gs * ST + sizeof(double) * 2 * gs;
   return cosb > stb ? cosb : stb;

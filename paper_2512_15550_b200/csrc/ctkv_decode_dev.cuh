@@ -115,7 +115,7 @@ __device__ void write_slot_norms(const DecodeParams& p, const T* q, int bi, int 
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-static __device__ int block_exclusive_scan(int x, int* total, double* scratch) {
+static __device__ __noinline__ int block_exclusive_scan(int x, int* total, double* scratch) {
   int* ws = reinterpret_cast<int*>(scratch);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int incl = x;
@@ -262,6 +262,87 @@ static __device__ void warp_top_slots(const DecodeParams& p, int u, int32_t* sel
     if (lane == 0) sel[r] = bidx;
     prev_key = bk;
     prev_idx = bidx;
+  }
+}
+
+// Top-C' slots of vals[0..C) (value desc, slot asc; ck/tensor_ops.py:121-141
+// on the group-max cosines of ck/retrieval.py:145-154) with the whole block:
+// every warp takes the top-C' of a contiguous chunk (lanes hold up to 8
+// values), then warp 0 takes the top-C' of the warps' candidates.  cand:
+// shared scratch of (blockDim/32) * c' (double, int) pairs.  c' <= 8.
+static __device__ __noinline__ void block_top_slots(const double* vals, int C, int cp, int32_t* out,
+                                                    double* cval, int* cidx) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int chunk = (C + nw - 1) / nw;
+  const int c0 = warp * chunk, c1 = min(C, c0 + chunk);
+  constexpr int KR = 8;
+  uint64_t rk[KR];
+  int ri[KR];
+#pragma unroll
+  for (int x = 0; x < KR; ++x) {
+    const int c = c0 + lane + 32 * x;
+    rk[x] = c < c1 ? okey64(__ldcg(vals + c)) : 0ull;
+    ri[x] = c < c1 ? c : INT32_MAX;
+  }
+  uint64_t prev_key = ~0ull;
+  int prev_idx = -1;
+  for (int r = 0; r < cp; ++r) {
+    uint64_t bk = 0;
+    int bidx = INT32_MAX;
+#pragma unroll
+    for (int x = 0; x < KR; ++x) {
+      const bool below = rk[x] < prev_key || (rk[x] == prev_key && ri[x] > prev_idx);
+      if (below && (rk[x] > bk || (rk[x] == bk && ri[x] < bidx))) { bk = rk[x]; bidx = ri[x]; }
+    }
+    for (int c = c0 + lane + 32 * KR; c < c1; c += 32) {   // chunks > 256 values only
+      const uint64_t k = okey64(__ldcg(vals + c));
+      const bool below = k < prev_key || (k == prev_key && c > prev_idx);
+      if (below && (k > bk || (k == bk && c < bidx))) { bk = k; bidx = c; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
+    }
+    if (lane == 0) {
+      cval[warp * cp + r] = bidx == INT32_MAX ? -INFINITY : __ldcg(vals + bidx);
+      cidx[warp * cp + r] = bidx;
+    }
+    prev_key = bk;
+    prev_idx = bidx;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int M = nw * cp;   // <= 32 * 8
+    uint64_t k8[KR];
+    int i8[KR];
+#pragma unroll
+    for (int x = 0; x < KR; ++x) {
+      const int m = lane + 32 * x;
+      k8[x] = m < M && cidx[m] != INT32_MAX ? okey64(cval[m]) : 0ull;
+      i8[x] = m < M ? cidx[m] : INT32_MAX;
+    }
+    prev_key = ~0ull;
+    prev_idx = -1;
+    for (int r = 0; r < cp; ++r) {
+      uint64_t bk = 0;
+      int bidx = INT32_MAX;
+#pragma unroll
+      for (int x = 0; x < KR; ++x) {
+        const bool below = k8[x] < prev_key || (k8[x] == prev_key && i8[x] > prev_idx);
+        if (below && (k8[x] > bk || (k8[x] == bk && i8[x] < bidx))) { bk = k8[x]; bidx = i8[x]; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
+        if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
+      }
+      if (lane == 0) out[r] = bidx;
+      prev_key = bk;
+      prev_idx = bidx;
+    }
   }
 }
 
