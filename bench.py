@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--build-mode", type=int, default=1, help="0 exact f64, 1 fast")
-    ap.add_argument("--lanes", type=int, default=4,
+    ap.add_argument("--lanes", type=int, default=8,
                     help="micro-batch lanes per GPU (sequence groups on their own streams)")
     return ap.parse_args()
 
@@ -450,7 +450,8 @@ def main():
                       "mode": "fast" if a.build_mode else "exact-f64"},
             "e2e": {"value": e2e_tok_s, "unit": "tok/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
-            "gpu_launches": (1 if fused else 2) * nl * a.lanes * a.steps,
+            # per (lane, layer): scan + chain + deferred tail kernels
+            "gpu_launches": (1 if fused else 3) * nl * a.lanes * a.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "graph": use_graph,

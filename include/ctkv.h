@@ -232,6 +232,9 @@ int ctkv_topk_rows(const float* values, int64_t rows, int64_t n, int32_t k, int3
  * kernel on/off (on<0 leaves it); host_out (may be NULL) receives up to n
  * u64 globaltimer stamps laid out [256 CTAs][12 checkpoints]. */
 int ctkv_debug_phase_timing(int32_t on, uint64_t* host_out, int32_t n);
+/* Profiling only: per-CTA task timeline of the persistent scan kernel
+ * ([cta][slot] globaltimer ns: 0 start, 1 end, 2+k task k ready). */
+int ctkv_debug_scan_timeline(int32_t on, uint64_t* host_out, int32_t n);
 
 #ifdef __cplusplus
 }

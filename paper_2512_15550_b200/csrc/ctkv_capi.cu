@@ -296,9 +296,15 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   if (v2 && ctkv::decode_variant() == 6 && chain_supported(p, L->dtype, L->head_dim)) {
     p.selg = w.selg;
     p.selctr = w.selctr;
+    p.sel_in_chain = ctkv::scan_variant_v6() == 4 && scan4_supported(p, L->dtype, L->head_dim);
     const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
-    if (phase & 1)
-      if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;
+    if (phase & 1) {
+      // scan4 has no last-CTA top-C' selection: the chain then selects itself
+      const bool s4 = p.sel_in_chain;
+      if (int rc = s4 ? launch_scan4(p, L->dtype, L->head_dim, st)
+                      : launch_scan(p, L->dtype, L->head_dim, nblocks, st))
+        return rc;
+    }
     if (phase & 2)
       if (int rc = launch_chain(p, L->dtype, L->head_dim, st)) return rc;
     const bool tail = (phase & 4) || ((phase & 2) && !(phase & 8));
@@ -511,6 +517,10 @@ int ctkv_centroid_norms(const ctkv_layout* L, const void* centroids, int32_t cap
   const int64_t rows = (int64_t)L->batch * L->query_heads * capacity;
   return launch_centroid_norms(L->dtype, L->head_dim, centroids, rows, cnorm,
                                static_cast<cudaStream_t>(stream));
+}
+
+int ctkv_debug_scan_timeline(int32_t on, uint64_t* host_out, int32_t n) {
+  return ctkv::scan4_timeline(on, reinterpret_cast<unsigned long long*>(host_out), n);
 }
 
 int ctkv_debug_phase_timing(int32_t on, uint64_t* host_out, int32_t n) {

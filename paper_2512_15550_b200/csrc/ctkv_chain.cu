@@ -231,7 +231,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
   cmark(0);
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = tid; i < gs * D; i += kCT) qs[i] = q[i];
-  if (tid < p.c_prime) sel[tid] = __ldcg(p.selg + (int64_t)u * p.c_prime + tid);
+  if (p.sel_in_chain) {   // scan4: top-C' of the unit's group-max cosines here
+    block_top_slots(p.gcos + (int64_t)u * p.C, p.C, p.c_prime, sel, S.scratch,
+                    reinterpret_cast<int*>(S.scratch + kCW * kCMaxLists));
+  } else if (tid < p.c_prime) {
+    sel[tid] = __ldcg(p.selg + (int64_t)u * p.c_prime + tid);
+  }
   __syncthreads();
   cmark(1);
 

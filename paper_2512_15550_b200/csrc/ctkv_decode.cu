@@ -2653,6 +2653,18 @@ int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
 // Decode path for bf16 (A/B switch CTKV_DECODE): 6 = 4-CTA cluster chain
 // kernel + deferred tail (default), 2 = 2-CTA cluster unit kernel, 5 = wide
 // unit pipeline, 4 = persistent layer kernel.
+// v6 scan kernel (A/B switch CTKV_SCAN): 2 = scan2 (default), 4 = the
+// persistent scan4 (faster alone, but its 1-CTA-per-SM footprint overlaps
+// worse with the lanes' chain kernels: measured 1820 vs 2242 tok/s)
+int scan_variant_v6() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CTKV_SCAN");
+    v = (e && e[0] == '4') ? 4 : 2;
+  }
+  return v;
+}
+
 int decode_variant() {
   static int v = -1;
   if (v < 0) {

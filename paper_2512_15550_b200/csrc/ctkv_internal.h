@@ -74,6 +74,7 @@ struct DecodeParams {
   // v6 chain: the scan's last cosine CTA of a unit writes its top-C' slots
   int32_t* selg;    // [U][c'] top-C' slots (ties -> smaller slot)
   int* selctr;      // [U] cosine-chunk completion counters (reset by the last CTA)
+  int sel_in_chain; // 1: the chain kernel selects top-C' from gcos itself (scan4)
   // staged io
   const int32_t* rec_in;
   const int32_t* len_in;
@@ -103,11 +104,16 @@ int static_tok_for(int dtype);
 int phase_timing(int on, unsigned long long* out, int n);
 int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int decode_variant();
+int scan_variant_v6();
 bool wide_supported(const DecodeParams& p, int dtype, int D);
 // what: 1 = recall + attend kernels, 2 = tail (DCU, sparse ids, cursor/total)
 int launch_wide(const DecodeParams& p, int dtype, int D, int what, cudaStream_t st);
 bool chain_supported(const DecodeParams& p, int dtype, int D);
 // v6: the unit chain on a 4-CTA cluster per unit (ctkv_chain.cu)
+bool scan4_supported(const DecodeParams& p, int dtype, int D);
+// persistent warp-specialised streaming scan (ctkv_scan.cu; CTKV_SCAN=4)
+int launch_scan4(const DecodeParams& p, int dtype, int D, cudaStream_t st);
+int scan4_timeline(int on, unsigned long long* out, int n);
 int chain_phase_timing(int on, unsigned long long* out, int n);
 int launch_chain(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_centroid_norms(int dtype, int D, const void* cent, int64_t rows, float* out, cudaStream_t st);
