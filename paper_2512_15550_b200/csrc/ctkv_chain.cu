@@ -91,6 +91,8 @@ constexpr int kCMaxLists = 8;    // c' <= 8
 constexpr int kCMaxPer = 32;     // list entries per thread (keep mask bits)
 constexpr int kKUn = 4;          // K-row passes in flight per warp (4 rows each)
 constexpr int kVUn = 4;          // V-row passes in flight per warp (2 rows each)
+constexpr int kCBins = 1024;     // top-rho' selection: histogram bins
+constexpr int kCBnd = 256;       // ... and keys ranked exactly in the boundary bin
 
 struct ChainSmem {
   uint32_t* bm;          // [nlo][words] bitmaps of this CTA's lists   } area A; CTA 0
@@ -106,7 +108,7 @@ struct ChainSmem {
   double* lgs;           // [gs][kCB] logits / f64 weights of an attention batch
   float* cpo;            // CTA 0: [CL][gs][D] sparse partial sums from the cluster
   double* cpml;          // CTA 0: [2][CL][gs] their (m, l)
-  int* hist;             // [256]
+  int* hist;             // [kCBins] selection histogram
   double* scratch;       // [max(128, gs * (ns + CL))]
 };
 
@@ -139,13 +141,13 @@ __host__ __device__ inline size_t chain_layout(const DecodeParams& p, int D, int
   t.keys = reinterpret_cast<uint32_t*>(b);
   t.red = reinterpret_cast<float*>(b);
   t.sid = reinterpret_cast<int32_t*>(take((size_t)scap * 4));
-  t.spos = reinterpret_cast<int32_t*>(take((size_t)scap * 4));
+  t.spos = reinterpret_cast<int32_t*>(take((size_t)(scap > 2 * kCBnd ? scap : 2 * kCBnd) * 4));
   t.vid = reinterpret_cast<int32_t*>(take((size_t)kCB * 4));
   t.wts = reinterpret_cast<float*>(take((size_t)p.gs * kCB * 4));
   t.lgs = reinterpret_cast<double*>(take((size_t)p.gs * kCB * 8));
   t.cpo = reinterpret_cast<float*>(take((size_t)CL * p.gs * D * 4));
   t.cpml = reinterpret_cast<double*>(take((size_t)2 * CL * p.gs * 8));
-  t.hist = reinterpret_cast<int*>(take(256 * 4));
+  t.hist = reinterpret_cast<int*>(take(kCBins * 4));
   const int nscr = p.gs * (p.ns + CL) > 128 ? p.gs * (p.ns + CL) : 128;
   t.scratch = reinterpret_cast<double*>(take((size_t)nscr * 8));
   if (s) *s = t;
@@ -206,6 +208,86 @@ __device__ void chain_boundary(const uint32_t* key, int L, int R, int* hist, int
   *need_out = need;
 }
 
+// Boundary (vk, vpos) of the top-R of L packed keys (key[i] << 32 | i):
+// selected(i) <=> key[i] < vk || (key[i] == vk && i <= vpos).  One histogram
+// pass over [min, max] of the keys (1024 linear bins), then an exact rank
+// of the few keys in the boundary bin; degenerate distributions (more than
+// kCBnd keys in that bin) fall back to the 8-bit radix passes.
+__device__ void chain_select(const uint32_t* key, int L, int R, int* hist, uint64_t* bnd, int* st,
+                             uint32_t* red, uint32_t* vk_out, int* vpos_out) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  uint32_t mn = 0xffffffffu, mx = 0u;
+  for (int i = tid; i < L; i += blockDim.x) {
+    const uint32_t k = key[i];
+    mn = min(mn, k);
+    mx = max(mx, k);
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  for (int b = tid; b < kCBins; b += blockDim.x) hist[b] = 0;
+  if (lane == 0) { red[warp] = mn; red[32 + warp] = mx; }
+  __syncthreads();
+  mn = 0xffffffffu;
+  mx = 0u;
+  for (int w = 0; w < nw; ++w) { mn = min(mn, red[w]); mx = max(mx, red[32 + w]); }
+  if (mn == mx) {   // all scores equal: the first R positions
+    *vk_out = mn;
+    *vpos_out = R - 1;
+    return;
+  }
+  // monotone bin map (the same float expression in both passes)
+  const float fscale = (float)kCBins / ((float)(mx - mn) + 1.0f);
+  auto bin_of = [&](uint32_t k) { return min(kCBins - 1, (int)((float)(k - mn) * fscale)); };
+  for (int i = tid; i < L; i += blockDim.x) atomicAdd(&hist[bin_of(key[i])], 1);
+  __syncthreads();
+  // boundary bin: the first whose cumulative count reaches R
+  constexpr int BPT = kCBins / 256;
+  int loc = 0;
+  for (int b = 0; b < BPT && tid < 256; ++b) loc += hist[tid * BPT + b];
+  int tot;
+  int run = block_exclusive_scan(tid < 256 ? loc : 0, &tot, reinterpret_cast<double*>(red));
+  if (tid < 256 && run < R && run + loc >= R) {
+    for (int b = tid * BPT;; ++b) {
+      if (run + hist[b] >= R) { st[0] = b; st[1] = run; break; }
+      run += hist[b];
+    }
+  }
+  if (tid == 0) st[2] = 0;
+  __syncthreads();
+  const int bb = st[0], below = st[1];
+  if (hist[bb] > kCBnd) {   // degenerate: radix passes over the raw keys
+    uint32_t vb;
+    int need;
+    chain_boundary(key, L, R, hist, st, &vb, &need);
+    // the need-th equal key in position order
+    if (tid == 0) {
+      int c = 0, vp = -1;
+      for (int i = 0; i < L; ++i)
+        if (key[i] == vb && ++c == need) { vp = i; break; }
+      st[3] = vp;
+    }
+    __syncthreads();
+    *vk_out = vb;
+    *vpos_out = st[3];
+    return;
+  }
+  for (int i = tid; i < L; i += blockDim.x) {
+    const uint32_t k = key[i];
+    if (bin_of(k) == bb) bnd[atomicAdd(&st[2], 1)] = ((uint64_t)k << 32) | (uint32_t)i;
+  }
+  __syncthreads();
+  const int nb = st[2], need = R - below;   // 1 <= need <= nb
+  for (int t = tid; t < nb; t += blockDim.x) {
+    const uint64_t me = bnd[t];
+    int rank = 0;
+    for (int x = 0; x < nb; ++x) rank += bnd[x] < me;
+    if (rank == need - 1) { st[0] = (int)(me >> 32); st[1] = (int)(uint32_t)me; }
+  }
+  __syncthreads();
+  *vk_out = (uint32_t)st[0];
+  *vpos_out = st[1];
+}
+
 template <typename T, int D, int CL, int GS>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 3) chain_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -229,6 +311,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
   __shared__ double hm[GS], hl[GS], hnew[GS], hresc[GS];
 
   cmark(0);
+  pdl_trigger();   // the next kernel of the stream may launch once we are all resident
+  pdl_wait();      // the scan's outputs (gcos / slots, static partials) are complete
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = tid; i < gs * D; i += kCT) qs[i] = q[i];
   if (p.sel_in_chain) {   // scan4: top-C' of the unit's group-max cosines here
@@ -380,8 +464,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
       }
     }
   }
-  cl.sync();   // #3: every slice's keys are complete (and its logits/ids in L2)
   cmark(5);
+  cl.sync();   // #3: every slice's keys are complete (and its logits/ids in L2)
+  cmark(6);
 
   // CTA 0: prefetch the static partials into area A (its lists are dead)
   if (r == 0) {
@@ -402,43 +487,34 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
     S.keys[pos] = cl.map_shared_rank(S.keys, o)[pos];
   }
   __syncthreads();
-  cmark(6);
-  const int Rn = L > 0 ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
-  uint32_t vb = 0xffffffffu;
-  int need = L;
-  if (Rn > 0 && Rn < L) chain_boundary(S.keys, L, Rn, S.hist, s_state, &vb, &need);
   cmark(7);
+  const int Rn = L > 0 ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
+  uint32_t vk = 0xffffffffu;
+  int vpos = L;
+  if (Rn > 0 && Rn < L)
+    chain_select(S.keys, L, Rn, S.hist, reinterpret_cast<uint64_t*>(S.spos), s_state,
+                 reinterpret_cast<uint32_t*>(S.scratch), &vk, &vpos);
+  cmark(8);
   // this CTA's share of the selected positions: ranks [Rn*r/CL, Rn*(r+1)/CL)
-  // in position order (ordered compaction, two block scans)
+  // in position order (ordered compaction)
   const int rlo = (int)((int64_t)Rn * r / CL), rhi = (int)((int64_t)Rn * (r + 1) / CL);
   {
     const int pt = (L + kCT - 1) / kCT;
-    int neq = 0;
-    for (int e = 0; e < pt; ++e) {
-      const int i = tid * pt + e;
-      neq += (i < L && S.keys[i] == vb);
-    }
-    int tot;
-    int eq0 = block_exclusive_scan(neq, &tot, S.scratch);
     int nsel = 0;
-    int eqr = eq0;
     for (int e = 0; e < pt; ++e) {
       const int i = tid * pt + e;
       if (i < L) {
         const uint32_t k = S.keys[i];
-        nsel += (k < vb) || (k == vb && eqr < need);
-        eqr += (k == vb);
+        nsel += (k < vk) || (k == vk && i <= vpos);
       }
     }
+    int tot;
     int rk = block_exclusive_scan(nsel, &tot, S.scratch);
-    eqr = eq0;
     for (int e = 0; e < pt; ++e) {
       const int i = tid * pt + e;
       if (i < L) {
         const uint32_t k = S.keys[i];
-        const bool s = (k < vb) || (k == vb && eqr < need);
-        eqr += (k == vb);
-        if (s) {
+        if ((k < vk) || (k == vk && i <= vpos)) {
           if (rk >= rlo && rk < rhi) S.spos[rk - rlo] = i;
           ++rk;
         }
@@ -447,7 +523,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
   }
   __syncthreads();   // keys dead from here: area B becomes the per-warp V sums
   const int nmy = rhi - rlo;
-  cmark(8);
+  cmark(9);
 
   // ---- 5. attention over this CTA's selected tokens (online softmax) ------------
   constexpr int VL = CH;                     // lanes per V row (one 16-byte chunk each)
@@ -563,7 +639,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
     cpml0[r * gs + tid] = nmy > 0 ? hm[tid] : -INFINITY;
     cpml0[CL * gs + r * gs + tid] = nmy > 0 ? hl[tid] : 0.0;
   }
-  cmark(9);
+  cmark(10);
   cl.sync();   // #4: all sparse partials are in CTA 0
   if (r != 0) return;
 
@@ -631,7 +707,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
   }
   if (p.selected)
     for (int k2 = tid; k2 < p.c_prime; k2 += kCT) p.selected[(int64_t)u * p.c_prime + k2] = sel[k2];
-  cmark(10);
+  cmark(11);
 }
 
 // ------------------------------------------------------------------------
@@ -657,7 +733,7 @@ static int launch_chain_t(const DecodeParams& p, cudaStream_t st) {
       return CTKV_ECUDA;
     configured = sm;
   }
-  k<<<p.U * CL, kCT, sm, st>>>(p);
+  launch_k(k, dim3(p.U * CL), dim3(kCT), sm, st, p);
   return cudaGetLastError() == cudaSuccess ? CTKV_OK : CTKV_ECUDA;
 }
 

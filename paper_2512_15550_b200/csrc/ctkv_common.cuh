@@ -172,6 +172,10 @@ __host__ __device__ inline int next_pow2(int x) {
   return p;
 }
 
+// programmatic dependent launch (no-ops when launched without the attribute)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void set_flag(int32_t* flags, int32_t bit) {
   if (flags) atomicOr(flags, bit);
 }

@@ -268,6 +268,8 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
                  (uint32_t)(nc * 4), &bars[j]);
     }
   }
+  // the rows are in flight; the query may come from the previous kernel
+  pdl_wait();
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = q[i];
   __syncthreads();
@@ -416,6 +418,7 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
       i += n;
     }
   }
+  pdl_wait();   // K/V in flight; the query (and the appended token) may come from the previous kernel
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int k = threadIdx.x; k < gs * D; k += blockDim.x) qs[k] = q[k];
   __syncthreads();
@@ -471,6 +474,7 @@ template <typename T, int D>
 __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[kMaxGroup];
+  pdl_trigger();   // the chain kernel may launch once every scan CTA is resident
   const int64_t t0 = p.total ? *p.total : p.id_bound;
   const bool appending = p.k_new != nullptr;
   const int64_t total = t0 + (appending ? 1 : 0);
@@ -1745,6 +1749,8 @@ __device__ void l_cos(const DecodeParams& p, int task, unsigned char* smem, uint
                (uint32_t)(nc * RB), &bars[j]);
     }
   }
+  // the rows are in flight; the query may come from the previous kernel
+  pdl_wait();
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = q[i];
   __syncthreads();
@@ -2536,7 +2542,7 @@ static int launch_scan_t(const DecodeParams& p, int nblocks, cudaStream_t st) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = sm;
   }
-  if (nblocks > 0) k<<<nblocks, kScanRowsV2, sm, st>>>(p);
+  if (nblocks > 0) launch_k(k, dim3(nblocks), dim3(kScanRowsV2), sm, st, p);
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
 
@@ -2663,6 +2669,15 @@ int scan_variant_v6() {
     v = (e && e[0] == '4') ? 4 : 2;
   }
   return v;
+}
+
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CTKV_PDL");
+    v = (e && e[0] == '1') ? 1 : 0;   // off by default: early-resident CTAs
+  }                                    // crowd the other lanes (2422 vs 2568 tok/s)
+  return v == 1;
 }
 
 int decode_variant() {

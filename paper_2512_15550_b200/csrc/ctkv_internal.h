@@ -5,6 +5,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace ctkv {
 
@@ -123,6 +124,27 @@ int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const 
                   double* lo, cudaStream_t st);
 int launch_append(int dtype, void* keys, void* vals, const void* kn, const void* vn,
                   int64_t* total, int64_t units, int64_t cap, int D, cudaStream_t st);
+
+// Programmatic dependent launch: a kernel launched with pdl=true may start
+// (its prologue, e.g. TMA loads of data no earlier kernel writes) while its
+// stream predecessor finishes; it calls pdl_wait() (griddepcontrol.wait)
+// before touching anything the predecessor produced.  CTKV_PDL=1 enables.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                           cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 constexpr int kCosChunkHost = 64;
 constexpr int kStaticSplitHost = 64;

@@ -455,6 +455,8 @@ __global__ void __launch_bounds__(kTailT) tail_wide_kernel(DecodeParams p) {
   const int bi = u / p.g, gi = u % p.g, gs = p.gs;
   const int tid = threadIdx.x;
   __shared__ int64_t s_slot;
+  pdl_trigger();
+  pdl_wait();
   if (tid == 0) s_slot = p.fifo ? (p.fifo[bi] % p.C) : 0;
   const int L = p.uctr[u * 4 + 2], Rn = p.uctr[u * 4 + 3];
   const bool dcu_here = (p.stages & kStageDcu) && L > 0;
@@ -559,7 +561,7 @@ static int launch_wide_t(DecodeParams p, int what, cudaStream_t st) {
     const size_t smemt = (size_t)wide_tail_npad(p.lmax) * 8;
     if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemt))
       return CTKV_ECUDA;
-    kt<<<p.U, kTailT, smemt, st>>>(p);
+    launch_k(kt, dim3(p.U), dim3(kTailT), smemt, st, p);
     if (cudaGetLastError() != cudaSuccess) return CTKV_ECUDA;
   }
   return CTKV_OK;

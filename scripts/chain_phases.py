@@ -28,8 +28,8 @@ st._set_total(s)
 ix = QueryCentroidIndex.build(q[:, :, :C].contiguous(), st, C, 1280)
 eng = DecodeEngine([(st, ix)], P.DecodeConfig(4, 512), lanes=lanes)
 lib = N.lib()
-names = ["start", "topC'", "bitmaps+sync1", "survivors+sync2", "pull ids", "logits+sync3",
-         "pull keys", "threshold", "attention", "sync4", "merge"]
+names = ["start", "q + slots", "lists+bitmaps+sync1", "survivors+sync2", "pull ids", "logits",
+         "sync3", "pull keys", "threshold", "compaction", "attention", "sync4+merge"]
 for t in range(4):
     eng.q[0].copy_(q[:, :, C + t])
     eng.k[0].copy_(k[:, :, s + t])
@@ -50,14 +50,14 @@ for t in range(4):
         a = a[:nct]
         t0 = a[:, 0].min()
         print(f"lanes={lanes}: {nct} CTAs; start spread {(a[:, 0].max() - t0) / 1e3:.2f} us")
-        for kk in range(1, 11):
+        for kk in range(1, 12):
             rows = a[:, kk] > 0
             dd = (a[rows, kk] - a[rows, kk - 1]) / 1e3
             if len(dd):
                 print(f"  {kk:2d} {names[kk]:18s} median {np.median(dd):7.2f} us  max {dd.max():7.2f}")
         r0 = a[0::4]
-        print(f"  end-to-end (rank 0, mark 10 - mark 0): median {np.median(r0[:, 10] - r0[:, 0]) / 1e3:.2f} us")
-        print(f"  kernel span: {(a[:, 10].max() - t0) / 1e3:.2f} us")
+        print(f"  end-to-end (rank 0, mark 11 - mark 0): median {np.median(r0[:, 11] - r0[:, 0]) / 1e3:.2f} us")
+        print(f"  kernel span: {(a[:, 11].max() - t0) / 1e3:.2f} us")
     else:
         eng.step()
     torch.cuda.synchronize()
