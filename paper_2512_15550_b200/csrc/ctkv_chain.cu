@@ -95,7 +95,7 @@ constexpr int kCBins = 1024;     // top-rho' selection: histogram bins
 constexpr int kCBnd = 256;       // ... and keys ranked exactly in the boundary bin
 
 struct ChainSmem {
-  uint32_t* bm;          // [nlo][words] bitmaps of this CTA's lists   } area A; CTA 0
+  uint32_t* bm;          // [words] OR of the lists before an owned one } area A; CTA 0
   int32_t* recl;         // [nlo][rho] this CTA's lists, survivors     } later: static partials
   float* spo;            // CTA 0, after the union: [ns][gs][D] static o
   double* spml;          //                          [2][ns][gs] static (m, l)
@@ -126,7 +126,7 @@ __host__ __device__ inline size_t chain_layout(const DecodeParams& p, int D, int
   const int nlo = chain_nlo(p.c_prime, CL);
   const int scap = chain_scap(p.lmax, CL);
   const int lmax = p.lmax > 1 ? p.lmax : 1;
-  const size_t bm_b = align16((size_t)nlo * p.bitmap_words * 4);
+  const size_t bm_b = align16((size_t)p.bitmap_words * 4);   // one OR-bitmap
   const size_t a_lists = bm_b + align16((size_t)nlo * p.rho * 4);
   const size_t spo_b = align16((size_t)p.ns * p.gs * D * 4);
   const size_t a_static = spo_b + align16((size_t)2 * p.ns * p.gs * 8);
@@ -324,48 +324,48 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
   __syncthreads();
   cmark(1);
 
-  // ---- 2. own lists: load, bitmap, first-occurrence test ----------------------
-  // (compact loops, not unrolled code: this phase runs once per kernel and a
-  // cold instruction cache costs more than the loop overhead)
-  const int nlo = chain_nlo(p.c_prime, CL);
+  // ---- 2. own lists: first-occurrence survivors ---------------------------------
+  // CTA r owns lists j = r, r+CL, ...  An entry of list j survives iff no list
+  // j' < j holds it (np.unique(return_index) order, ck/retrieval.py:156-162),
+  // tested against a local bitmap that ORs lists 0..j-1 (re-read from L2; no
+  // cross-CTA traffic).  Loops stay compact: this phase runs once per kernel.
   const int nown = (p.c_prime - r + CL - 1) / CL;      // lists r, r + CL, ... < c'
   int32_t* raw = reinterpret_cast<int32_t*>(S.keys);   // area B: [nown][rho] raw ids
-  {
-    constexpr int LU = 8;
-    for (int sl = 0; sl < nown; ++sl) {
-      const int32_t* row = p.lists + ((int64_t)u * p.C + sel[r + CL * sl]) * p.rho;
-      int32_t* dst = raw + sl * p.rho;
+  const int per = (p.rho + kCT - 1) / kCT;             // entries per thread per list
+  constexpr int LU = 8;
+  auto list_row = [&](int j) { return p.lists + ((int64_t)u * p.C + sel[j]) * p.rho; };
+  for (int sl = 0; sl < nown; ++sl) {   // own lists -> raw (range-checked)
+    const int32_t* row = list_row(r + CL * sl);
+    int32_t* dst = raw + sl * p.rho;
+    for (int i0 = tid; i0 < p.rho; i0 += kCT * LU) {
+      int v[LU];
+#pragma unroll
+      for (int x = 0; x < LU; ++x) v[x] = i0 + x * kCT < p.rho ? __ldg(row + i0 + x * kCT) : kEmpty;
+#pragma unroll
+      for (int x = 0; x < LU; ++x) {
+        int id = v[x];
+        if (id != kEmpty && (id < 0 || id >= total)) { set_flag(p.flags, kFlagIdRange); id = kEmpty; }
+        if (i0 + x * kCT < p.rho) dst[i0 + x * kCT] = id;
+      }
+    }
+  }
+  for (int i = tid; i < p.bitmap_words; i += kCT) S.bm[i] = 0u;
+  int jdone = 0;                                        // lists already in the bitmap
+  for (int sl = 0; sl < nown; ++sl) {
+    const int j = r + CL * sl;
+    __syncthreads();                                    // bitmap cleared / previous tests done
+    for (; jdone < j; ++jdone) {                        // OR lists jdone .. j-1 into the bitmap
+      const int32_t* row = list_row(jdone);
       for (int i0 = tid; i0 < p.rho; i0 += kCT * LU) {
         int v[LU];
 #pragma unroll
         for (int x = 0; x < LU; ++x) v[x] = i0 + x * kCT < p.rho ? __ldg(row + i0 + x * kCT) : kEmpty;
 #pragma unroll
-        for (int x = 0; x < LU; ++x) {
-          int id = v[x];
-          if (id != kEmpty && (id < 0 || id >= total)) { set_flag(p.flags, kFlagIdRange); id = kEmpty; }
-          if (i0 + x * kCT < p.rho) dst[i0 + x * kCT] = id;
-        }
+        for (int x = 0; x < LU; ++x)
+          if (v[x] >= 0 && v[x] < total) atomicOr(&S.bm[v[x] >> 5], 1u << (v[x] & 31));
       }
     }
-    for (int i = tid; i < nlo * p.bitmap_words; i += kCT) S.bm[i] = 0u;
     __syncthreads();
-    for (int sl = 0; sl < nown; ++sl) {
-      uint32_t* bm = S.bm + sl * p.bitmap_words;
-#pragma unroll 4
-      for (int i = tid; i < p.rho; i += kCT) {
-        const int id = raw[sl * p.rho + i];
-        if (id != kEmpty) atomicOr(&bm[id >> 5], 1u << (id & 31));
-      }
-    }
-  }
-  cl.sync();   // #1: every list's bitmap is complete
-  cmark(2);
-  // survivors, compacted in position order per list (thread t owns entries
-  // [t*per, (t+1)*per)); the earlier lists' bits are read with independent
-  // remote loads
-  const int per = (p.rho + kCT - 1) / kCT;
-  for (int sl = 0; sl < nown; ++sl) {
-    const int j = r + CL * sl;
     const int32_t* rl = raw + sl * p.rho;
     unsigned keepm = 0;
     int cnt = 0;
@@ -373,16 +373,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
     for (int e = 0; e < per; ++e) {
       const int i = tid * per + e;
       const int id = i < p.rho ? rl[i] : kEmpty;
-      uint32_t hit = 0;
-      if (id != kEmpty) {
-        uint32_t w[kCMaxLists - 1];
-#pragma unroll
-        for (int j2 = 0; j2 < kCMaxLists - 1; ++j2)
-          w[j2] = j2 < j ? (cl.map_shared_rank(S.bm, j2 % CL) + (j2 / CL) * p.bitmap_words)[id >> 5] : 0u;
-#pragma unroll
-        for (int j2 = 0; j2 < kCMaxLists - 1; ++j2) hit |= w[j2] >> (id & 31);
-      }
-      const bool keep = id != kEmpty && !(hit & 1u);
+      const bool keep = id != kEmpty && !((S.bm[id >> 5] >> (id & 31)) & 1u);
       keepm |= (keep ? 1u : 0u) << e;
       cnt += keep;
     }
@@ -393,6 +384,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
       if ((keepm >> e) & 1u) S.recl[sl * p.rho + o++] = rl[tid * per + e];
     if (tid < CL) cl.map_shared_rank(lcnt, tid)[j] = tot;
   }
+  cmark(2);
   cl.sync();   // #2: survivor counts everywhere, survivors compacted
   cmark(3);
 

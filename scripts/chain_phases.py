@@ -28,7 +28,7 @@ st._set_total(s)
 ix = QueryCentroidIndex.build(q[:, :, :C].contiguous(), st, C, 1280)
 eng = DecodeEngine([(st, ix)], P.DecodeConfig(4, 512), lanes=lanes)
 lib = N.lib()
-names = ["start", "q + slots", "lists+bitmaps+sync1", "survivors+sync2", "pull ids", "logits",
+names = ["start", "q + slots", "lists+survivors", "sync2", "pull ids", "logits",
          "sync3", "pull keys", "threshold", "compaction", "attention", "sync4+merge"]
 for t in range(4):
     eng.q[0].copy_(q[:, :, C + t])
@@ -55,6 +55,10 @@ for t in range(4):
             dd = (a[rows, kk] - a[rows, kk - 1]) / 1e3
             if len(dd):
                 print(f"  {kk:2d} {names[kk]:18s} median {np.median(dd):7.2f} us  max {dd.max():7.2f}")
+        print("  per rank (median us):", "  ".join(names[kk][:10] for kk in range(1, 12)))
+        for rk in range(4):
+            rr = a[rk::4]
+            print(f"   rank {rk}:", "  ".join(f"{np.median(rr[:, kk] - rr[:, kk - 1]) / 1e3:10.2f}" for kk in range(1, 12)))
         r0 = a[0::4]
         print(f"  end-to-end (rank 0, mark 11 - mark 0): median {np.median(r0[:, 11] - r0[:, 0]) / 1e3:.2f} us")
         print(f"  kernel span: {(a[:, 11].max() - t0) / 1e3:.2f} us")
