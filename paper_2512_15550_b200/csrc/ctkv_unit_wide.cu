@@ -42,6 +42,7 @@ constexpr int kWItems = 32;            // union entries per thread (c' rho <= 81
 constexpr int kWMaxLists = 8;          // c' <= 8
 constexpr int kWMaxGs = 8;             // gs <= 8
 constexpr int kTailT = 512;            // threads per tail CTA
+constexpr int kTailBins = 1024;        // counting-sort bins of the tail ordering
 
 struct WideSmem {
   uint64_t* area;    // union bitmaps [c'-1][words]; finisher: packed keys [lmax]
@@ -103,6 +104,11 @@ __host__ __device__ inline size_t wide_c_layout(const DecodeParams& p, int D, in
   t.scratch = reinterpret_cast<double*>(take(sizeof(double) * nscr));
   if (s) *s = t;
   return off;
+}
+
+__host__ __device__ inline size_t wide_tail_smem(const DecodeParams& p) {
+  const int lmax = p.lmax > 1 ? p.lmax : 1;
+  return (size_t)3 * lmax * 4 + (size_t)2 * kTailBins * 4;
 }
 
 __host__ __device__ inline int wide_tail_npad(int lmax) {
@@ -450,11 +456,17 @@ __device__ void tail_sort(uint64_t* skey) {
 template <typename T, int D>
 __global__ void __launch_bounds__(kTailT) tail_wide_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* skey = reinterpret_cast<uint64_t*>(smem);
   const int u = blockIdx.x;
   const int bi = u / p.g, gi = u % p.g, gs = p.gs;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ int64_t s_slot;
+  __shared__ uint32_t s_mm[2 * (kTailT / 32)];
+  const int lmax = p.lmax > 1 ? p.lmax : 1;
+  uint32_t* k32 = reinterpret_cast<uint32_t*>(smem);   // [lmax] score keys by position
+  int* binned = reinterpret_cast<int*>(k32 + lmax);    // [lmax] positions grouped by bin
+  int* order = binned + lmax;                          // [lmax] position of rank r
+  int* hist = order + lmax;                            // [kTailBins]
+  int* cur = hist + kTailBins;                         // [kTailBins]
   pdl_trigger();
   pdl_wait();
   if (tid == 0) s_slot = p.fifo ? (p.fifo[bi] % p.C) : 0;
@@ -465,20 +477,57 @@ __global__ void __launch_bounds__(kTailT) tail_wide_kernel(DecodeParams p) {
   const int32_t* rec = p.recg + (int64_t)u * p.lmax;
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   if (need_sort) {
-    const int npad = wide_tail_npad(L);
-    for (int i = tid; i < npad; i += kTailT) skey[i] = i < L ? kg[i] : ~0ull;
-    __syncthreads();
-    switch (npad / kTailT) {
-      case 1: tail_sort<1>(skey); break;
-      case 2: tail_sort<2>(skey); break;
-      case 4: tail_sort<4>(skey); break;
-      case 8: tail_sort<8>(skey); break;
-      default: tail_sort<16>(skey); break;
+    // full (score desc, position asc) order by a counting sort over linear
+    // bins of [min, max] of the score keys, then an exact rank inside each
+    // (small) bin -- O(L), no comparison sort
+    uint32_t mn = 0xffffffffu, mx = 0u;
+    for (int i = tid; i < L; i += kTailT) {
+      const uint32_t k = (uint32_t)(__ldcg(kg + i) >> 32);
+      k32[i] = k;
+      mn = min(mn, k);
+      mx = max(mx, k);
     }
-  } else {
+    mn = __reduce_min_sync(0xffffffffu, mn);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if (lane == 0) { s_mm[warp] = mn; s_mm[kTailT / 32 + warp] = mx; }
+    for (int b = tid; b < kTailBins; b += kTailT) hist[b] = 0;
     __syncthreads();
+    mn = 0xffffffffu;
+    mx = 0u;
+    for (int w = 0; w < kTailT / 32; ++w) { mn = min(mn, s_mm[w]); mx = max(mx, s_mm[kTailT / 32 + w]); }
+    const float fscale = (float)kTailBins / ((float)(mx - mn) + 1.0f);
+    auto bin_of = [&](uint32_t k) { return min(kTailBins - 1, (int)((float)(k - mn) * fscale)); };
+    for (int i = tid; i < L; i += kTailT) atomicAdd(&hist[bin_of(k32[i])], 1);
+    __syncthreads();
+    {
+      constexpr int BPT = kTailBins / kTailT;
+      int loc = 0;
+      for (int x = 0; x < BPT; ++x) loc += hist[tid * BPT + x];
+      int tot;
+      int run = block_exclusive_scan(loc, &tot, reinterpret_cast<double*>(s_mm));
+      for (int x = 0; x < BPT; ++x) {
+        cur[tid * BPT + x] = run;
+        run += hist[tid * BPT + x];
+      }
+    }
+    __syncthreads();
+    for (int i = tid; i < L; i += kTailT) binned[atomicAdd(&cur[bin_of(k32[i])], 1)] = i;
+    __syncthreads();
+    for (int i = tid; i < L; i += kTailT) {
+      const uint32_t k = k32[i];
+      const int b = bin_of(k);
+      const int e = cur[b], s0 = e - hist[b];
+      int r = s0;
+      for (int x = s0; x < e; ++x) {
+        const int j = binned[x];
+        const uint32_t kj = k32[j];
+        r += (kj < k) || (kj == k && j < i);
+      }
+      order[r] = i;
+    }
   }
-  auto pos_at = [&](int i) { return (int)(uint32_t)(skey[i] & 0xffffffffu); };
+  __syncthreads();
+  auto pos_at = [&](int i) { return order[i]; };
   if (dcu_here) {
     const int64_t slot = s_slot;
     int32_t* row = p.lists + ((int64_t)u * p.C + slot) * p.rho;
@@ -558,7 +607,7 @@ static int launch_wide_t(DecodeParams p, int what, cudaStream_t st) {
     const bool any = (p.stages & (kStageDcu | kStageAppendTail)) || p.sparse_ids;
     if (!any) return CTKV_OK;
     auto kt = tail_wide_kernel<T, D>;
-    const size_t smemt = (size_t)wide_tail_npad(p.lmax) * 8;
+    const size_t smemt = wide_tail_smem(p);
     if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemt))
       return CTKV_ECUDA;
     launch_k(kt, dim3(p.U), dim3(kTailT), smemt, st, p);
@@ -571,7 +620,7 @@ bool wide_supported(const DecodeParams& p, int dtype, int D) {
   if (dtype != CTKV_BF16 || (D != 64 && D != 128)) return false;
   if (p.gs > kWMaxGs || p.c_prime > kWMaxLists) return false;
   if ((int64_t)p.c_prime * p.rho > (int64_t)kWWarps * 32 * kWItems) return false;
-  if (wide_tail_npad(p.lmax) * 8 > 128 * 1024) return false;
+  if (wide_tail_smem(p) > 200 * 1024) return false;
   if (wide_b_layout(p, 2, nullptr, nullptr) > 200 * 1024) return false;
   return true;
 }
