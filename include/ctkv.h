@@ -235,6 +235,14 @@ int ctkv_debug_phase_timing(int32_t on, uint64_t* host_out, int32_t n);
 /* Profiling only: per-CTA task timeline of the persistent scan kernel
  * ([cta][slot] globaltimer ns: 0 start, 1 end, 2+k task k ready). */
 int ctkv_debug_scan_timeline(int32_t on, uint64_t* host_out, int32_t n);
+/* Profiling only: when on, decode launches record their kernels' spans
+ * (globaltimer min start / max end per kind: scan, chain, tail) in the last
+ * 64 bytes of the workspace reserved for it (read with ctkv_debug_timeline_rw;
+ * see scripts/kernel_timeline.py). */
+int ctkv_debug_kernel_timeline(int32_t on);
+/* Read (8 x u64) and optionally reset a decode workspace's kernel spans. */
+int ctkv_debug_timeline_rw(const ctkv_layout* L, int32_t capacity, int32_t rho, int32_t c_prime,
+                           void* workspace, uint64_t* host_out, int32_t reset);
 
 #ifdef __cplusplus
 }

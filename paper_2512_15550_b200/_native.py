@@ -89,6 +89,8 @@ SIGNATURES = {
     "ctkv_topk_rows": (c_i32, [c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_size, c_vp]),
     "ctkv_debug_phase_timing": (c_i32, [c_i32, c_vp, c_i32]),
     "ctkv_debug_scan_timeline": (c_i32, [c_i32, c_vp, c_i32]),
+    "ctkv_debug_kernel_timeline": (c_i32, [c_i32]),
+    "ctkv_debug_timeline_rw": (c_i32, [ctypes.POINTER(Layout), c_i32, c_i32, c_i32, c_vp, c_vp, c_i32]),
     "ctkv_centroid_norms": (c_i32, [ctypes.POINTER(Layout), c_vp, c_i32, c_vp, c_vp]),
 }
 

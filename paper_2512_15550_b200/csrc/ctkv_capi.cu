@@ -58,6 +58,7 @@ struct DecodeWs {
   float* apo;
   double* apl;
   double* wmax;
+  unsigned long long* tl;
   int32_t* selg;
   int* selctr;
   size_t bytes;
@@ -100,6 +101,7 @@ DecodeWs carve_decode(const ctkv_layout* L, int C, int lmax, int ns, void* base,
   w.apo = reinterpret_cast<float*>(take(sizeof(float) * (size_t)U * 8 * gs * d));
   w.apl = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * 8 * gs));
   w.wmax = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * gs));
+  w.tl = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 8));
   w.selg = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U * std::max(c_prime, 1)));
   w.selctr = reinterpret_cast<int*>(take(sizeof(int) * (size_t)U));
   w.bytes = off;
@@ -275,6 +277,7 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.apo = w.apo;
   p.apl = w.apl;
   p.wmax = w.wmax;
+  p.tl = ctkv::kernel_timeline(-1) ? w.tl : nullptr;
   p.out = A->out;
   p.row_max = A->row_max;
   p.denom = A->denom;
@@ -517,6 +520,21 @@ int ctkv_centroid_norms(const ctkv_layout* L, const void* centroids, int32_t cap
   const int64_t rows = (int64_t)L->batch * L->query_heads * capacity;
   return launch_centroid_norms(L->dtype, L->head_dim, centroids, rows, cnorm,
                                static_cast<cudaStream_t>(stream));
+}
+
+int ctkv_debug_kernel_timeline(int32_t on) { return ctkv::kernel_timeline(on); }
+
+int ctkv_debug_timeline_rw(const ctkv_layout* L, int32_t capacity, int32_t rho, int32_t c_prime,
+                           void* workspace, uint64_t* host_out, int32_t reset) {
+  if (int rc = check_layout(L)) return rc;
+  DecodeWs w = carve_decode(L, capacity, c_prime * rho, static_slots(L), workspace, c_prime);
+  if (host_out && cudaMemcpy(host_out, w.tl, 64, cudaMemcpyDeviceToHost) != cudaSuccess) return CTKV_ECUDA;
+  if (reset) {
+    unsigned long long init[8];
+    for (int k = 0; k < 4; ++k) { init[2 * k] = ~0ull; init[2 * k + 1] = 0ull; }
+    if (cudaMemcpy(w.tl, init, 64, cudaMemcpyHostToDevice) != cudaSuccess) return CTKV_ECUDA;
+  }
+  return CTKV_OK;
 }
 
 int ctkv_debug_scan_timeline(int32_t on, uint64_t* host_out, int32_t n) {

@@ -311,6 +311,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
   __shared__ double hm[GS], hl[GS], hnew[GS], hresc[GS];
 
   cmark(0);
+  ktl_mark(p.tl, 1, false);
   pdl_trigger();   // the next kernel of the stream may launch once we are all resident
   pdl_wait();      // the scan's outputs (gcos / slots, static partials) are complete
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
@@ -633,7 +634,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
   }
   cmark(10);
   cl.sync();   // #4: all sparse partials are in CTA 0
-  if (r != 0) return;
+  if (r != 0) {
+    ktl_mark(p.tl, 1, true);
+    return;
+  }
 
   // ---- 6. CTA 0: exact merge with the static partials ---------------------------------
   cp_async_wait_all();
@@ -700,6 +704,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
   if (p.selected)
     for (int k2 = tid; k2 < p.c_prime; k2 += kCT) p.selected[(int64_t)u * p.c_prime + k2] = sel[k2];
   cmark(11);
+  __syncthreads();
+  ktl_mark(p.tl, 1, true);
 }
 
 // ------------------------------------------------------------------------
@@ -725,7 +731,7 @@ static int launch_chain_t(const DecodeParams& p, cudaStream_t st) {
       return CTKV_ECUDA;
     configured = sm;
   }
-  launch_k(k, dim3(p.U * CL), dim3(kCT), sm, st, p);
+  launch_k(k, dim3(p.U * CL), dim3(kCT), sm, st, kPrioHigh, p);
   return cudaGetLastError() == cudaSuccess ? CTKV_OK : CTKV_ECUDA;
 }
 

@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[kMaxGroup];
   pdl_trigger();   // the chain kernel may launch once every scan CTA is resident
+  ktl_mark(p.tl, 0, false);
   const int64_t t0 = p.total ? *p.total : p.id_bound;
   const bool appending = p.k_new != nullptr;
   const int64_t total = t0 + (appending ? 1 : 0);
@@ -496,6 +497,8 @@ __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
       vals[(uu * p.cap + t0) * D + e] = vn[i];
     }
   }
+  __syncthreads();
+  ktl_mark(p.tl, 0, true);
 }
 
 // ------------------------------------------------------------------------
@@ -2542,7 +2545,7 @@ static int launch_scan_t(const DecodeParams& p, int nblocks, cudaStream_t st) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = sm;
   }
-  if (nblocks > 0) launch_k(k, dim3(nblocks), dim3(kScanRowsV2), sm, st, p);
+  if (nblocks > 0) launch_k(k, dim3(nblocks), dim3(kScanRowsV2), sm, st, kPrioLow, p);
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
 
@@ -2669,6 +2672,26 @@ int scan_variant_v6() {
     v = (e && e[0] == '4') ? 4 : 2;
   }
   return v;
+}
+
+int kernel_timeline(int on) {   // host switch; on < 0 queries
+  static int v = 0;
+  if (on >= 0) v = on;
+  return v;
+}
+
+int launch_priority(LaunchPrio pr) {
+  static int lo = 1, hi = 0, on = -1;
+  if (on < 0) {
+    const char* e = getenv("CTKV_PRIO");
+    on = (e && e[0] == '0') ? 0 : 1;
+    if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) { lo = 0; hi = 0; }
+  }
+  if (!on) return lo;   // default (lowest) priority everywhere
+  // numerically lower = higher priority; hi..lo
+  if (pr == kPrioHigh) return hi;
+  if (pr == kPrioMid) return (lo + hi) / 2;
+  return lo;
 }
 
 bool pdl_enabled() {

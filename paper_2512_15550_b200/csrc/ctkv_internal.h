@@ -71,6 +71,7 @@ struct DecodeParams {
   float* apo;       // [U][8][gs][D] sparse attention partials
   double* apl;      // [U][8][gs]
   double* wmax;     // [U][gs] per-head max of the selected logits
+  unsigned long long* tl;  // [4 kinds][start, end] globaltimer span of this step's kernels (debug)
   int wparts_b, wparts_c;
   // v6 chain: the scan's last cosine CTA of a unit writes its top-C' slots
   int32_t* selg;    // [U][c'] top-C' slots (ties -> smaller slot)
@@ -105,6 +106,7 @@ int static_tok_for(int dtype);
 int phase_timing(int on, unsigned long long* out, int n);
 int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int decode_variant();
+int kernel_timeline(int on);
 int scan_variant_v6();
 bool wide_supported(const DecodeParams& p, int dtype, int D);
 // what: 1 = recall + attend kernels, 2 = tail (DCU, sparse ids, cursor/total)
@@ -130,19 +132,31 @@ int launch_append(int dtype, void* keys, void* vals, const void* kn, const void*
 // stream predecessor finishes; it calls pdl_wait() (griddepcontrol.wait)
 // before touching anything the predecessor produced.  CTKV_PDL=1 enables.
 bool pdl_enabled();
+// Launch priorities (CTA dispatch order when several kernels wait for SMs):
+// the latency-critical chain kernels go first, the bandwidth-bound scans
+// last.  CTKV_PRIO=0 disables.
+enum LaunchPrio { kPrioLow = 0, kPrioMid = 1, kPrioHigh = 2 };
+int launch_priority(LaunchPrio pr);
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                           cudaStream_t st, Args&&... args) {
+                           cudaStream_t st, LaunchPrio pr, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributePriority;
+  attr[n].val.priority = launch_priority(pr);
+  ++n;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = n;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -469,6 +469,7 @@ __global__ void __launch_bounds__(kTailT) tail_wide_kernel(DecodeParams p) {
   int* cur = hist + kTailBins;                         // [kTailBins]
   pdl_trigger();
   pdl_wait();
+  ktl_mark(p.tl, 2, false);
   if (tid == 0) s_slot = p.fifo ? (p.fifo[bi] % p.C) : 0;
   const int L = p.uctr[u * 4 + 2], Rn = p.uctr[u * 4 + 3];
   const bool dcu_here = (p.stages & kStageDcu) && L > 0;
@@ -565,6 +566,8 @@ __global__ void __launch_bounds__(kTailT) tail_wide_kernel(DecodeParams p) {
       }
     }
   }
+  __syncthreads();
+  ktl_mark(p.tl, 2, true);
 }
 
 // ------------------------------------------------------------------------
@@ -610,7 +613,7 @@ static int launch_wide_t(DecodeParams p, int what, cudaStream_t st) {
     const size_t smemt = wide_tail_smem(p);
     if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smemt))
       return CTKV_ECUDA;
-    launch_k(kt, dim3(p.U), dim3(kTailT), smemt, st, p);
+    launch_k(kt, dim3(p.U), dim3(kTailT), smemt, st, kPrioMid, p);
     if (cudaGetLastError() != cudaSuccess) return CTKV_ECUDA;
   }
   return CTKV_OK;

@@ -1,0 +1,95 @@
+"""Steady-state timeline of one CUDA-graph decode step (cfg2, lanes): per
+(lane, layer) the [start, end] span of the scan, chain and tail kernels
+(globaltimer, recorded by the kernels when the debug timeline is on)."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2512_15550_b200 as P  # noqa: E402
+from paper_2512_15550_b200 import _native as N  # noqa: E402
+from paper_2512_15550_b200.engine import DecodeEngine  # noqa: E402
+from paper_2512_15550_b200.index import QueryCentroidIndex  # noqa: E402
+from paper_2512_15550_b200.store import KvStore  # noqa: E402
+
+NL = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+lanes = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+b, h, g, d, s, C, T = 8, 32, 8, 128, 98304, 2048, 16
+built, tails = [], []
+for li in range(NL):
+    lay = P.HeadLayout(b, h, g, s + T, d)
+    q, k, v, _ = P.generate(P.DriftConfig(seed=42 + li, s=s, decode_steps=T), lay, dtype=torch.bfloat16,
+                            q_rows=(s - C, s + T))
+    st = KvStore(P.HeadLayout(b, h, g, s, d), 128, 1024, dtype=torch.bfloat16, capacity=s + T,
+                 host_api=False)
+    st.keys[:, :, :s].copy_(k[:, :, :s])
+    st.values[:, :, :s].copy_(v[:, :, :s])
+    st._set_total(s)
+    built.append((st, QueryCentroidIndex.build(q[:, :, :C].contiguous(), st, C, 1280)))
+    tails.append((q[:, :, C:].contiguous(), k[:, :, s:].contiguous(), v[:, :, s:].contiguous()))
+    del q, k, v
+lib = N.lib()
+lib.ctkv_debug_kernel_timeline(1)
+eng = DecodeEngine(built, P.DecodeConfig(4, 512), lanes=lanes)
+
+
+def load(t):
+    for li in range(NL):
+        eng.q[li].copy_(tails[li][0][:, :, t])
+        eng.k[li].copy_(tails[li][1][:, :, t])
+        eng.v[li].copy_(tails[li][2][:, :, t])
+
+
+buf = (ctypes.c_uint64 * 8)()
+for t in range(6):
+    load(t)
+    if t == 2:
+        eng.capture()
+    if t >= 4:
+        torch.cuda.synchronize()
+        for L in eng.layers:
+            lay, sd, idd, args, ws, wsn = L.call
+            lib.ctkv_debug_timeline_rw(lay, L.index.capacity, L.index.rho, 4, ws, None, 1)
+        torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    eng.replay() if t >= 3 else eng.step()
+    e1.record()
+    torch.cuda.synchronize()
+    if t == 5:
+        rows = []
+        for k_ in range(lanes):
+            for li in range(NL):
+                L = eng.lane_layers[k_][li]
+                lay, sd, idd, args, ws, wsn = L.call
+                lib.ctkv_debug_timeline_rw(lay, L.index.capacity, L.index.rho, 4, ws, buf, 0)
+                rows.append((k_, li, list(buf)))
+        t0 = min(r[2][0] for r in rows)
+        print(f"step {e0.elapsed_time(e1) * 1e3:.0f} us (events), {NL} layers x {lanes} lanes")
+        span = {0: [], 1: [], 2: []}
+        for k_, li, v in rows:
+            for kind in range(3):
+                span[kind].append((v[2 * kind + 1] - v[2 * kind]) / 1e3)
+        for kind, nm in enumerate(["scan", "chain", "tail"]):
+            a = np.array(span[kind])
+            print(f"  {nm:6s} span per launch: median {np.median(a):6.1f}  p90 {np.percentile(a, 90):6.1f} us")
+        for k_ in (0, lanes - 1):
+            line = []
+            for li in range(NL):
+                v = rows[k_ * NL + li][2]
+                line.append(f"L{li}: s[{(v[0]-t0)/1e3:.0f},{(v[1]-t0)/1e3:.0f}] c[{(v[2]-t0)/1e3:.0f},{(v[3]-t0)/1e3:.0f}] t[{(v[4]-t0)/1e3:.0f},{(v[5]-t0)/1e3:.0f}]")
+            print(f"  lane {k_}: " + "  ".join(line))
+        # gaps on a lane's critical path: chain(l) end -> scan(l+1) start, scan end -> chain start
+        g1, g2 = [], []
+        for k_ in range(lanes):
+            for li in range(NL):
+                v = rows[k_ * NL + li][2]
+                g1.append((v[2] - v[1]) / 1e3)
+                if li + 1 < NL:
+                    w = rows[k_ * NL + li + 1][2]
+                    g2.append((w[0] - v[3]) / 1e3)
+        print(f"  gap scan->chain median {np.median(g1):.1f} us; chain->next scan median {np.median(g2):.1f} us")
+lib.ctkv_debug_kernel_timeline(0)
