@@ -69,9 +69,13 @@ def ncu_traffic(kernel: str):
     (profiles/ncu_traffic.json, written by scripts/ncu_traffic.py), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            return json.load(fh)[kernel]["dram_bytes_per_launch"]
+            db = json.load(fh)
+        for key in (kernel, kernel.split("::")[-1]):
+            if key in db:
+                return db[key]["dram_bytes_per_launch"]
     except Exception:
-        return None
+        pass
+    return None
 
 
 def peaks():
@@ -243,7 +247,7 @@ def main():
     plan = ShardPlan(world, rank, B, a.kv_heads, a.query_heads)
     b, g, h, d = plan.b_loc, plan.g_loc, plan.h_loc, a.head_dim
     s = a.seq
-    T = a.warmup + a.steps + a.e2e_steps + 8 + a.cpu_steps + 2
+    T = a.warmup + a.steps + a.e2e_steps + 12 + a.cpu_steps + 2
     layout = P.HeadLayout(b, h, g, s + T, d)
     cfg = P.DecodeConfig(a.c_prime, a.rho_prime)
 
@@ -272,7 +276,6 @@ def main():
         build_ms.append(ev0.elapsed_time(ev1))
         layers.append((store, index))
         del q
-    engine = DecodeEngine(layers, cfg, plan=plan, group=group, lanes=a.lanes)
     nl = a.layers
     # all step inputs, device resident: [T, L, b, heads, d]
     Qall = torch.stack([t[0].permute(2, 0, 1, 3) for t in tails], dim=1).contiguous()
@@ -281,16 +284,36 @@ def main():
     del tails
     step_i = [0]
 
-    def load_inputs():
+    def load_inputs(eng):
         t = step_i[0]
-        engine.q.copy_(Qall[t])
-        engine.k.copy_(Kall[t])
-        engine.v.copy_(Vall[t])
+        eng.q.copy_(Qall[t])
+        eng.k.copy_(Kall[t])
+        eng.v.copy_(Vall[t])
         step_i[0] += 1
 
+    # ---- per-kernel timing at full-layer size (one launch per kernel covers
+    # all b*g units of a layer), eager, CUDA events on the launching stream;
+    # run before the lanes engine, which then continues from this state ----
+    nmeas = 3
+    tengine = DecodeEngine(layers, cfg, plan=plan, group=group, lanes=1)
+    load_inputs(tengine)
+    tengine.step()
+    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(nl)]
+           for _ in range(nmeas)]
+    rl_tot = 0
+    for m in range(nmeas):
+        load_inputs(tengine)
+        tengine.step(events=evs[m])
+        torch.cuda.synchronize()
+        rl_tot += sum(int(L.bufs.recall_len.sum()) for L in tengine.layers)
+    tengine.check()
+    scan_ms = statistics.mean(e[0].elapsed_time(e[1]) for run_ in evs for e in run_)
+    unit_ms = statistics.mean(e[1].elapsed_time(e[2]) for run_ in evs for e in run_)
+    del tengine
+    engine = DecodeEngine(layers, cfg, plan=plan, group=group, lanes=a.lanes)
     # ---- warm-up (eager), capture, more warm-up ----
     for _ in range(max(1, a.warmup // 2)):
-        load_inputs()
+        load_inputs(engine)
         engine.step()
     torch.cuda.synchronize()
     engine.check()
@@ -299,7 +322,7 @@ def main():
         engine.capture()
     run = engine.replay if use_graph else engine.step
     for _ in range(a.warmup - max(1, a.warmup // 2)):
-        load_inputs()
+        load_inputs(engine)
         run()
     torch.cuda.synchronize()
 
@@ -312,7 +335,7 @@ def main():
     with ClockSampler(local) as clk:
         start.record()
         for _ in range(a.steps):
-            load_inputs()
+            load_inputs(engine)
             run()
         stop.record()
         torch.cuda.synchronize()
@@ -327,37 +350,28 @@ def main():
     ms_step = ms_total / a.steps
     tok_s = B * a.steps / (ms_total / 1e3)
 
-    # ---- per-kernel timing (events on the launching stream, eager) ----
-    nmeas = 3
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(nl * a.lanes)]
-           for _ in range(nmeas)]
-    rl_tot = 0
-    for m in range(nmeas):
-        load_inputs()
-        engine.step(events=evs[m])
-        torch.cuda.synchronize()
-        rl_tot += sum(int(L.bufs.recall_len.sum()) for L in engine.layers)
-    scan_ms = statistics.mean(e[0].elapsed_time(e[1]) for run_ in evs for e in run_)
-    unit_ms = statistics.mean(e[1].elapsed_time(e[2]) for run_ in evs for e in run_)
     Lbar = rl_tot / (nmeas * nl * b * g)      # mean recall length per (b, g) unit
     e = 2
     gs = h // g
-    U = b * g // a.lanes                       # units per kernel launch (one lane)
+    U = b * g                                  # units per kernel launch (timing pass: full layer)
     n_static = a.init_len + a.local_len
     C = a.capacity
-    scan_bytes = U * (gs * C * d * e + 2 * n_static * d * e + gs * d * e + 2 * d * e) \
-        + U * C * 8 + U * math.ceil(n_static / 64) * gs * (d * 4 + 16)
-    unit_bytes = U * (C * 8 + 4 * a.c_prime * a.rho + e * d * Lbar + e * d * a.rho_prime
-                      + 8 * gs * Lbar * 2 + e * gs * d + 4 * a.rho + 4 * gs * d
-                      + math.ceil(n_static / 64) * gs * (d * 4 + 16))
+    # algorithmic bytes per launch (full-layer launch: U = b*g units)
+    ns = math.ceil(n_static / 128)                # static splits (bf16: 128 tokens)
+    scan_bytes = U * (gs * C * d * e + gs * C * 4          # centroid rows + cached norms
+                      + 2 * n_static * d * e               # static K, V
+                      + gs * d * e + 2 * d * e             # query heads, appended K/V
+                      + C * 8 + ns * gs * (d * 4 + 16))    # group-max cosines, static partials
+    unit_bytes = U * (C * 8 + 4 * a.c_prime * a.rho                # cosines, selected lists
+                      + e * d * Lbar + e * d * a.rho_prime          # K rows (rerank), V rows
+                      + 16 * gs * Lbar + 12 * Lbar                  # logits w+r, keys, ids
+                      + ns * gs * (d * 4 + 16) + 4 * gs * d)        # static partials, output
+    # step total: SURVEY.md section 8(d)
     algo_bytes = b * g * (h // g * C * d * e + 4 * a.c_prime * a.rho + e * d * Lbar
-                      + e * d * a.rho_prime + 2 * e * d * n_static + e * gs * d + 4 * gs * d
-                      + e * gs * d + 4 * a.rho + 2 * e * d) * nl
+                          + e * d * a.rho_prime + 2 * e * d * n_static + e * gs * d + 4 * gs * d
+                          + e * gs * d + 4 * a.rho + 2 * e * d) * nl
     scan_gbs = scan_bytes / (scan_ms * 1e-3) / 1e9
     unit_gbs = unit_bytes / (unit_ms * 1e-3) / 1e9 if unit_ms > 1e-4 else 0.0
-    # one persistent layer kernel per layer (v4) vs scan + unit kernels (v2)
-    fused = unit_ms < 2e-3
-    layer_bytes = algo_bytes / nl
 
     # ---- e2e through host buffers (pinned H2D of q/k/v, D2H of outputs) ----
     hq = Qall[:a.e2e_steps + 1].cpu().pin_memory()
@@ -423,24 +437,17 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic drift workload (GPU generator: spectral decay, drift, RoPE, needles)",
             "config": _config(a, world),
-            "roofline": ({"bound": "hbm", "kernel": "layer_kernel (whole decode layer: scan, "
-                                                    "retrieve, attend, DCU)",
-                          "achieved": layer_bytes / (scan_ms * 1e-3) / 1e9, "peak": hbm,
-                          "peak_kind": peak_kind, "unit": "GB/s",
-                          "frac": layer_bytes / (scan_ms * 1e-3) / 1e9 / hbm,
-                          "traffic": ncu_traffic("ctkv::layer_kernel"),
-                          "bytes_per_launch": layer_bytes, "ms_per_launch": scan_ms}
-                         if fused else
-                         {"bound": "hbm", "kernel": "scan_kernel (centroid cosine + static attention)",
-                          "achieved": scan_gbs, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                          "frac": scan_gbs / hbm, "traffic": ncu_traffic("ctkv::scan2_kernel"),
-                          "bytes_per_launch": scan_bytes, "ms_per_launch": scan_ms}),
+            "roofline": {"bound": "hbm",
+                         "kernel": "scan2_kernel (centroid cosines + static attention), "
+                                   "full-layer launch",
+                         "achieved": scan_gbs, "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": scan_gbs / hbm, "traffic": ncu_traffic("ctkv::scan2_kernel"),
+                         "bytes_per_launch": scan_bytes, "ms_per_launch": scan_ms},
             "kernels": {
-                ("layer_kernel" if fused else "scan_kernel"):
-                    {"ms": scan_ms, "bytes": layer_bytes if fused else scan_bytes,
-                     "gbs": (layer_bytes if fused else scan_bytes) / (scan_ms * 1e-3) / 1e9},
-                "unit_kernel": {"ms": unit_ms, "bytes": 0 if fused else unit_bytes, "gbs": unit_gbs,
-                                "mean_recall_len": Lbar, "alpha": Lbar / (a.c_prime * a.rho)},
+                "scan_kernel": {"ms": scan_ms, "bytes": scan_bytes, "gbs": scan_gbs},
+                "unit_kernel": {"name": "chain_kernel", "ms": unit_ms, "bytes": unit_bytes,
+                                "gbs": unit_gbs, "mean_recall_len": Lbar,
+                                "alpha": Lbar / (a.c_prime * a.rho)},
                 "step": {"algorithmic_bytes": algo_bytes,
                          "gbs": algo_bytes / (ms_step * 1e-3) / 1e9,
                          "frac": algo_bytes / (ms_step * 1e-3) / 1e9 / hbm},
@@ -451,7 +458,7 @@ def main():
             "e2e": {"value": e2e_tok_s, "unit": "tok/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             # per (lane, layer): scan + chain + deferred tail kernels
-            "gpu_launches": (1 if fused else 3) * nl * a.lanes * a.steps,
+            "gpu_launches": 3 * nl * a.lanes * a.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "graph": use_graph,

@@ -543,6 +543,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
       for (int hh = 0; hh < GS; ++hh) lgs[hh * kCB + i] = __ldcg(lgg + (int64_t)hh * p.lmax + pos);
     }
     __syncthreads();
+    // the first round of V rows is in flight while the weights are computed
+    uint4 rawv[kVUn];
+    const int t00 = warp * VR;
+#pragma unroll
+    for (int x = 0; x < kVUn; ++x) {
+      const int t = t00 + x * kCW * VR + vrw;
+      rawv[x] = t < n ? ldg16(reinterpret_cast<const uint4*>(vals_g + (int64_t)S.vid[t] * D) + vsub)
+                      : make_uint4(0, 0, 0, 0);
+    }
     // running max per head (warp hh), then one exp per (head, token)
     for (int hh = warp; hh < GS; hh += kCW) {
       double m = -INFINITY;
@@ -580,20 +589,21 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[hh][e] *= resc[hh];
     // weighted V rows: VL lanes per row, kVUn passes in flight
-    for (int t0 = warp * VR; t0 < n; t0 += kCW * VR * kVUn) {
-      uint4 raw[kVUn];
+    for (int t0 = t00; t0 < n; t0 += kCW * VR * kVUn) {
+      if (t0 != t00) {
 #pragma unroll
-      for (int x = 0; x < kVUn; ++x) {
-        const int t = t0 + x * kCW * VR + vrw;
-        raw[x] = t < n ? ldg16(reinterpret_cast<const uint4*>(vals_g + (int64_t)S.vid[t] * D) + vsub)
-                       : make_uint4(0, 0, 0, 0);
+        for (int x = 0; x < kVUn; ++x) {
+          const int t = t0 + x * kCW * VR + vrw;
+          rawv[x] = t < n ? ldg16(reinterpret_cast<const uint4*>(vals_g + (int64_t)S.vid[t] * D) + vsub)
+                          : make_uint4(0, 0, 0, 0);
+        }
       }
 #pragma unroll
       for (int x = 0; x < kVUn; ++x) {
         const int t = t0 + x * kCW * VR + vrw;
         if (t >= n) continue;
         float f[8];
-        unpack16<T>(raw[x], f);
+        unpack16<T>(rawv[x], f);
 #pragma unroll
         for (int hh = 0; hh < GS; ++hh)
           if (hh < gs) {

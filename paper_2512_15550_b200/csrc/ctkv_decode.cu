@@ -268,11 +268,18 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
                  (uint32_t)(nc * 4), &bars[j]);
     }
   }
-  // the rows are in flight; the query may come from the previous kernel
+  // the rows are in flight; the query may come from the previous kernel and
+  // rides its own bulk copy
   pdl_wait();
-  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = q[i];
+  uint64_t* barq = &bars[kMaxGroup - 1];
+  if (threadIdx.x == 0) {
+    bar_init(barq, 1);
+    bar_expect(barq, (uint32_t)(gs * D * sizeof(T)));
+    bulk_g2s(qs, static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D,
+             (uint32_t)(gs * D * sizeof(T)), barq);
+  }
   __syncthreads();
+  bar_wait(barq, 0);
   query_norms<T, D>(qs, gs, qn, threadIdx.x >> 5, blockDim.x >> 5);
   __syncthreads();
   for (int r = threadIdx.x; r < gs * CC; r += blockDim.x) {
@@ -1752,11 +1759,18 @@ __device__ void l_cos(const DecodeParams& p, int task, unsigned char* smem, uint
                (uint32_t)(nc * RB), &bars[j]);
     }
   }
-  // the rows are in flight; the query may come from the previous kernel
+  // the rows are in flight; the query may come from the previous kernel and
+  // rides its own bulk copy
   pdl_wait();
-  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int i = threadIdx.x; i < gs * D; i += blockDim.x) qs[i] = q[i];
+  uint64_t* barq = &bars[kMaxGroup - 1];
+  if (threadIdx.x == 0) {
+    bar_init(barq, 1);
+    bar_expect(barq, (uint32_t)(gs * D * sizeof(T)));
+    bulk_g2s(qs, static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D,
+             (uint32_t)(gs * D * sizeof(T)), barq);
+  }
   __syncthreads();
+  bar_wait(barq, 0);
   query_norms<T, D>(qs, gs, qn, threadIdx.x >> 5, blockDim.x >> 5);
   __syncthreads();
   for (int r = threadIdx.x; r < gs * CC; r += blockDim.x) {
