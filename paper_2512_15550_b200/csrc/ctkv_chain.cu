@@ -89,8 +89,8 @@ constexpr int kCW = kCT / 32;
 constexpr int kCB = 128;         // selected rows per attention batch
 constexpr int kCMaxLists = 8;    // c' <= 8
 constexpr int kCMaxPer = 32;     // list entries per thread (keep mask bits)
-constexpr int kKUn = 4;          // K-row passes in flight per warp (4 rows each)
-constexpr int kVUn = 4;          // V-row passes in flight per warp (2 rows each)
+constexpr int kKUn = 8;          // K-row passes in flight per warp (4 rows each)
+constexpr int kVUn = 8;          // V-row passes in flight per warp (2 rows each)
 constexpr int kCBins = 1024;     // top-rho' selection: histogram bins
 constexpr int kCBnd = 256;       // ... and keys ranked exactly in the boundary bin
 
@@ -289,7 +289,7 @@ __device__ void chain_select(const uint32_t* key, int L, int R, int* hist, uint6
 }
 
 template <typename T, int D, int CL, int GS>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, GS >= 8 ? 2 : 3) chain_kernel(DecodeParams p) {
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   cg::cluster_group cl = cg::this_cluster();
   const int r = (int)cl.block_rank();
