@@ -396,47 +396,87 @@ __global__ void __launch_bounds__(256) kth_value_kernel(const float* __restrict_
   if (threadIdx.x == 0) thr[blockIdx.x] = okey32_inv(prefix);
 }
 
-template <int IPT>
-__device__ void select_sort(const uint64_t* src, int cnt, uint64_t* cs) {
-  uint64_t k[IPT];
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int e = threadIdx.x * IPT + i;
-    k[i] = e < cnt ? src[e] : ~0ull;
-  }
-  bitonic_regs<IPT>(k, cs);
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) cs[threadIdx.x * IPT + i] = k[i];
-  __syncthreads();
-}
-
-// per row: exact top-rho of the candidates (sorted), or flag for fallback
-__global__ void __launch_bounds__(512) select_kernel(const uint64_t* __restrict__ cand,
-                                                     const int32_t* __restrict__ counts, int cap,
-                                                     int rho, int C, int32_t* __restrict__ lists,
-                                                     int32_t add, int32_t* fail_n,
-                                                     int32_t* fail_rows) {
-  extern __shared__ uint64_t cs[];
+// per row: exact top-rho of the candidates in (score desc, key asc) order, or
+// flag the row for the fallback.  O(n) counting sort instead of a comparison
+// sort: linear bins over [min, max] of the candidates' score keys, bin
+// offsets by a block scan, then each candidate's exact rank inside its
+// (small) bin; ranks < rho are written straight to the list.
+constexpr int kSelT = 256, kSelBins = 2048;
+__global__ void __launch_bounds__(kSelT) select_kernel(const uint64_t* __restrict__ cand,
+                                                       const int32_t* __restrict__ counts, int cap,
+                                                       int rho, int C, int32_t* __restrict__ lists,
+                                                       int32_t add, int32_t* fail_n,
+                                                       int32_t* fail_rows) {
+  extern __shared__ uint64_t ck[];                            // [cap] candidates
+  int* binned = reinterpret_cast<int*>(ck + cap);             // [cap] indices grouped by bin
+  __shared__ int hist[kSelBins], cur[kSelBins];
+  __shared__ uint32_t s_mm[2 * kSelT / 32];
+  __shared__ int s_ws[kSelT / 32 + 1];
   const int64_t row = blockIdx.x;
   const int cnt = counts[row];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (cnt < rho || cnt > cap) {
-    if (threadIdx.x == 0) fail_rows[atomicAdd(fail_n, 1)] = (int32_t)row;
+    if (tid == 0) fail_rows[atomicAdd(fail_n, 1)] = (int32_t)row;
     return;
   }
-  int np = next_pow2(max(cnt, 1));
-  if (np < 512) np = 512;
   const uint64_t* src = cand + row * cap;
-  // register/shuffle bitonic: strides inside a warp never touch shared memory
-  switch (np) {
-    case 512: select_sort<1>(src, cnt, cs); break;
-    case 1024: select_sort<2>(src, cnt, cs); break;
-    case 2048: select_sort<4>(src, cnt, cs); break;
-    case 4096: select_sort<8>(src, cnt, cs); break;
-    default: select_sort<16>(src, cnt, cs); break;
+  uint32_t mn = 0xffffffffu, mx = 0u;
+  for (int i = tid; i < cnt; i += kSelT) {
+    const uint64_t k = __ldg(src + i);
+    ck[i] = k;
+    mn = min(mn, (uint32_t)(k >> 32));
+    mx = max(mx, (uint32_t)(k >> 32));
   }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) { s_mm[warp] = mn; s_mm[kSelT / 32 + warp] = mx; }
+  for (int b = tid; b < kSelBins; b += kSelT) hist[b] = 0;
+  __syncthreads();
+  mn = 0xffffffffu;
+  mx = 0u;
+  for (int w = 0; w < kSelT / 32; ++w) { mn = min(mn, s_mm[w]); mx = max(mx, s_mm[kSelT / 32 + w]); }
+  const float fscale = (float)kSelBins / ((float)(mx - mn) + 1.0f);
+  auto bin_of = [&](uint64_t k) {
+    return min(kSelBins - 1, (int)((float)((uint32_t)(k >> 32) - mn) * fscale));
+  };
+  for (int i = tid; i < cnt; i += kSelT) atomicAdd(&hist[bin_of(ck[i])], 1);
+  __syncthreads();
+  // exclusive scan of the bins: thread t owns bins [8t, 8t+8)
+  {
+    constexpr int BPT = kSelBins / kSelT;
+    int loc = 0;
+#pragma unroll
+    for (int x = 0; x < BPT; ++x) loc += hist[tid * BPT + x];
+    int incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_ws[warp] = incl;
+    __syncthreads();
+    int wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += s_ws[w];
+    int run = wpre + incl - loc;
+#pragma unroll
+    for (int x = 0; x < BPT; ++x) {
+      cur[tid * BPT + x] = run;
+      run += hist[tid * BPT + x];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < cnt; i += kSelT) binned[atomicAdd(&cur[bin_of(ck[i])], 1)] = i;
+  __syncthreads();
   int32_t* dst = lists + row * rho;
-  for (int i = threadIdx.x; i < rho; i += blockDim.x) dst[i] = (int32_t)(cs[i] & 0xffffffffu) + add;
+  for (int i = tid; i < cnt; i += kSelT) {
+    const uint64_t k = ck[i];
+    const int b = bin_of(k);
+    const int e = cur[b], s0 = e - hist[b];
+    if (s0 >= rho) continue;                    // the whole bin ranks below the list
+    int r = s0;
+    for (int x = s0; x < e; ++x) r += ck[binned[x]] < k;
+    if (r < rho) dst[r] = (int32_t)(k & 0xffffffffu) + add;
+  }
 }
 
 // full-row scores for fallback rows: one CTA per (row, 256-key block)
@@ -548,7 +588,11 @@ static Plan make_plan(const BuildParams& p) {
   pl.ks = (int)std::ceil(mean + 6.0 * std::sqrt(mean)) + 1;
   if (pl.ks > pl.ns) pl.ks = (int)pl.ns;
   const int64_t expect = (int64_t)pl.ks * pl.S;
-  pl.cap = next_pow2((int)std::min<int64_t>(std::max<int64_t>(2 * expect, p.rho + 1024), 1 << 14));
+  // candidates above the sample threshold: ~expect +- S*sqrt(ks); 8 sigma of
+  // headroom (rows beyond it take the exact fallback)
+  const int64_t head = (int64_t)std::ceil(8.0 * pl.S * std::sqrt((double)pl.ks));
+  pl.cap = (int)std::min<int64_t>(((std::max<int64_t>(expect + head, p.rho + 1024) + 255) / 256) * 256,
+                                  1 << 14);
   pl.CB = kBN / p.gs;
   return pl;
 }
@@ -647,9 +691,9 @@ int build_tc(const BuildParams& p, int /*dtype*/, void* ws, size_t ws_bytes, cud
   if (int rc = launch_gemm(mapK, mapC, gp, katoms, st)) return rc;
   // 4. select
   cudaMemsetAsync(fail_n, 0, sizeof(int32_t), st);
-  const size_t sel_smem = (size_t)std::max(pl.cap, 512) * 8;
+  const size_t sel_smem = (size_t)pl.cap * 12;
   cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
-  select_kernel<<<(unsigned)(U * p.C), 512, sel_smem, st>>>(cand, counts, pl.cap, p.rho, p.C,
+  select_kernel<<<(unsigned)(U * p.C), kSelT, sel_smem, st>>>(cand, counts, pl.cap, p.rho, p.C,
                                                             p.lists, (int32_t)p.off_begin, fail_n,
                                                             fail_rows);
   // 5. exact fallback for rows outside [rho, cap] (host reads the count once)
