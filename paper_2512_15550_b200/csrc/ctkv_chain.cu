@@ -312,7 +312,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
 
   cmark(0);
   ktl_mark(p.tl, 1, false);
-  pdl_trigger();   // the next kernel of the stream may launch once we are all resident
   pdl_wait();      // the scan's outputs (gcos / slots, static partials) are complete
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = tid; i < gs * D; i += kCT) qs[i] = q[i];
@@ -515,6 +514,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     }
   }
   __syncthreads();   // keys dead from here: area B becomes the per-warp V sums
+  // the stream's next kernel (the next layer's scan) may start launching now:
+  // its CTAs stage their centroid rows while this chain attends and merges
+  pdl_trigger();
   const int nmy = rhi - rlo;
   cmark(9);
 
