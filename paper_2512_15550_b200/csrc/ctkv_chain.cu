@@ -312,6 +312,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
 
   cmark(0);
   ktl_mark(p.tl, 1, false);
+  ktl_mark(p.tl, 3, true);   // the last CTA start (slot 3 end = max start)
   pdl_wait();      // the scan's outputs (gcos / slots, static partials) are complete
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = tid; i < gs * D; i += kCT) qs[i] = q[i];
@@ -724,11 +725,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
 // launcher
 // ------------------------------------------------------------------------
 
-static int chain_cl() {   // CTKV_CHAIN_CL=8 selects 8-CTA clusters (A/B)
+static int chain_cl() {   // CTKV_CHAIN_CL=2|8 selects 2- or 8-CTA clusters (A/B)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("CTKV_CHAIN_CL");
-    v = (e && e[0] == '8') ? 8 : 4;
+    v = (e && e[0] == '8') ? 8 : (e && e[0] == '2') ? 2 : 4;
   }
   return v;
 }
@@ -778,7 +779,11 @@ static int launch_chain_g(const DecodeParams& p, cudaStream_t st) {
 
 template <int D>
 static int launch_chain_d(const DecodeParams& p, cudaStream_t st) {
-  return chain_cl() == 8 ? launch_chain_g<D, 8>(p, st) : launch_chain_g<D, 4>(p, st);
+  switch (chain_cl()) {
+    case 2: return launch_chain_g<D, 2>(p, st);
+    case 8: return launch_chain_g<D, 8>(p, st);
+    default: return launch_chain_g<D, 4>(p, st);
+  }
 }
 
 int launch_chain(const DecodeParams& p, int dtype, int D, cudaStream_t st) {

@@ -54,6 +54,8 @@ for t in range(6):
             lay, sd, idd, args, ws, wsn = L.call
             lib.ctkv_debug_timeline_rw(lay, L.index.capacity, L.index.rho, 4, ws, None, 1)
         torch.cuda.synchronize()
+    if t == 5:
+        lib.ctkv_debug_phase_timing(1, None, 0)   # chain phase marks under load
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     eng.replay() if t >= 3 else eng.step()
@@ -92,4 +94,19 @@ for t in range(6):
                     w = rows[k_ * NL + li + 1][2]
                     g2.append((w[0] - v[3]) / 1e3)
         print(f"  gap scan->chain median {np.median(g1):.1f} us; chain->next scan median {np.median(g2):.1f} us")
+        sk = [(r[2][7] - r[2][2]) / 1e3 for r in rows]
+        print(f"  chain CTA start skew (last start - first start): median {np.median(sk):.1f} us, p90 {np.percentile(sk, 90):.1f}")
+n = 512 * 12
+pb = (ctypes.c_uint64 * n)()
+lib.ctkv_debug_phase_timing(0, pb, n)
+a = np.frombuffer(pb, dtype=np.uint64).reshape(512, 12).astype(np.int64)[:eng.bl * g * 4]
+names = ["start", "q + slots", "lists+survivors", "sync2", "pull ids", "logits", "sync3",
+         "pull keys", "threshold", "compaction", "attention", "sync4+merge"]
+print("  chain phases under load (last writer per CTA slot), median us:")
+for kk in range(1, 12):
+    rows = a[:, kk] > 0
+    dd = (a[rows, kk] - a[rows, kk - 1]) / 1e3
+    if kk == 11:
+        dd = (a[0::4, 11] - a[0::4, 10]) / 1e3
+    print(f"    {names[kk]:18s} {np.median(dd):7.2f}")
 lib.ctkv_debug_kernel_timeline(0)
