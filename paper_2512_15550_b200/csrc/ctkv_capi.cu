@@ -49,15 +49,9 @@ struct DecodeWs {
   double* logits;
   double* cval;
   int32_t* cidx;
-  int* ctr;
   int32_t* recg;
-  int32_t* Lg;
   uint64_t* keyg;
   int* uctr;
-  int32_t* wsel;
-  float* apo;
-  double* apl;
-  double* wmax;
   unsigned long long* tl;
   int32_t* selg;
   int* selctr;
@@ -92,15 +86,9 @@ DecodeWs carve_decode(const ctkv_layout* L, int C, int lmax, int ns, void* base,
   w.cval = reinterpret_cast<double*>(take(sizeof(double) * ncand_total));
   w.cidx = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * ncand_total));
   const size_t lm = (size_t)std::max(lmax, 1);
-  w.ctr = reinterpret_cast<int*>(take(sizeof(int) * (3 + 4 * (size_t)U)));
   w.recg = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U * lm));
-  w.Lg = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U));
   w.keyg = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * (size_t)U * lm));
   w.uctr = reinterpret_cast<int*>(take(sizeof(int) * 4 * (size_t)U));
-  w.wsel = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U * lm));
-  w.apo = reinterpret_cast<float*>(take(sizeof(float) * (size_t)U * 8 * gs * d));
-  w.apl = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * 8 * gs));
-  w.wmax = reinterpret_cast<double*>(take(sizeof(double) * (size_t)U * gs));
   w.tl = reinterpret_cast<unsigned long long*>(take(sizeof(unsigned long long) * 8));
   w.selg = reinterpret_cast<int32_t*>(take(sizeof(int32_t) * (size_t)U * std::max(c_prime, 1)));
   w.selctr = reinterpret_cast<int*>(take(sizeof(int) * (size_t)U));
@@ -268,15 +256,9 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.cval = w.cval;
   p.cidx = w.cidx;
   p.ncand = ncand_for(L, A->c_prime);
-  p.ctr = w.ctr;
   p.recg = w.recg;
-  p.Lg = w.Lg;
   p.keyg = w.keyg;
   p.uctr = w.uctr;
-  p.wsel = w.wsel;
-  p.apo = w.apo;
-  p.apl = w.apl;
-  p.wmax = w.wmax;
   p.tl = ctkv::kernel_timeline(-1) ? w.tl : nullptr;
   p.out = A->out;
   p.row_max = A->row_max;
@@ -296,7 +278,8 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   // v6: scan, then the 4-CTA cluster chain kernel; its tail (DCU, sparse
   // ids, cursor/total) can be deferred (phase bit 8) and enqueued separately
   // (phase 4) on another stream
-  if (v2 && ctkv::decode_variant() == 6 && chain_supported(p, L->dtype, L->head_dim)) {
+  if (v2 && ctkv::decode_variant() == 6 && chain_supported(p, L->dtype, L->head_dim) &&
+      tail_supported(p, L->dtype, L->head_dim)) {
     p.selg = w.selg;
     p.selctr = w.selctr;
     p.sel_in_chain = ctkv::scan_variant_v6() == 4 && scan4_supported(p, L->dtype, L->head_dim);
@@ -311,26 +294,9 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
     if (phase & 2)
       if (int rc = launch_chain(p, L->dtype, L->head_dim, st)) return rc;
     const bool tail = (phase & 4) || ((phase & 2) && !(phase & 8));
-    return tail ? launch_wide(p, L->dtype, L->head_dim, 2, st) : CTKV_OK;
-  }
-  // v5: wide unit pipeline; its tail (DCU, sparse ids, cursor/total) can be
-  // deferred (phase bit 8) and enqueued separately (phase 4) on another stream
-  if (v2 && ctkv::decode_variant() == 5 && wide_supported(p, L->dtype, L->head_dim)) {
-    const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
-    if (phase & 1)
-      if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;
-    const bool tail = (phase & 4) || ((phase & 2) && !(phase & 8));
-    const int what = ((phase & 2) ? 1 : 0) | (tail ? 2 : 0);
-    return what ? launch_wide(p, L->dtype, L->head_dim, what, st) : CTKV_OK;
+    return tail ? launch_tail(p, L->dtype, L->head_dim, st) : CTKV_OK;
   }
   p.uctr = nullptr;
-  // v4: one persistent layer kernel with a dependency-ordered task queue
-  const bool v4 = v2 && L->head_dim <= 128 && A->c_prime <= 64 && lmax <= 8192 &&
-                  ctkv::decode_variant() == 4;
-  if (v4) {
-    if (phase & 1) return launch_layer(p, L->dtype, L->head_dim, st);
-    return CTKV_OK;
-  }
   const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
   if (phase & 1)
     if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;

@@ -34,7 +34,7 @@
 //
 // The unit's keys and recall ids go to global memory for the deferred tail
 // kernel (full order, FIFO DCU, ordered sparse ids, cursor advance --
-// tail_wide_kernel in ctkv_unit_wide.cu), which runs on a side stream.
+// tail_kernel in ctkv_tail.cu), which runs on a side stream.
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>

@@ -1,16 +1,19 @@
 // Decode-step kernels for the B200 CTkvr path (sm_100a).
 //
-// One decode step per layer is two kernels (plus nothing else: the KV
-// append is folded into the first one):
+// The bf16 fused step is scan2_kernel (here) followed by the cluster chain
+// kernel (ctkv_chain.cu) and the deferred tail (ctkv_tail.cu).  This
+// file holds the scan, the exact f64 unit kernel of the fp32 parity path and
+// the staged API calls, the 2-CTA unit2 kernel (bf16 fallback), and the
+// generic id-list attention:
 //
-//   scan_kernel   -- every SM streams HBM: (a) per (b,g) unit, the cosine of
+//   scan2_kernel  -- every SM streams HBM: (a) per (b,g) unit, the cosine of
 //                    the gs query heads against all C centroids with the GQA
 //                    group max (Alg. 2 L1-2; ck/retrieval.py:144-145,
 //                    ck/tensor_ops.py:190-207); (b) split-K attention partials
 //                    over the static partition [0,L_init) U [ring_start,total)
 //                    (ck/retrieval.py:341-344).  Block 0 also appends the new
 //                    token's K/V (ck/store.py:114-129).
-//   unit_kernel   -- one CTA per (b,g) unit: top-C' slots (ties -> smaller
+//   unit_kernel   -- (fp32 / staged) one CTA per (b,g) unit: top-C' slots (ties -> smaller
 //                    slot), first-occurrence union of their lists through a
 //                    shared-memory bitmap (ck/retrieval.py:151-162), gathered
 //                    f64 q.k rerank with group max (ck/retrieval.py:171-218),
@@ -491,8 +494,6 @@ __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
     cos_task<T, D>(p, blockIdx.x, smem, bars);
   else
     static_task<T, D>(p, blockIdx.x - ncos, t0, total, smem, bars);
-  if (p.uctr != nullptr && blockIdx.x == gridDim.x - 1)
-    for (int i = threadIdx.x; i < 4 * p.U; i += blockDim.x) p.uctr[i] = 0;
   if (appending && blockIdx.x == 0) {
     T* keys = static_cast<T*>(const_cast<void*>(p.keys));
     T* vals = static_cast<T*>(const_cast<void*>(p.values));
@@ -506,301 +507,6 @@ __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
   }
   __syncthreads();
   ktl_mark(p.tl, 0, true);
-}
-
-// ------------------------------------------------------------------------
-// v3 scan: persistent and warp-specialised.  One CTA per SM; warp 0 (one
-// lane) is a TMA-bulk producer that keeps kScanStages x 64 KB of the CTA's
-// next tasks in flight; warps 1..8 consume: cosine tasks (256 centroid rows,
-// one row per thread, + chunk-local top-C' candidates) and static-attention
-// tasks (128 tokens of K and V).  Tasks are dealt round-robin
-// (task = blockIdx.x + k * gridDim.x), cosine tasks first.
-// ------------------------------------------------------------------------
-
-constexpr int kScanStages = 3;
-constexpr int kStageBytes = 64 * 1024 + 2048;   // rows/K+V + the unit's query heads (gs<=8)
-constexpr int kScan3Threads = 32 + kScanRowsV2;  // producer warp + 8 consumer warps
-
-__device__ __forceinline__ void bar_arrive_local(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(bar)) : "memory");
-}
-__device__ __forceinline__ void cons_sync() {   // consumer warps only
-  asm volatile("bar.sync 1, %0;" ::"n"(kScanRowsV2) : "memory");
-}
-
-template <typename T, int D>
-__device__ void scan3_issue(const DecodeParams& p, int task, int64_t t0, int64_t total,
-                            unsigned char* stage, uint64_t* full) {
-  constexpr int RB = D * int(sizeof(T));
-  const int ncos = p.U * p.cos_blocks_per_unit;
-  const int gs = p.gs;
-  const T* qsrc;
-  uint32_t bytes = 0;
-  unsigned char* qdst = stage + 64 * 1024;
-  if (task < ncos) {
-    const int CC = kScanRowsV2 / gs, cpu = p.cos_blocks_per_unit;
-    const int u = task / cpu, chunk = task % cpu;
-    const int bi = u / p.g, gi = u % p.g;
-    const int c0 = chunk * CC, nc = min(CC, p.C - c0);
-    qsrc = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-    bytes = (uint32_t)(gs * nc * RB + gs * RB);
-    bar_expect(full, bytes);
-    const T* cent = static_cast<const T*>(p.cent);
-    for (int j = 0; j < gs; ++j)
-      bulk_g2s(stage + (size_t)j * CC * RB, cent + (((int64_t)bi * p.h + gi * gs + j) * p.C + c0) * D,
-               (uint32_t)(nc * RB), full);
-  } else {
-    constexpr int ST = static_tok<T>();
-    const int st = task - ncos;
-    const int u = st / p.ns, split = st % p.ns;
-    const int bi = u / p.g, gi = u % p.g;
-    qsrc = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-    const StaticSpan span(total, p.init_len, p.local_len);
-    const int64_t i0 = (int64_t)split * ST;
-    const int nt = (int)max((int64_t)0, min((int64_t)ST, span.n_static - i0));
-    bytes = (uint32_t)(2 * nt * RB + gs * RB);
-    bar_expect(full, bytes);
-    const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
-    const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
-    T* Ks = reinterpret_cast<T*>(stage);
-    T* Vs = Ks + (size_t)ST * D;
-    const bool appending = p.k_new != nullptr;
-    int64_t i = i0;
-    const int64_t i1 = i0 + nt;
-    while (i < i1) {
-      const int64_t id = span.id(i);
-      const int64_t run_end = (i < span.n_init) ? min(i1, span.n_init) : i1;
-      int64_t n = run_end - i;
-      const bool has_new = appending && id <= t0 && t0 < id + n;
-      if (has_new) n = t0 - id;
-      if (n > 0) {
-        bulk_g2s(Ks + (size_t)(i - i0) * D, keys + id * D, (uint32_t)(n * RB), full);
-        bulk_g2s(Vs + (size_t)(i - i0) * D, vals + id * D, (uint32_t)(n * RB), full);
-      }
-      if (has_new) {
-        const int64_t at = i + n - i0;
-        bulk_g2s(Ks + (size_t)at * D, static_cast<const T*>(p.k_new) + (int64_t)u * D, RB, full);
-        bulk_g2s(Vs + (size_t)at * D, static_cast<const T*>(p.v_new) + (int64_t)u * D, RB, full);
-        n += 1;
-      }
-      i += n;
-    }
-  }
-  bulk_g2s(qdst, qsrc, (uint32_t)(gs * RB), full);
-}
-
-// consumer side of a cosine task (256 threads; rows already in `stage`)
-template <typename T, int D>
-__device__ void scan3_cos(const DecodeParams& p, int task, const unsigned char* stage,
-                          double* cosv, double* qn) {
-  const int ct = threadIdx.x - 32;            // consumer thread 0..255
-  const int gs = p.gs, CC = kScanRowsV2 / gs;
-  const int cpu = p.cos_blocks_per_unit;
-  const int u = task / cpu, chunk = task % cpu;
-  const int c0 = chunk * CC, nc = min(CC, p.C - c0);
-  const T* rows = reinterpret_cast<const T*>(stage);
-  const T* qs = reinterpret_cast<const T*>(stage + 64 * 1024);
-  query_norms<T, D>(qs, gs, qn, ct >> 5, kScanRowsV2 / 32);
-  double dot = 0.0, nrm = 0.0;
-  const int j = ct / CC, c = ct % CC;
-  const bool live = j < gs && c < nc;
-  const int bi3 = u / p.g, gi3 = u % p.g;
-  if (live) {
-    if (p.cnorm != nullptr) {
-      row_dot<T, D, false>(qs + j * D, rows + (size_t)ct * D, ct, dot, nrm);
-      nrm = (double)__ldg(p.cnorm + ((int64_t)bi3 * p.h + gi3 * gs + j) * p.C + c0 + c);
-      nrm *= nrm;
-    } else {
-      row_dot<T, D, true>(qs + j * D, rows + (size_t)ct * D, ct, dot, nrm);
-    }
-  }
-  cons_sync();
-  if (live) {
-    const double den = qn[j] * sqrt(nrm);
-    double cv;
-    if (den == 0.0) {
-      cv = 0.0;
-      set_flag(p.flags, kFlagDegenerate);
-    } else {
-      cv = fmin(fmax(dot / den, -1.0), 1.0);
-    }
-    cosv[ct] = cv;
-  }
-  cons_sync();
-  double* gv = cosv + kScanRowsV2;
-  if (ct < nc) {
-    double m = cosv[ct];
-    for (int jj = 1; jj < gs; ++jj) m = fmax(m, cosv[jj * CC + ct]);
-    p.gcos[(int64_t)u * p.C + c0 + ct] = m;
-    gv[ct] = m;
-  }
-  if (p.cval != nullptr) {
-    cons_sync();
-    if (ct < 32) {
-      const int lane = ct;
-      uint64_t prev_key = ~0ull;
-      int prev_idx = -1;
-      const int64_t base = ((int64_t)u * cpu + chunk) * p.ncand;
-      for (int r = 0; r < p.ncand; ++r) {
-        uint64_t bk = 0;
-        int bidx = INT32_MAX;
-        for (int cc = lane; cc < nc; cc += 32) {
-          const uint64_t k = okey64(gv[cc]);
-          const int i = c0 + cc;
-          const bool below = k < prev_key || (k == prev_key && i > prev_idx);
-          if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
-          const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
-          if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
-        }
-        if (lane == 0) {
-          p.cval[base + r] = bidx == INT32_MAX ? -INFINITY : gv[bidx - c0];
-          p.cidx[base + r] = bidx;
-        }
-        prev_key = bk;
-        prev_idx = bidx;
-      }
-    }
-  }
-}
-
-// consumer side of a static-attention task
-template <typename T, int D>
-__device__ void scan3_static(const DecodeParams& p, int st, int64_t total,
-                             const unsigned char* stage, double* lg, float* w, double* ml) {
-  constexpr int ST = static_tok<T>();
-  const int ct = threadIdx.x - 32;
-  const int gs = p.gs;
-  const int u = st / p.ns, split = st % p.ns;
-  const StaticSpan span(total, p.init_len, p.local_len);
-  const int64_t i0 = (int64_t)split * ST;
-  const int nt = (int)max((int64_t)0, min((int64_t)ST, span.n_static - i0));
-  const int64_t slot = (int64_t)u * p.ns + split;
-  double* pm = p.pm + slot * gs;
-  double* pl = p.pl + slot * gs;
-  float* po = p.po + slot * gs * D;
-  if (nt == 0) {
-    for (int i = ct; i < gs * D; i += kScanRowsV2) po[i] = 0.f;
-    if (ct < gs) { pm[ct] = -INFINITY; pl[ct] = 0.0; }
-    return;
-  }
-  const T* Ks = reinterpret_cast<const T*>(stage);
-  const T* Vs = Ks + (size_t)ST * D;
-  const T* qs = reinterpret_cast<const T*>(stage + 64 * 1024);
-  const double scale = 1.0 / sqrt((double)D);
-  for (int pr = ct; pr < nt * gs; pr += kScanRowsV2) {
-    const int t = pr % nt, j = pr / nt;
-    double dot, nrm;
-    row_dot<T, D, false>(qs + j * D, Ks + (size_t)t * D, t, dot, nrm);
-    lg[j * ST + t] = dot * scale;
-  }
-  cons_sync();
-  const int warp = ct >> 5, lane = ct & 31;
-  for (int j = warp; j < gs; j += kScanRowsV2 / 32) {
-    double m = -INFINITY;
-    for (int t = lane; t < nt; t += 32) m = fmax(m, lg[j * ST + t]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    double l = 0.0;
-    for (int t = lane; t < nt; t += 32) {
-      const double e = exp(lg[j * ST + t] - m);
-      w[j * ST + t] = (float)e;
-      l += e;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane == 0) { ml[j] = m; ml[gs + j] = l; }
-  }
-  cons_sync();
-  for (int pr = ct; pr < gs * (D / 2); pr += kScanRowsV2) {
-    const int j = pr / (D / 2), e = 2 * (pr % (D / 2));
-    float a0 = 0.f, a1 = 0.f;
-    const float* wj = w + j * ST;
-    for (int t = 0; t < nt; ++t) {
-      const T* vr = Vs + (size_t)t * D + e;
-      a0 = fmaf(wj[t], to_f(vr[0]), a0);
-      a1 = fmaf(wj[t], to_f(vr[1]), a1);
-    }
-    po[j * D + e] = a0;
-    po[j * D + e + 1] = a1;
-  }
-  if (ct < gs) {
-    pm[ct] = ml[ct];
-    pl[ct] = ml[gs + ct];
-  }
-}
-
-template <typename T, int D>
-__global__ void __launch_bounds__(kScan3Threads, 1) scan3_kernel(DecodeParams p) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t full[kScanStages], empty[kScanStages];
-  const int64_t t0 = p.total ? *p.total : p.id_bound;
-  const bool appending = p.k_new != nullptr;
-  const int64_t total = t0 + (appending ? 1 : 0);
-  const int ncos = p.do_cos ? p.U * p.cos_blocks_per_unit : 0;
-  const int ntasks = ncos + p.U * p.ns;
-  // per-task scratch after the stage ring
-  unsigned char* scratch = smem + (size_t)kScanStages * kStageBytes;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kScanStages; ++s) {
-      bar_init(&full[s], 1);
-      bar_init(&empty[s], 1);
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    if (threadIdx.x == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
-        bar_wait(&empty[stage], phase ^ 1);
-        scan3_issue<T, D>(p, task, t0, total, smem + (size_t)stage * kStageBytes, &full[stage]);
-        if (++stage == kScanStages) { stage = 0; phase ^= 1; }
-      }
-    }
-  } else {
-    int stage = 0;
-    uint32_t phase = 0;
-    constexpr int ST = static_tok<T>();
-    double* cosv = reinterpret_cast<double*>(scratch);                 // [2 * 256]
-    double* qn = cosv + 2 * kScanRowsV2;                               // [8]
-    double* lg = qn + 8;                                               // [gs<=8][ST]
-    float* w = reinterpret_cast<float*>(lg + 8 * ST);                  // [gs][ST]
-    double* ml = reinterpret_cast<double*>(w + 8 * ST);                // [2][gs]
-    for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
-      bar_wait(&full[stage], phase);
-      const unsigned char* st = smem + (size_t)stage * kStageBytes;
-      if (task < ncos)
-        scan3_cos<T, D>(p, task, st, cosv, qn);
-      else
-        scan3_static<T, D>(p, task - ncos, total, st, lg, w, ml);
-      cons_sync();   // every consumer is done with the stage (and the scratch)
-      if (threadIdx.x == 32) bar_arrive_local(&empty[stage]);
-      if (++stage == kScanStages) { stage = 0; phase ^= 1; }
-    }
-  }
-  if (appending && blockIdx.x == 0) {
-    __syncthreads();
-    T* keys = static_cast<T*>(const_cast<void*>(p.keys));
-    T* vals = static_cast<T*>(const_cast<void*>(p.values));
-    const T* kn = static_cast<const T*>(p.k_new);
-    const T* vn = static_cast<const T*>(p.v_new);
-    for (int64_t i = threadIdx.x; i < (int64_t)p.U * D; i += blockDim.x) {
-      const int64_t uu = i / D, e = i % D;
-      keys[(uu * p.cap + t0) * D + e] = kn[i];
-      vals[(uu * p.cap + t0) * D + e] = vn[i];
-    }
-  }
-}
-
-template <typename T, int D>
-size_t scan3_smem() {
-  constexpr int ST = static_tok<T>();
-  return (size_t)kScanStages * kStageBytes + sizeof(double) * (2 * kScanRowsV2 + 8) +
-         sizeof(double) * 8 * ST + sizeof(float) * 8 * ST + sizeof(double) * 2 * 8;
 }
 
 template <typename T, int D>
@@ -1676,747 +1382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kU2Threads, 1)
 }
 
 // ------------------------------------------------------------------------
-// v4 layer kernel: persistent workers (2 per SM) + a dependency-ordered task
-// queue.  Task ids, in claim order:
-//   cos(u, chunk)  -> gcos + chunk top-C' candidates          [U * cpu]
-//   union(u)       -> top-C' slots, first-occurrence union     [U]
-//   static(u, j)   -> static-partition softmax partials        [U * ns]
-//   logit(u, k)    -> rerank logits + packed keys, part k      [U * kLParts]
-//   attend(u)      -> top-rho' select, sparse attention, merge [U]
-//   dcu(u)         -> full order, FIFO DCU, ordered sparse ids [U]
-// A task only waits on tasks with smaller ids (already claimed by running
-// workers), so the spin-waits cannot deadlock.  Cross-task data goes through
-// L2 (ld.global.cg); completion counters use release/acquire.
-// ------------------------------------------------------------------------
-
-constexpr int kLW = 256;          // threads per worker
-constexpr int kLParts = 8;        // logit tasks per unit
-constexpr int kLUnionItems = 32;  // union elements per thread in registers (c'rho <= 8192)
-
-__device__ __forceinline__ int ld_acq(const int* p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void wait_ge(const int* p, int target) {
-  if (threadIdx.x == 0) {
-    while (ld_acq(p) < target) __nanosleep(32);
-  }
-  __syncthreads();
-}
-__device__ __forceinline__ void task_done(int* p) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(p, 1);
-  }
-}
-template <typename X>
-__device__ __forceinline__ X ldcg(const X* p) { return __ldcg(p); }
-
-struct LayerPlan {
-  int cpu, ncos, o_union, o_static, o_logit, o_att, o_dcu, ntask;
-  int *claim, *started, *dcu_done, *cos_done, *union_done, *static_done, *logit_done;
-  __device__ LayerPlan(const DecodeParams& p) {
-    cpu = p.cos_blocks_per_unit;
-    ncos = p.U * cpu;
-    o_union = ncos;
-    o_static = o_union + p.U;
-    o_logit = o_static + p.U * p.ns;
-    o_att = o_logit + p.U * kLParts;
-    o_dcu = o_att + p.U;
-    ntask = o_dcu + p.U;
-    claim = p.ctr;
-    started = p.ctr + 1;
-    dcu_done = p.ctr + 2;
-    cos_done = p.ctr + 3;
-    union_done = cos_done + p.U;
-    static_done = union_done + p.U;
-    logit_done = static_done + p.U;
-  }
-};
-
-// cosine task with persistent barriers (parity tracked in `ph`)
-template <typename T, int D>
-__device__ void l_cos(const DecodeParams& p, int task, unsigned char* smem, uint64_t* bars,
-                      uint32_t& ph) {
-  constexpr int RB = D * int(sizeof(T));
-  const int gs = p.gs, CC = kScanRowsV2 / gs;
-  const int cpu = p.cos_blocks_per_unit;
-  const int u = task / cpu, chunk = task % cpu;
-  const int bi = u / p.g, gi = u % p.g;
-  const int c0 = chunk * CC, nc = min(CC, p.C - c0);
-  T* rows = reinterpret_cast<T*>(smem);
-  T* qs = reinterpret_cast<T*>(smem + (size_t)kScanRowsV2 * RB);
-  double* qn = reinterpret_cast<double*>(qs + gs * D);
-  double* cosv = qn + gs;
-  double* gv = cosv + kScanRowsV2;
-  const T* cent = static_cast<const T*>(p.cent);
-  if (threadIdx.x == 0) {
-    for (int j = 0; j < gs; ++j) {
-      bar_expect(&bars[j], (uint32_t)(nc * RB));
-      bulk_g2s(rows + (size_t)j * CC * D, cent + (((int64_t)bi * p.h + gi * gs + j) * p.C + c0) * D,
-               (uint32_t)(nc * RB), &bars[j]);
-    }
-  }
-  // the rows are in flight; the query may come from the previous kernel and
-  // rides its own bulk copy
-  pdl_wait();
-  uint64_t* barq = &bars[kMaxGroup - 1];
-  if (threadIdx.x == 0) {
-    bar_init(barq, 1);
-    bar_expect(barq, (uint32_t)(gs * D * sizeof(T)));
-    bulk_g2s(qs, static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D,
-             (uint32_t)(gs * D * sizeof(T)), barq);
-  }
-  __syncthreads();
-  bar_wait(barq, 0);
-  query_norms<T, D>(qs, gs, qn, threadIdx.x >> 5, blockDim.x >> 5);
-  __syncthreads();
-  for (int r = threadIdx.x; r < gs * CC; r += blockDim.x) {
-    const int j = r / CC, c = r % CC;
-    if (c >= nc) continue;
-    bar_wait(&bars[j], (ph >> j) & 1u);
-    double dot, nrm;
-    double cn;
-    if (p.cnorm != nullptr) {
-      row_dot<T, D, false>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
-      cn = (double)__ldcg(p.cnorm + ((int64_t)bi * p.h + gi * gs + j) * p.C + c0 + c);
-    } else {
-      row_dot<T, D, true>(qs + j * D, rows + (size_t)r * D, r, dot, nrm);
-      cn = sqrt(nrm);
-    }
-    const double den = qn[j] * cn;
-    double cv;
-    if (den == 0.0) {
-      cv = 0.0;
-      set_flag(p.flags, kFlagDegenerate);
-    } else {
-      cv = fmin(fmax(dot / den, -1.0), 1.0);
-    }
-    cosv[r] = cv;
-  }
-  ph ^= (1u << gs) - 1u;
-  __syncthreads();
-  for (int c = threadIdx.x; c < nc; c += blockDim.x) {
-    double m = cosv[c];
-    for (int j = 1; j < gs; ++j) m = fmax(m, cosv[j * CC + c]);
-    p.gcos[(int64_t)u * p.C + c0 + c] = m;
-    gv[c] = m;
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    uint64_t prev_key = ~0ull;
-    int prev_idx = -1;
-    const int64_t base = ((int64_t)u * cpu + chunk) * p.ncand;
-    for (int r = 0; r < p.ncand; ++r) {
-      uint64_t bk = 0;
-      int bidx = INT32_MAX;
-      for (int cc = lane; cc < nc; cc += 32) {
-        const uint64_t k = okey64(gv[cc]);
-        const int i = c0 + cc;
-        const bool below = k < prev_key || (k == prev_key && i > prev_idx);
-        if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
-        if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
-      }
-      if (lane == 0) {
-        p.cval[base + r] = bidx == INT32_MAX ? -INFINITY : gv[bidx - c0];
-        p.cidx[base + r] = bidx;
-      }
-      prev_key = bk;
-      prev_idx = bidx;
-    }
-  }
-}
-
-template <typename T, int D>
-__device__ void l_static(const DecodeParams& p, int stt, int64_t t0, int64_t total,
-                         unsigned char* smem, uint64_t* bars, uint32_t& ph) {
-  constexpr int RB = D * int(sizeof(T));
-  constexpr int ST = static_tok<T>();
-  const int gs = p.gs;
-  const int u = stt / p.ns, split = stt % p.ns;
-  const int bi = u / p.g, gi = u % p.g;
-  const StaticSpan span(total, p.init_len, p.local_len);
-  const int64_t i0 = (int64_t)split * ST;
-  const int nt = (int)max((int64_t)0, min((int64_t)ST, span.n_static - i0));
-  T* Ks = reinterpret_cast<T*>(smem);
-  T* Vs = Ks + (size_t)ST * D;
-  T* qs = Vs + (size_t)ST * D;
-  double* lg = reinterpret_cast<double*>(qs + gs * D);
-  float* w = reinterpret_cast<float*>(lg + gs * ST);
-  double* ml = reinterpret_cast<double*>(w + gs * ST);
-  const int64_t slot = (int64_t)u * p.ns + split;
-  double* pm = p.pm + slot * gs;
-  double* pl = p.pl + slot * gs;
-  float* po = p.po + slot * gs * D;
-  if (nt == 0) {
-    for (int i = threadIdx.x; i < gs * D; i += blockDim.x) po[i] = 0.f;
-    if (threadIdx.x < gs) { pm[threadIdx.x] = -INFINITY; pl[threadIdx.x] = 0.0; }
-    return;
-  }
-  const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
-  const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
-  const bool appending = p.k_new != nullptr;
-  uint64_t* barK = &bars[0];
-  uint64_t* barV = &bars[1];
-  if (threadIdx.x == 0) {
-    bar_expect(barK, (uint32_t)(nt * RB));
-    bar_expect(barV, (uint32_t)(nt * RB));
-    int64_t i = i0;
-    const int64_t i1 = i0 + nt;
-    while (i < i1) {
-      const int64_t id = span.id(i);
-      const int64_t run_end = (i < span.n_init) ? min(i1, span.n_init) : i1;
-      int64_t n = run_end - i;
-      const bool has_new = appending && id <= t0 && t0 < id + n;
-      if (has_new) n = t0 - id;
-      if (n > 0) {
-        bulk_g2s(Ks + (size_t)(i - i0) * D, keys + id * D, (uint32_t)(n * RB), barK);
-        bulk_g2s(Vs + (size_t)(i - i0) * D, vals + id * D, (uint32_t)(n * RB), barV);
-      }
-      if (has_new) {
-        const int64_t at = i + n - i0;
-        bulk_g2s(Ks + (size_t)at * D, static_cast<const T*>(p.k_new) + (int64_t)u * D, RB, barK);
-        bulk_g2s(Vs + (size_t)at * D, static_cast<const T*>(p.v_new) + (int64_t)u * D, RB, barV);
-        n += 1;
-      }
-      i += n;
-    }
-  }
-  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int k = threadIdx.x; k < gs * D; k += blockDim.x) qs[k] = q[k];
-  __syncthreads();
-  bar_wait(barK, ph & 1u);
-  const double scale = 1.0 / sqrt((double)D);
-  for (int pr = threadIdx.x; pr < nt * gs; pr += blockDim.x) {
-    const int t = pr % nt, j = pr / nt;
-    double dot, nrm;
-    row_dot<T, D, false>(qs + j * D, Ks + (size_t)t * D, t, dot, nrm);
-    lg[j * ST + t] = dot * scale;
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int j = warp; j < gs; j += nw) {
-    double m = -INFINITY;
-    for (int t = lane; t < nt; t += 32) m = fmax(m, lg[j * ST + t]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    double l = 0.0;
-    for (int t = lane; t < nt; t += 32) {
-      const double e = exp(lg[j * ST + t] - m);
-      w[j * ST + t] = (float)e;
-      l += e;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane == 0) { ml[j] = m; ml[gs + j] = l; }
-  }
-  __syncthreads();
-  bar_wait(barV, (ph >> 1) & 1u);
-  ph ^= 3u;
-  for (int pr = threadIdx.x; pr < gs * (D / 2); pr += blockDim.x) {
-    const int j = pr / (D / 2), e = 2 * (pr % (D / 2));
-    float a0 = 0.f, a1 = 0.f;
-    const float* wj = w + j * ST;
-    for (int t = 0; t < nt; ++t) {
-      const T* vr = Vs + (size_t)t * D + e;
-      a0 = fmaf(wj[t], to_f(vr[0]), a0);
-      a1 = fmaf(wj[t], to_f(vr[1]), a1);
-    }
-    po[j * D + e] = a0;
-    po[j * D + e + 1] = a1;
-  }
-  if (threadIdx.x < gs) {
-    pm[threadIdx.x] = ml[threadIdx.x];
-    pl[threadIdx.x] = ml[gs + threadIdx.x];
-  }
-}
-
-// top-C' slots + first-occurrence union -> recg[u][*], Lg[u]
-__device__ void l_union(const DecodeParams& p, int u, int64_t total, unsigned char* smem) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-  int32_t* sel = reinterpret_cast<int32_t*>(smem);                   // [c_prime]
-  int* wtot = sel + 64;                                               // [nw + 1]
-  uint32_t* bm = reinterpret_cast<uint32_t*>(smem + 512);             // [c'][words]
-  const int cpu = p.cos_blocks_per_unit;
-  if (warp == 0) {
-    const int M = cpu * p.ncand;
-    const double* cv = p.cval + (int64_t)u * M;
-    const int32_t* ci = p.cidx + (int64_t)u * M;
-    constexpr int KR = 8;
-    uint64_t rk[KR];
-    int ri[KR];
-#pragma unroll
-    for (int r = 0; r < KR; ++r) {
-      const int m = lane + 32 * r;
-      rk[r] = m < M ? okey64(ldcg(cv + m)) : 0ull;
-      ri[r] = m < M ? ldcg(ci + m) : INT32_MAX;
-    }
-    uint64_t prev_key = ~0ull;
-    int prev_idx = -1;
-    for (int r = 0; r < p.c_prime; ++r) {
-      uint64_t bk = 0;
-      int bidx = INT32_MAX;
-#pragma unroll
-      for (int x = 0; x < KR; ++x) {
-        const bool below = rk[x] < prev_key || (rk[x] == prev_key && ri[x] > prev_idx);
-        if (below && (rk[x] > bk || (rk[x] == bk && ri[x] < bidx))) { bk = rk[x]; bidx = ri[x]; }
-      }
-      for (int m = lane + 32 * KR; m < M; m += 32) {
-        const uint64_t k = okey64(ldcg(cv + m));
-        const int i = ldcg(ci + m);
-        const bool below = k < prev_key || (k == prev_key && i > prev_idx);
-        if (below && (k > bk || (k == bk && i < bidx))) { bk = k; bidx = i; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
-        if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
-      }
-      if (lane == 0) sel[r] = bidx;
-      prev_key = bk;
-      prev_idx = bidx;
-    }
-  }
-  const int nb = p.c_prime;
-  const int words = (int)((total + 31) >> 5);
-  for (int i = tid; i < nb * words; i += blockDim.x) bm[i] = 0u;
-  __syncthreads();
-  if (p.selected)
-    for (int r = tid; r < p.c_prime; r += blockDim.x) p.selected[(int64_t)u * p.c_prime + r] = sel[r];
-  const int n = nb * p.rho;
-  const int P = ((n + nw - 1) / nw + 31) & ~31;
-  const int nit = P / 32;
-  int ids[kLUnionItems];
-  int lst[kLUnionItems];
-#pragma unroll
-  for (int it = 0; it < kLUnionItems; ++it) {
-    ids[it] = kEmpty;
-    lst[it] = 0;
-    const int o = warp * P + it * 32 + lane;
-    if (it < nit && o < n) {
-      const int j = o / p.rho;
-      int id = p.lists[((int64_t)u * p.C + sel[j]) * p.rho + (o - j * p.rho)];
-      if (id != kEmpty && (id < 0 || id >= total)) { set_flag(p.flags, kFlagIdRange); id = kEmpty; }
-      ids[it] = id;
-      lst[it] = j;
-    }
-  }
-#pragma unroll
-  for (int it = 0; it < kLUnionItems; ++it)
-    if (ids[it] != kEmpty) atomicOr(&bm[lst[it] * words + (ids[it] >> 5)], 1u << (ids[it] & 31));
-  __syncthreads();
-  int wcount = 0;
-  unsigned keepm[kLUnionItems];
-#pragma unroll
-  for (int it = 0; it < kLUnionItems; ++it) {
-    bool keep = ids[it] != kEmpty;
-    if (keep)
-      for (int j2 = 0; j2 < lst[it]; ++j2)
-        keep = keep && !((bm[j2 * words + (ids[it] >> 5)] >> (ids[it] & 31)) & 1u);
-    keepm[it] = __ballot_sync(0xffffffffu, keep);
-    wcount += __popc(keepm[it]);
-  }
-  if (lane == 0) wtot[warp] = wcount;
-  __syncthreads();
-  int base = 0;
-  for (int w = 0; w < warp; ++w) base += wtot[w];
-  int32_t* rec = p.recg + (int64_t)u * p.lmax;
-  const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-  for (int it = 0; it < kLUnionItems; ++it) {
-    if ((keepm[it] >> lane) & 1u) rec[base + __popc(keepm[it] & lt)] = ids[it];
-    base += __popc(keepm[it]);
-  }
-  if (tid == 0) {
-    int t = 0;
-    for (int w = 0; w < nw; ++w) t += wtot[w];
-    p.Lg[u] = t;
-    if (p.recall_len) p.recall_len[u] = t;
-    set_flag(p.flags, t > 0 ? kFlagNonEmptyRecall : kFlagEmptyRecall);
-  }
-}
-
-// rerank logits of recall positions [lo, hi) of unit u (8 lanes per row)
-template <typename T, int D>
-__device__ void l_logit(const DecodeParams& p, int u, int part, unsigned char* smem) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-  const int L = ldcg(p.Lg + u);
-  const int lo = (int)((int64_t)L * part / kLParts), hi = (int)((int64_t)L * (part + 1) / kLParts);
-  if (hi <= lo) return;
-  const int bi = u / p.g, gi = u % p.g, gs = p.gs;
-  T* qs = reinterpret_cast<T*>(smem);
-  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int i = tid; i < gs * D; i += blockDim.x) qs[i] = q[i];
-  __syncthreads();
-  const int32_t* rec = p.recg + (int64_t)u * p.lmax;
-  double* lg = p.logits + (int64_t)u * gs * p.lmax;
-  uint64_t* kg = p.keyg + (int64_t)u * p.lmax;
-  const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
-  const double scale = 1.0 / sqrt((double)D);
-  constexpr int VPR = D * int(sizeof(T)) / 16;
-  constexpr int LPRL = VPR >= 8 ? 8 : VPR;
-  constexpr int CPL = VPR / LPRL;
-  constexpr int RPWL = 32 / LPRL;
-  constexpr int UNL = 6;
-  const int sub = lane % LPRL, rw = lane / LPRL;
-  const int stepw = nw * RPWL;
-  for (int b0 = lo + warp * RPWL; b0 < hi; b0 += stepw * UNL) {
-    uint4 raw[UNL][CPL];
-    int tt[UNL];
-#pragma unroll
-    for (int u2 = 0; u2 < UNL; ++u2) {
-      tt[u2] = b0 + u2 * stepw + rw;
-      if (tt[u2] < hi) {
-        const uint4* r4 = reinterpret_cast<const uint4*>(keys + (int64_t)ldcg(rec + tt[u2]) * D);
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) raw[u2][c] = ldg16(r4 + c * LPRL + sub);
-      } else {
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) raw[u2][c] = make_uint4(0, 0, 0, 0);
-      }
-    }
-#pragma unroll
-    for (int u2 = 0; u2 < UNL; ++u2) {
-      double gmax = -INFINITY;
-      for (int hh = 0; hh < gs; ++hh) {
-        const uint4* q4 = reinterpret_cast<const uint4*>(qs + hh * D);
-        double a = 0.0;
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) a += (double)bf16x8_dot(q4[c * LPRL + sub], raw[u2][c], 0.f);
-#pragma unroll
-        for (int o = 1; o < LPRL; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-        a *= scale;
-        if (sub == 0 && tt[u2] < hi) lg[(int64_t)hh * p.lmax + tt[u2]] = a;
-        gmax = fmax(gmax, a);
-      }
-      if (sub == 0 && tt[u2] < hi)
-        kg[tt[u2]] = ((uint64_t)(~okey32((float)gmax)) << 32) | (uint32_t)tt[u2];
-    }
-  }
-}
-
-// top-rho' set, sparse attention over it, exact merge with the static partials
-template <typename T, int D>
-__device__ void l_attend(const DecodeParams& p, int u, unsigned char* smem) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-  const int gs = p.gs, ns = p.ns;
-  const int bi = u / p.g, gi = u % p.g;
-  const int L = ldcg(p.Lg + u);
-  const int Rn = (L > 0) ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
-  // smem: keys [L] (then the V reduce area) | spos [Rn] | wts | spml | spo | hist | scratch
-  size_t off = 0;
-  auto take = [&](size_t b) { unsigned char* x = smem + off; off += align16(b); return x; };
-  const size_t red_bytes = (size_t)nw * gs * D * 4;
-  const size_t key_bytes = (size_t)(L > 0 ? L : 1) * 8;
-  uint64_t* keys = reinterpret_cast<uint64_t*>(take(key_bytes > red_bytes ? key_bytes : red_bytes));
-  int* spos = reinterpret_cast<int*>(take(sizeof(int) * (Rn > 0 ? Rn : 1)));
-  float* wts = reinterpret_cast<float*>(take(sizeof(float) * gs * kAttnChunk));
-  double* spml = reinterpret_cast<double*>(take(sizeof(double) * 2 * ns * gs));
-  float* spo = reinterpret_cast<float*>(take(sizeof(float) * ns * gs * D));
-  int* hist = reinterpret_cast<int*>(take(sizeof(int) * 256));
-  double* scr = reinterpret_cast<double*>(take(sizeof(double) * (gs * (ns + 1) > 64 ? gs * (ns + 1) : 64)));
-  __shared__ double ms[kMaxGroup], ls[kMaxGroup];
-  __shared__ int s_state[4];
-  const int64_t pbase = (int64_t)u * ns;
-  for (int i = tid; i < ns * gs; i += blockDim.x) {
-    spml[i] = ldcg(p.pm + pbase * gs + i);
-    spml[ns * gs + i] = ldcg(p.pl + pbase * gs + i);
-  }
-  for (int i = tid; i < ns * gs * D; i += blockDim.x) spo[i] = ldcg(p.po + pbase * gs * D + i);
-  const uint64_t* kg = p.keyg + (int64_t)u * p.lmax;
-  for (int i = tid; i < L; i += blockDim.x) keys[i] = ldcg(kg + i);
-  __syncthreads();
-  const int nsel = Rn > 0 ? select_smallest(keys, L, Rn, spos, hist, s_state) : 0;
-  const double* lg = p.logits + (int64_t)u * gs * p.lmax;
-  const int32_t* rec = p.recg + (int64_t)u * p.lmax;
-  for (int h0 = 0; h0 < gs; h0 += 4) {
-    double m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-    for (int i = tid; i < nsel; i += blockDim.x) {
-      const int ps = spos[i];
-#pragma unroll
-      for (int hh = 0; hh < 4; ++hh)
-        if (h0 + hh < gs) m4[hh] = fmax(m4[hh], ldcg(lg + (int64_t)(h0 + hh) * p.lmax + ps));
-    }
-#pragma unroll
-    for (int hh = 0; hh < 4; ++hh)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m4[hh] = fmax(m4[hh], __shfl_xor_sync(0xffffffffu, m4[hh], o));
-    __syncthreads();
-    if (lane == 0)
-#pragma unroll
-      for (int hh = 0; hh < 4; ++hh) scr[warp * 4 + hh] = m4[hh];
-    __syncthreads();
-    if (tid < 4 && h0 + tid < gs) {
-      double m = -INFINITY;
-      for (int w = 0; w < nw; ++w) m = fmax(m, scr[w * 4 + tid]);
-      ms[h0 + tid] = m;
-      ls[h0 + tid] = 0.0;
-    }
-  }
-  __syncthreads();
-  float* red = reinterpret_cast<float*>(keys);
-  for (int i = tid; i < nw * gs * D; i += blockDim.x) red[i] = 0.f;
-  const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
-  for (int c0 = 0; c0 < nsel; c0 += kAttnChunk) {
-    const int n = min(kAttnChunk, nsel - c0);
-    for (int h0 = 0; h0 < gs; h0 += 4) {
-      double l4[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int i = tid; i < n; i += blockDim.x) {
-        const int ps = spos[c0 + i];
-#pragma unroll
-        for (int hh = 0; hh < 4; ++hh)
-          if (h0 + hh < gs) {
-            const double e = exp(ldcg(lg + (int64_t)(h0 + hh) * p.lmax + ps) - ms[h0 + hh]);
-            wts[(h0 + hh) * kAttnChunk + i] = (float)e;
-            l4[hh] += e;
-          }
-      }
-#pragma unroll
-      for (int hh = 0; hh < 4; ++hh)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) l4[hh] += __shfl_xor_sync(0xffffffffu, l4[hh], o);
-      __syncthreads();
-      if (lane == 0)
-#pragma unroll
-        for (int hh = 0; hh < 4; ++hh) scr[warp * 4 + hh] = l4[hh];
-      __syncthreads();
-      if (tid < 4 && h0 + tid < gs) {
-        double l = 0.0;
-        for (int w = 0; w < nw; ++w) l += scr[w * 4 + tid];
-        ls[h0 + tid] += l;
-      }
-    }
-    __syncthreads();
-    accum_weighted_rows<T, D>(
-        n, gs, [&](int t) -> const T* { return vals + (int64_t)ldcg(rec + spos[c0 + t]) * D; },
-        [&](int hh, int t) { return wts[hh * kAttnChunk + t]; }, red + (int64_t)warp * gs * D);
-    __syncthreads();
-  }
-  // merge: per-head weights once, then per element
-  if (tid < gs) {
-    const int hh = tid;
-    double M = ls[hh] > 0.0 ? ms[hh] : -INFINITY;
-    for (int j = 0; j < ns; ++j)
-      if (spml[ns * gs + j * gs + hh] > 0.0) M = fmax(M, spml[j * gs + hh]);
-    double Ls = 0.0;
-    for (int j = 0; j < ns; ++j) {
-      const double lj = spml[ns * gs + j * gs + hh];
-      const double w = lj > 0.0 ? exp(spml[j * gs + hh] - M) : 0.0;
-      scr[hh * (ns + 1) + j] = w;
-      Ls += w * lj;
-    }
-    const double wsp = ls[hh] > 0.0 ? exp(ms[hh] - M) : 0.0;
-    scr[hh * (ns + 1) + ns] = wsp;
-    Ls += wsp * ls[hh];
-    ms[hh] = M;
-    ls[hh] = Ls;
-  }
-  __syncthreads();
-  bool none = false;
-  for (int i = tid; i < gs * D; i += blockDim.x) {
-    const int hh = i / D, e = i % D;
-    float o0 = 0.f;
-    for (int w = 0; w < nw; ++w) o0 += red[(int64_t)w * gs * D + i];
-    const double* wh = scr + hh * (ns + 1);
-    double O = wh[ns] * (double)o0;
-    for (int j = 0; j < ns; ++j) O += wh[j] * (double)spo[(j * gs + hh) * D + e];
-    const double Ls = ls[hh];
-    const int64_t oh = (int64_t)bi * p.h + gi * gs + hh;
-    if (Ls > 0.0) {
-      p.out[oh * D + e] = (float)(O / Ls);
-    } else {
-      p.out[oh * D + e] = 0.f;
-      none = true;
-    }
-    if (e == 0) {
-      if (p.row_max) p.row_max[oh] = ms[hh];
-      if (p.denom) p.denom[oh] = Ls;
-    }
-  }
-  if (none) set_flag(p.flags, kFlagNoTokens);
-  if (p.sparse_len && tid == 0) p.sparse_len[u] = Rn;
-}
-
-template <int IPT>
-__device__ void l_sort(uint64_t* keys) {
-  uint64_t k[IPT];
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) k[i] = keys[threadIdx.x * IPT + i];
-  bitonic_regs<IPT>(k, keys);
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) keys[threadIdx.x * IPT + i] = k[i];
-  __syncthreads();
-}
-
-// full order, FIFO DCU, ordered sparse ids; the last one advances the cursor
-template <typename T, int D>
-__device__ void l_dcu(const DecodeParams& p, int u, int64_t t0, const LayerPlan& lp,
-                      unsigned char* smem) {
-  const int tid = threadIdx.x;
-  const int gs = p.gs;
-  const int bi = u / p.g, gi = u % p.g;
-  const int L = ldcg(p.Lg + u);
-  const bool dcu_here = (p.stages & kStageDcu) && L > 0;
-  const int Rn = (L > 0) ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
-  const bool need_order = L > 0 && (dcu_here || (p.sparse_ids && p.use_rerank));
-  uint64_t* keys = reinterpret_cast<uint64_t*>(smem);
-  const int32_t* rec = p.recg + (int64_t)u * p.lmax;
-  __shared__ int64_t s_slot;
-  if (tid == 0) s_slot = p.fifo ? (ldcg(p.fifo + bi) % p.C) : 0;
-  if (need_order) {
-    int np = next_pow2(L);
-    if (np < (int)blockDim.x) np = blockDim.x;
-    const uint64_t* kg = p.keyg + (int64_t)u * p.lmax;
-    for (int i = tid; i < np; i += blockDim.x) keys[i] = i < L ? ldcg(kg + i) : ~0ull;
-    __syncthreads();
-    switch (np / (int)blockDim.x) {
-      case 1: l_sort<1>(keys); break;
-      case 2: l_sort<2>(keys); break;
-      case 4: l_sort<4>(keys); break;
-      case 8: l_sort<8>(keys); break;
-      case 16: l_sort<16>(keys); break;
-      default: bitonic_sort_u64(keys, np); break;
-    }
-  }
-  __syncthreads();
-  auto pos_at = [&](int i) { return (int)(uint32_t)(keys[i] & 0xffffffffu); };
-  if (dcu_here) {
-    const int64_t slot = s_slot;
-    int32_t* row = p.lists + ((int64_t)u * p.C + slot) * p.rho;
-    const int keep = min(p.rho, L);
-    for (int i = tid; i < p.rho; i += blockDim.x) row[i] = i < keep ? ldcg(rec + pos_at(i)) : kEmpty;
-    T* cent = static_cast<T*>(p.cent);
-    const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-    for (int i = tid; i < gs * D; i += blockDim.x) {
-      const int hh = i / D, e = i % D;
-      cent[(((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D + e] = q[i];
-    }
-    write_slot_norms<T, D>(p, q, bi, gi, slot);
-  }
-  if (p.sparse_ids)
-    for (int i = tid; i < p.sparse_cap; i += blockDim.x)
-      p.sparse_ids[(int64_t)u * p.sparse_cap + i] =
-          i < Rn ? ldcg(rec + (p.use_rerank ? pos_at(i) : i)) : kEmpty;
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    if (dcu_here) atomicAdd(&p.sync[1 + bi], 1);
-    __threadfence();
-    const int prev = atomicAdd(lp.dcu_done, 1);
-    if (prev == p.U - 1) {
-      // every dcu(u) has read its cursor; every worker has read *total
-      while (ld_acq(lp.started) < (int)gridDim.x) __nanosleep(32);
-      __threadfence();
-      for (int b2 = 0; b2 < p.b; ++b2) {
-        const int hits = atomicExch(&p.sync[1 + b2], 0);
-        if (hits > 0) p.fifo[b2] = ldcg(p.fifo + b2) % p.C + 1;
-      }
-      if (p.k_new != nullptr) *p.total = t0 + 1;
-      __threadfence();
-    }
-  }
-}
-
-template <typename T, int D>
-__global__ void __launch_bounds__(kLW, 2) layer_kernel(DecodeParams p) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t bars[kMaxGroup];
-  __shared__ int s_task;
-  __shared__ int64_t s_t0;
-  const LayerPlan lp(p);
-  if (threadIdx.x == 0) {
-    s_t0 = *p.total;
-    for (int j = 0; j < kMaxGroup; ++j) bar_init(&bars[j], 1);
-    __threadfence();
-    atomicAdd(lp.started, 1);
-  }
-  __syncthreads();
-  const int64_t t0 = s_t0;
-  const bool appending = p.k_new != nullptr;
-  const int64_t total = t0 + (appending ? 1 : 0);
-  if (appending && blockIdx.x == 0) {
-    T* keys = static_cast<T*>(const_cast<void*>(p.keys));
-    T* vals = static_cast<T*>(const_cast<void*>(p.values));
-    const T* kn = static_cast<const T*>(p.k_new);
-    const T* vn = static_cast<const T*>(p.v_new);
-    for (int64_t i = threadIdx.x; i < (int64_t)p.U * D; i += blockDim.x) {
-      const int64_t uu = i / D, e = i % D;
-      keys[(uu * p.cap + t0) * D + e] = kn[i];
-      vals[(uu * p.cap + t0) * D + e] = vn[i];
-    }
-  }
-  uint32_t ph = 0;
-  while (true) {
-    if (threadIdx.x == 0) s_task = atomicAdd(lp.claim, 1);
-    __syncthreads();
-    const int task = s_task;
-    __syncthreads();
-    if (task >= lp.ntask) break;
-    if (task < lp.o_union) {
-      l_cos<T, D>(p, task, smem, bars, ph);
-      task_done(lp.cos_done + task / lp.cpu);
-    } else if (task < lp.o_static) {
-      const int u = task - lp.o_union;
-      wait_ge(lp.cos_done + u, lp.cpu);
-      l_union(p, u, total, smem);
-      task_done(lp.union_done + u);
-    } else if (task < lp.o_logit) {
-      const int st = task - lp.o_static;
-      l_static<T, D>(p, st, t0, total, smem, bars, ph);
-      task_done(lp.static_done + st / p.ns);
-    } else if (task < lp.o_att) {
-      const int x = task - lp.o_logit, u = x / kLParts;
-      wait_ge(lp.union_done + u, 1);
-      l_logit<T, D>(p, u, x % kLParts, smem);
-      task_done(lp.logit_done + u);
-    } else if (task < lp.o_dcu) {
-      const int u = task - lp.o_att;
-      wait_ge(lp.logit_done + u, kLParts);
-      wait_ge(lp.static_done + u, p.ns);
-      l_attend<T, D>(p, u, smem);
-      __syncthreads();
-    } else {
-      const int u = task - lp.o_dcu;
-      wait_ge(lp.logit_done + u, kLParts);
-      l_dcu<T, D>(p, u, t0, lp, smem);
-    }
-  }
-}
-
-template <typename T, int D>
-size_t layer_smem(const DecodeParams& p) {
-  constexpr int RB = D * int(sizeof(T));
-  constexpr int ST = static_tok<T>();
-  const int gs = p.gs, ns = p.ns;
-  const size_t cosb = (size_t)kScanRowsV2 * RB + (size_t)gs * RB + 8 * gs + 16 * kScanRowsV2;
-  const size_t stb = (size_t)2 * ST * RB + (size_t)gs * RB + 12 * (size_t)gs * ST + 16 * gs;
-  const int words = (int)((p.cap + 31) / 32);
-  const size_t unb = 512 + (size_t)p.c_prime * words * 4;
-  const int L = p.lmax;
-  const size_t red = (size_t)(kLW / 32) * gs * D * 4;
-  const size_t attb = align16(((size_t)L * 8 > red ? (size_t)L * 8 : red)) + align16(4 * (size_t)L) +
-                      align16(4 * (size_t)gs * kAttnChunk) + align16(16 * (size_t)ns * gs) +
-                      align16(4 * (size_t)ns * gs * D) + 1024 + align16(8 * (size_t)(gs * (ns + 1) + 64));
-  int np = next_pow2(L > 1 ? L : 1);
-  if (np < kLW) np = kLW;
-  const size_t dcub = (size_t)np * 8;
-  size_t m = cosb;
-  for (size_t x : {stb, unb, attb, dcub}) m = x > m ? x : m;
-  return m + 256;
-}
-
-// ------------------------------------------------------------------------
-// generic id-list attention: split partials + merge (sparse_attention API)
+// generic id-list attention (sparse_attention API): split-K partials + merge
 // ------------------------------------------------------------------------
 
 template <typename T, int D>
@@ -2518,40 +1484,9 @@ size_t scan_smem_bytes(const DecodeParams& p, int D) {
   return std::max(cosb, attb);
 }
 
-static int num_sms_dev() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
-}
-
-static int scan_variant() {   // CTKV_SCAN=3 selects the persistent scan3 (A/B testing)
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CTKV_SCAN");
-    v = (e && e[0] == '3') ? 3 : 2;
-  }
-  return v;
-}
 
 template <typename T, int D>
 static int launch_scan_t(const DecodeParams& p, int nblocks, cudaStream_t st) {
-  if (sizeof(T) == 2 && D <= 128 && p.gs <= 8 && scan_variant() == 3) {
-    // persistent warp-specialised scan: one CTA per SM streaming its tasks
-    const size_t sm3 = scan3_smem<T, D>();
-    auto k3 = scan3_kernel<T, D>;
-    static bool set3 = false;
-    if (!set3) {
-      cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
-      set3 = true;
-    }
-    const int grid = nblocks < num_sms_dev() ? nblocks : num_sms_dev();
-    if (grid > 0) k3<<<grid, kScan3Threads, sm3, st>>>(p);
-    return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
-  }
   const size_t sm = scan2_smem<T, D>(p.gs);
   auto k = scan2_kernel<T, D>;
   static size_t configured = 0;
@@ -2645,37 +1580,6 @@ int phase_timing(int on, unsigned long long* out, int n) {
   }
   return 0;
 }
-template <typename T, int D>
-static int launch_layer_t(const DecodeParams& p, cudaStream_t st) {
-  const size_t sm = layer_smem<T, D>(p);
-  if (sm > 220 * 1024) return CTKV_ECONFIG;
-  auto k = layer_kernel<T, D>;
-  static size_t configured = 0;
-  if (sm > configured) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    configured = sm;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kLW, sm);
-  if (per_sm < 1) return CTKV_ECONFIG;
-  const int grid = num_sms_dev() * (per_sm > 2 ? 2 : per_sm);
-  cudaMemsetAsync(p.ctr, 0, sizeof(int) * (3 + 4 * p.U), st);
-  k<<<grid, kLW, sm, st>>>(p);
-  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
-}
-
-int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
-  if (dtype != CTKV_BF16) return CTKV_ECONFIG;
-  switch (D) {
-    case 64: return launch_layer_t<__nv_bfloat16, 64>(p, st);
-    case 128: return launch_layer_t<__nv_bfloat16, 128>(p, st);
-  }
-  return CTKV_ESHAPE;
-}
-
-// Decode path for bf16 (A/B switch CTKV_DECODE): 6 = 4-CTA cluster chain
-// kernel + deferred tail (default), 2 = 2-CTA cluster unit kernel, 5 = wide
-// unit pipeline, 4 = persistent layer kernel.
 // v6 scan kernel (A/B switch CTKV_SCAN): 2 = scan2 (default), 4 = the
 // persistent scan4 (faster alone, but its 1-CTA-per-SM footprint overlaps
 // worse with the lanes' chain kernels: measured 1820 vs 2242 tok/s)
@@ -2721,7 +1625,7 @@ int decode_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("CTKV_DECODE");
-    v = (e && (e[0] == '5' || e[0] == '4' || e[0] == '2')) ? e[0] - '0' : 6;
+    v = (e && e[0] == '2') ? 2 : 6;
   }
   return v;
 }

@@ -60,17 +60,10 @@ struct DecodeParams {
   double* cval;     // [U][cos_blocks_per_unit][ncand] chunk top-C' cosines
   int32_t* cidx;    // [U][cos_blocks_per_unit][ncand] their centroid slots
   int ncand;        // min(C', centroids per cos chunk)
-  // layer kernel (v4) task-queue state
-  int* ctr;         // [3 + 4U] claim, started, dcu_done, cos/union/static/logit done per unit
+  // chain -> tail hand-off (per unit, by recall position)
   int32_t* recg;    // [U][lmax] recalled ids, first-occurrence order
-  int32_t* Lg;      // [U] recall lengths
-  uint64_t* keyg;   // [U][lmax] packed (score, position) rerank keys
-  // wide unit pipeline (v5, ctkv_unit_wide.cu)
-  int* uctr;        // [U][4] recall done, attend done, L, Rn (zeroed by the scan)
-  int32_t* wsel;    // [U][lmax] selected recall positions, ascending
-  float* apo;       // [U][8][gs][D] sparse attention partials
-  double* apl;      // [U][8][gs]
-  double* wmax;     // [U][gs] per-head max of the selected logits
+  uint64_t* keyg;   // [U][lmax] packed (~f32 score, position) rerank keys
+  int* uctr;        // [U][4]: [2] = L (recall length), [3] = R (sparse length)
   unsigned long long* tl;  // [4 kinds][start, end] globaltimer span of this step's kernels (debug)
   int wparts_b, wparts_c;
   // v6 chain: the scan's last cosine CTA of a unit writes its top-C' slots
@@ -104,13 +97,12 @@ int launch_unit2(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 size_t unit2_smem_bytes(const DecodeParams& p, int D);
 int static_tok_for(int dtype);
 int phase_timing(int on, unsigned long long* out, int n);
-int launch_layer(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int decode_variant();
 int kernel_timeline(int on);
 int scan_variant_v6();
-bool wide_supported(const DecodeParams& p, int dtype, int D);
-// what: 1 = recall + attend kernels, 2 = tail (DCU, sparse ids, cursor/total)
-int launch_wide(const DecodeParams& p, int dtype, int D, int what, cudaStream_t st);
+bool tail_supported(const DecodeParams& p, int dtype, int D);
+// the deferred tail of the fused step: order, DCU, sparse ids, cursor/total (ctkv_tail.cu)
+int launch_tail(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 bool chain_supported(const DecodeParams& p, int dtype, int D);
 // v6: the unit chain on a 4-CTA cluster per unit (ctkv_chain.cu)
 bool scan4_supported(const DecodeParams& p, int dtype, int D);

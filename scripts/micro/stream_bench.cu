@@ -75,8 +75,8 @@ __global__ void ldg_stream(const uint4* base, int64_t n, float* out) {
   if (acc == 1234.5f) out[0] = acc;
 }
 
-int main() {
-  const int64_t bytes = 174LL << 20;
+int main(int argc, char** argv) {
+  const int64_t bytes = (argc > 1 ? atoll(argv[1]) : 174LL) << 20;
   char* base;
   cudaMalloc(&base, bytes + (64 << 20));
   cudaMemset(base, 0, bytes);
@@ -114,8 +114,8 @@ int main() {
     const int64_t nt = bytes / kb;
     timeit([&] { tma_stream<<<sms, 288, st * kb>>>(base, nt, kb, st, out); }, name);
   }
-  for (int t : {256, 512, 1024}) {
-    for (int per : {1, 2, 4, 8}) {
+  for (int t : {256, 512}) {
+    for (int per : {1, 2, 4}) {
       char name[64];
       snprintf(name, sizeof name, "ldg %d thr x %d ctas/sm", t, per);
       timeit([&] { ldg_stream<<<sms * per, t>>>(reinterpret_cast<const uint4*>(base), bytes / 16, out); }, name);
