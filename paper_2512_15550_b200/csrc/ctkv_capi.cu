@@ -504,7 +504,10 @@ int ctkv_debug_timeline_rw(const ctkv_layout* L, int32_t capacity, int32_t rho, 
 }
 
 int ctkv_debug_scan_timeline(int32_t on, uint64_t* host_out, int32_t n) {
-  return ctkv::scan4_timeline(on, reinterpret_cast<unsigned long long*>(host_out), n);
+  // the persistent scan4 when selected (CTKV_SCAN=4), else scan2 ([cta][4])
+  if (ctkv::scan_variant_v6() == 4)
+    return ctkv::scan4_timeline(on, reinterpret_cast<unsigned long long*>(host_out), n);
+  return ctkv::scan2_timeline(on, reinterpret_cast<unsigned long long*>(host_out), n);
 }
 
 int ctkv_debug_phase_timing(int32_t on, uint64_t* host_out, int32_t n) {

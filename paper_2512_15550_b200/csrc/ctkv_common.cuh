@@ -114,6 +114,10 @@ __device__ __forceinline__ uint64_t okey64(double v) {
   uint64_t b = static_cast<uint64_t>(__double_as_longlong(v));
   return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
 }
+__device__ __forceinline__ double okey64_inv(uint64_t k) {
+  const uint64_t b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(b));
+}
 __device__ __forceinline__ uint32_t okey32(float v) {
   v = v + 0.0f;
   uint32_t b = __float_as_uint(v);

@@ -266,84 +266,96 @@ static __device__ void warp_top_slots(const DecodeParams& p, int u, int32_t* sel
 }
 
 // Top-C' slots of vals[0..C) (value desc, slot asc; ck/tensor_ops.py:121-141
-// on the group-max cosines of ck/retrieval.py:145-154) with the whole block:
-// every warp takes the top-C' of a contiguous chunk (lanes hold up to 8
-// values), then warp 0 takes the top-C' of the warps' candidates.  cand:
-// shared scratch of (blockDim/32) * c' (double, int) pairs.  c' <= 8.
-static __device__ __noinline__ void block_top_slots(const double* vals, int C, int cp, int32_t* out,
-                                                    double* cval, int* cidx) {
+// on the group-max cosines of ck/retrieval.py:145-154) with the whole block,
+// by sorting networks (no serial arg-max rounds, no lane-divergent code
+// around the shuffles; scripts/micro/topc_bench):
+//   1. each thread keeps a sorted top-K of its strided values (branch-free
+//      insertion);
+//   2. warps merge lane lists pairwise by butterflies: the top-K of two
+//      sorted K-lists is bitonic after one compare per position, then a
+//      log K half-cleaner sorts it;
+//   3. warp 0 merges the warps' lists the same way.
+// K = 4 or 8 >= c'; C <= 16 values per thread.  cval/cidx: shared scratch of
+// (blockDim/32) * K entries.
+struct TopEnt {
+  uint64_t k;
+  int i;
+};
+__device__ __forceinline__ bool top_better(const TopEnt& a, const TopEnt& b) {
+  return (a.k > b.k) | ((a.k == b.k) & (a.i < b.i));
+}
+__device__ __forceinline__ void top_cswap(TopEnt& a, TopEnt& b) {   // a := better
+  const bool sw = top_better(b, a);
+  const TopEnt t = a;
+  a = sw ? b : a;
+  b = sw ? t : b;
+}
+template <int K>
+__device__ __forceinline__ void top_merge_shfl(TopEnt (&t)[K], int o) {
+  TopEnt pt[K];
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    pt[r].k = __shfl_xor_sync(0xffffffffu, t[r].k, o);
+    pt[r].i = __shfl_xor_sync(0xffffffffu, t[r].i, o);
+  }
+#pragma unroll
+  for (int r = 0; r < K; ++r) t[r] = top_better(t[r], pt[K - 1 - r]) ? t[r] : pt[K - 1 - r];
+#pragma unroll
+  for (int st = K / 2; st > 0; st >>= 1)
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+      if ((r & st) == 0) top_cswap(t[r], t[r + st]);
+}
+template <int K>
+__device__ void block_top_k(const double* vals, int C, int cp, int32_t* out, double* cval,
+                            int* cidx) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int chunk = (C + nw - 1) / nw;
-  const int c0 = warp * chunk, c1 = min(C, c0 + chunk);
-  constexpr int KR = 8;
-  uint64_t rk[KR];
-  int ri[KR];
+  TopEnt t[K];
 #pragma unroll
-  for (int x = 0; x < KR; ++x) {
-    const int c = c0 + lane + 32 * x;
-    rk[x] = c < c1 ? okey64(__ldcg(vals + c)) : 0ull;
-    ri[x] = c < c1 ? c : INT32_MAX;
+  for (int r = 0; r < K; ++r) t[r] = TopEnt{0ull, INT32_MAX};
+  constexpr int PT = 16;
+  double v[PT];
+#pragma unroll
+  for (int x = 0; x < PT; ++x) {
+    const int c = threadIdx.x + x * (int)blockDim.x;
+    v[x] = c < C ? __ldcg(vals + c) : 0.0;
   }
-  uint64_t prev_key = ~0ull;
-  int prev_idx = -1;
-  for (int r = 0; r < cp; ++r) {
-    uint64_t bk = 0;
-    int bidx = INT32_MAX;
+  const int per = (C + (int)blockDim.x - 1) / (int)blockDim.x;   // uniform
 #pragma unroll
-    for (int x = 0; x < KR; ++x) {
-      const bool below = rk[x] < prev_key || (rk[x] == prev_key && ri[x] > prev_idx);
-      if (below && (rk[x] > bk || (rk[x] == bk && ri[x] < bidx))) { bk = rk[x]; bidx = ri[x]; }
-    }
-    for (int c = c0 + lane + 32 * KR; c < c1; c += 32) {   // chunks > 256 values only
-      const uint64_t k = okey64(__ldcg(vals + c));
-      const bool below = k < prev_key || (k == prev_key && c > prev_idx);
-      if (below && (k > bk || (k == bk && c < bidx))) { bk = k; bidx = c; }
-    }
+  for (int x = 0; x < PT; ++x) {
+    if (x >= per) break;
+    const int c = threadIdx.x + x * (int)blockDim.x;
+    TopEnt e{c < C ? okey64(v[x]) : 0ull, c < C ? c : INT32_MAX};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
-      if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
-    }
-    if (lane == 0) {
-      cval[warp * cp + r] = bidx == INT32_MAX ? -INFINITY : __ldcg(vals + bidx);
-      cidx[warp * cp + r] = bidx;
-    }
-    prev_key = bk;
-    prev_idx = bidx;
+    for (int r = 0; r < K; ++r) top_cswap(t[r], e);   // insertion: t stays sorted
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) top_merge_shfl<K>(t, o);
+  if (lane == 0)
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      cval[warp * K + r] = __longlong_as_double((long long)t[r].k);
+      cidx[warp * K + r] = t[r].i;
+    }
   __syncthreads();
   if (warp == 0) {
-    const int M = nw * cp;   // <= 32 * 8
-    uint64_t k8[KR];
-    int i8[KR];
 #pragma unroll
-    for (int x = 0; x < KR; ++x) {
-      const int m = lane + 32 * x;
-      k8[x] = m < M && cidx[m] != INT32_MAX ? okey64(cval[m]) : 0ull;
-      i8[x] = m < M ? cidx[m] : INT32_MAX;
-    }
-    prev_key = ~0ull;
-    prev_idx = -1;
-    for (int r = 0; r < cp; ++r) {
-      uint64_t bk = 0;
-      int bidx = INT32_MAX;
+    for (int r = 0; r < K; ++r)
+      t[r] = lane < nw ? TopEnt{(uint64_t)__double_as_longlong(cval[lane * K + r]), cidx[lane * K + r]}
+                       : TopEnt{0ull, INT32_MAX};
 #pragma unroll
-      for (int x = 0; x < KR; ++x) {
-        const bool below = k8[x] < prev_key || (k8[x] == prev_key && i8[x] > prev_idx);
-        if (below && (k8[x] > bk || (k8[x] == bk && i8[x] < bidx))) { bk = k8[x]; bidx = i8[x]; }
-      }
+    for (int o = 16; o > 0; o >>= 1) top_merge_shfl<K>(t, o);
+    if (lane == 0)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
-        const int i2 = __shfl_xor_sync(0xffffffffu, bidx, o);
-        if (k2 > bk || (k2 == bk && i2 < bidx)) { bk = k2; bidx = i2; }
-      }
-      if (lane == 0) out[r] = bidx;
-      prev_key = bk;
-      prev_idx = bidx;
-    }
+      for (int r = 0; r < K; ++r)
+        if (r < cp) out[r] = t[r].i;                 // compile-time index: t stays in registers
   }
+}
+
+static __device__ __noinline__ void block_top_slots(const double* vals, int C, int cp, int32_t* out,
+                                                    double* cval, int* cidx) {
+  if (cp <= 4) block_top_k<4>(vals, C, cp, out, cval, cidx);
+  else block_top_k<8>(vals, C, cp, out, cval, cidx);
 }
 
 }  // namespace ctkv

@@ -109,6 +109,7 @@ bool scan4_supported(const DecodeParams& p, int dtype, int D);
 // persistent warp-specialised streaming scan (ctkv_scan.cu; CTKV_SCAN=4)
 int launch_scan4(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int scan4_timeline(int on, unsigned long long* out, int n);
+int scan2_timeline(int on, unsigned long long* out, int n);
 int chain_phase_timing(int on, unsigned long long* out, int n);
 int launch_chain(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 int launch_centroid_norms(int dtype, int D, const void* cent, int64_t rows, float* out, cudaStream_t st);
