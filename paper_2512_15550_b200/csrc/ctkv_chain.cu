@@ -51,7 +51,7 @@ namespace ctkv {
 namespace cg = cooperative_groups;
 
 // per-CTA phase timestamps (globaltimer, ns), profiling only: [cta][mark]
-constexpr int kCPhaseCtas = 512, kCPhases = 12;
+constexpr int kCPhaseCtas = 512, kCPhases = 16;
 __device__ unsigned long long g_cphase[kCPhaseCtas][kCPhases];
 __device__ int g_cphase_on;
 __device__ __forceinline__ void cmark(int k) {
@@ -70,6 +70,15 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t dsmem_addr(const void* ptr, int rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(sa(ptr)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
 
 // f64 exp out of line: one copy of its ~200 instructions per kernel
 __device__ __noinline__ double dexp(double x) { return exp(x); }
@@ -328,52 +337,51 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   // ---- 2. own lists: first-occurrence survivors ---------------------------------
   // CTA r owns lists j = r, r+CL, ...  An entry of list j survives iff no list
   // j' < j holds it (np.unique(return_index) order, ck/retrieval.py:156-162),
-  // tested against a local bitmap that ORs lists 0..j-1 (re-read from L2; no
-  // cross-CTA traffic).  Loops stay compact: this phase runs once per kernel.
+  // tested against a local bitmap that ORs lists 0..j-1.  Lists 0..jmax are
+  // staged in area B by TMA bulk copies issued together (one L2/HBM round
+  // trip however many lists precede the owned one).
   const int nown = (p.c_prime - r + CL - 1) / CL;      // lists r, r + CL, ... < c'
-  int32_t* raw = reinterpret_cast<int32_t*>(S.keys);   // area B: [nown][rho] raw ids
+  const int jmax = r + CL * (nown - 1);                // last owned list
+  int32_t* stage = reinterpret_cast<int32_t*>(S.keys);   // area B: [jmax + 1][rho] raw ids
   const int per = (p.rho + kCT - 1) / kCT;             // entries per thread per list
-  constexpr int LU = 8;
   auto list_row = [&](int j) { return p.lists + ((int64_t)u * p.C + sel[j]) * p.rho; };
-  for (int sl = 0; sl < nown; ++sl) {   // own lists -> raw (range-checked)
-    const int32_t* row = list_row(r + CL * sl);
-    int32_t* dst = raw + sl * p.rho;
-    for (int i0 = tid; i0 < p.rho; i0 += kCT * LU) {
-      int v[LU];
-#pragma unroll
-      for (int x = 0; x < LU; ++x) v[x] = i0 + x * kCT < p.rho ? __ldg(row + i0 + x * kCT) : kEmpty;
-#pragma unroll
-      for (int x = 0; x < LU; ++x) {
-        int id = v[x];
-        if (id != kEmpty && (id < 0 || id >= total)) { set_flag(p.flags, kFlagIdRange); id = kEmpty; }
-        if (i0 + x * kCT < p.rho) dst[i0 + x * kCT] = id;
+  const bool bulk = (p.rho & 3) == 0 && (reinterpret_cast<uintptr_t>(p.lists) & 15) == 0;
+  __shared__ __align__(8) uint64_t lbar;
+  if (nown > 0) {
+    if (bulk) {
+      if (tid == 0) {
+        bar_init(&lbar, 1);
+        bar_expect(&lbar, (uint32_t)((jmax + 1) * p.rho * 4));
+        for (int j = 0; j <= jmax; ++j) bulk_g2s(stage + j * p.rho, list_row(j), p.rho * 4, &lbar);
       }
+    } else {
+      for (int i = tid; i < (jmax + 1) * p.rho; i += kCT)
+        stage[i] = __ldg(list_row(i / p.rho) + i % p.rho);
     }
   }
   for (int i = tid; i < p.bitmap_words; i += kCT) S.bm[i] = 0u;
+  __syncthreads();   // barrier initialised, bitmap cleared (and the plain-load stage written)
+  if (nown > 0 && bulk) bar_wait(&lbar, 0);
   int jdone = 0;                                        // lists already in the bitmap
   for (int sl = 0; sl < nown; ++sl) {
     const int j = r + CL * sl;
-    __syncthreads();                                    // bitmap cleared / previous tests done
+    if (sl > 0) __syncthreads();                        // previous tests done
     for (; jdone < j; ++jdone) {                        // OR lists jdone .. j-1 into the bitmap
-      const int32_t* row = list_row(jdone);
-      for (int i0 = tid; i0 < p.rho; i0 += kCT * LU) {
-        int v[LU];
-#pragma unroll
-        for (int x = 0; x < LU; ++x) v[x] = i0 + x * kCT < p.rho ? __ldg(row + i0 + x * kCT) : kEmpty;
-#pragma unroll
-        for (int x = 0; x < LU; ++x)
-          if (v[x] >= 0 && v[x] < total) atomicOr(&S.bm[v[x] >> 5], 1u << (v[x] & 31));
+      const int32_t* row = stage + jdone * p.rho;
+      for (int i = tid; i < p.rho; i += kCT) {
+        const int v = row[i];
+        if (v >= 0 && v < total) atomicOr(&S.bm[v >> 5], 1u << (v & 31));
       }
     }
     __syncthreads();
-    const int32_t* rl = raw + sl * p.rho;
+    const int32_t* rl = stage + j * p.rho;
     unsigned keepm = 0;
     int cnt = 0;
 #pragma unroll 4
     for (int e = 0; e < per; ++e) {
       const int i = tid * per + e;
-      const int id = i < p.rho ? rl[i] : kEmpty;
+      int id = i < p.rho ? rl[i] : kEmpty;
+      if (id != kEmpty && (id < 0 || id >= total)) { set_flag(p.flags, kFlagIdRange); id = kEmpty; }
       const bool keep = id != kEmpty && !((S.bm[id >> 5] >> (id & 31)) & 1u);
       keepm |= (keep ? 1u : 0u) << e;
       cnt += keep;
@@ -420,6 +428,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     const int sub = lane % LPR, rw = lane / LPR;
     constexpr int RPW = 32 / LPR;          // rows per warp pass
     const uint4* q4 = reinterpret_cast<const uint4*>(qs);
+    // every CTA's area B is free after barrier #2: the keys go to all of them
+    uint32_t rkeys[CL > 1 ? CL - 1 : 1];   // shared::cluster addresses
+#pragma unroll
+    for (int o = 0; o < CL - 1; ++o) rkeys[o] = dsmem_addr(S.keys, (r + 1 + o) % CL);
     for (int b0 = warp * RPW; b0 < n_sl; b0 += kCW * RPW * kKUn) {
       uint4 raw[kKUn][CPL];
 #pragma unroll
@@ -434,27 +446,56 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
           for (int c = 0; c < CPL; ++c) raw[x][c] = make_uint4(0, 0, 0, 0);
         }
       }
+      if (b0 == warp * RPW) cmark(12);   // first round issued
 #pragma unroll
       for (int x = 0; x < kKUn; ++x) {
         const int t = b0 + x * kCW * RPW + rw;
-        double gmax = -INFINITY;
+        if (x == 1 && b0 == warp * RPW) cmark(13);   // first row of the first round done
+        double a[GS];
 #pragma unroll
         for (int hh = 0; hh < GS; ++hh) {
-          double a = 0.0;
+          a[hh] = (double)bf16x8_dot(q4[hh * CH + sub], raw[x][0], 0.f);
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) a += (double)bf16x8_dot(q4[hh * CH + c * LPR + sub], raw[x][c], 0.f);
-#pragma unroll
-          for (int o = 1; o < LPR; o <<= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-          a *= scale;
-          if (sub == 0 && t < n_sl) lgg[(int64_t)hh * p.lmax + lo + t] = a;
-          gmax = fmax(gmax, a);
+          for (int c = 1; c < CPL; ++c) a[hh] += (double)bf16x8_dot(q4[hh * CH + c * LPR + sub], raw[x][c], 0.f);
         }
+        // transposed reduction over the row's LPR lanes: every level halves
+        // the heads a lane carries (it keeps one half and ships the other),
+        // so a row costs GS - 1 + log2(LPR) double shuffles, not GS * log2(LPR)
+        int hh = 0;
+        int dup = 0;   // lane bits of the levels that only summed (same head)
+#pragma unroll
+        for (int lv = 0, s = LPR / 2; s > 0; ++lv, s >>= 1) {
+          const int H = GS >> lv;   // heads carried into this level
+          if (H > 1) {
+            const bool hi = (sub & s) != 0;
+#pragma unroll
+            for (int i = 0; i < H / 2; ++i) {
+              const double keep = hi ? a[i + H / 2] : a[i];
+              const double send = hi ? a[i] : a[i + H / 2];
+              a[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+            }
+            hh += hi ? H / 2 : 0;
+          } else {
+            a[0] += __shfl_xor_sync(0xffffffffu, a[0], s);
+            dup |= s;
+          }
+        }
+        const double lg = a[0] * scale;
+        if ((sub & dup) == 0 && t < n_sl) lgg[(int64_t)hh * p.lmax + lo + t] = lg;
+        // group max over the heads (max commutes with the f32 rounding)
+        float gm = (float)lg;
+#pragma unroll
+        for (int lv = 0, s = LPR / 2; s > 0; ++lv, s >>= 1)
+          if ((GS >> lv) > 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, s));
         if (sub == 0 && t < n_sl) {
-          const uint32_t k32 = ~okey32((float)gmax);
+          const uint32_t k32 = ~okey32(gm);
           S.keys[lo + t] = k32;
+#pragma unroll
+          for (int o = 0; o < CL - 1; ++o) st_cluster_u32(rkeys[o] + 4u * (uint32_t)(lo + t), k32);
           kg[lo + t] = ((uint64_t)k32 << 32) | (uint32_t)(lo + t);
         }
       }
+      if (b0 == warp * RPW) cmark(14);   // first round done
     }
   }
   cmark(5);
@@ -472,14 +513,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     cp_async_commit();
   }
 
-  // ---- 4. top-rho' boundary over all L keys --------------------------------------
-  for (int pos = tid; pos < L; pos += kCT) {
-    if (pos >= lo && pos < hi) continue;
-    int o = 0;
-    while ((int)((int64_t)(o + 1) * L / CL) <= pos) ++o;
-    S.keys[pos] = cl.map_shared_rank(S.keys, o)[pos];
-  }
-  __syncthreads();
+  // ---- 4. top-rho' boundary over all L keys (pushed here before barrier #3) ----
   cmark(7);
   const int Rn = L > 0 ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
   uint32_t vk = 0xffffffffu;

@@ -42,10 +42,10 @@ for t in range(4):
         torch.cuda.synchronize()
         eng._launch(L0, 2 | 8)
         torch.cuda.synchronize()
-        n = 512 * 12
+        n = 512 * 16
         buf = (ctypes.c_uint64 * n)()
         lib.ctkv_debug_phase_timing(0, buf, n)
-        a = np.frombuffer(buf, dtype=np.uint64).reshape(512, 12).astype(np.int64)
+        a = np.frombuffer(buf, dtype=np.uint64).reshape(512, 16).astype(np.int64)
         nct = eng.bl * g * 4
         a = a[:nct]
         t0 = a[:, 0].min()
@@ -59,6 +59,11 @@ for t in range(4):
         for rk in range(4):
             rr = a[rk::4]
             print(f"   rank {rk}:", "  ".join(f"{np.median(rr[:, kk] - rr[:, kk - 1]) / 1e3:10.2f}" for kk in range(1, 12)))
+        sub = [(4, 12, "K round 1 issued"), (12, 13, "first K row done"), (13, 14, "rest of round 1"),
+               (14, 5, "later rounds")]
+        for a0, a1, nm in sub:
+            dd = (a[:, a1] - a[:, a0]) / 1e3
+            print(f"     logits: {nm:18s} median {np.median(dd):7.2f} us")
         r0 = a[0::4]
         print(f"  end-to-end (rank 0, mark 11 - mark 0): median {np.median(r0[:, 11] - r0[:, 0]) / 1e3:.2f} us")
         print(f"  kernel span: {(a[:, 11].max() - t0) / 1e3:.2f} us")

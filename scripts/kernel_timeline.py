@@ -96,10 +96,10 @@ for t in range(6):
         print(f"  gap scan->chain median {np.median(g1):.1f} us; chain->next scan median {np.median(g2):.1f} us")
         sk = [(r[2][7] - r[2][2]) / 1e3 for r in rows]
         print(f"  chain CTA start skew (last start - first start): median {np.median(sk):.1f} us, p90 {np.percentile(sk, 90):.1f}")
-n = 512 * 12
+n = 512 * 16
 pb = (ctypes.c_uint64 * n)()
 lib.ctkv_debug_phase_timing(0, pb, n)
-a = np.frombuffer(pb, dtype=np.uint64).reshape(512, 12).astype(np.int64)[:eng.bl * g * 4]
+a = np.frombuffer(pb, dtype=np.uint64).reshape(512, 16).astype(np.int64)[:eng.bl * g * 4]
 names = ["start", "q + slots", "lists+survivors", "sync2", "pull ids", "logits", "sync3",
          "pull keys", "threshold", "compaction", "attention", "sync4+merge"]
 print("  chain phases under load (last writer per CTA slot), median us:")
