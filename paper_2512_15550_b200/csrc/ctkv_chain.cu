@@ -420,7 +420,103 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   cmark(4);
 
   // ---- 3. rerank logits of the slice (K rows gathered into registers) ----------
-  {
+  if (!p.chain_simt) {
+    // Tensor-core form: per warp, 16-row blocks of the slice as the A operand
+    // of mma.m16n8k16 (bf16 products exact, f32 sum per 16-element k-step,
+    // f64 across the k-steps), the gs query heads as the B columns.  The
+    // order of near-equal scores can differ from the SIMT form's (both lie
+    // well inside the north_star's 1e-6 tie window; tests/test_parity_gpu.py).  A lane
+    // loads 16 B pieces of rows g and g+8; the dot product is invariant to
+    // a common permutation of k, so each piece is used as the k-step
+    // fragment as loaded and q is permuted the same way.
+    const double scale = 1.0 / sqrt((double)D);
+    const T* keys_g = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
+    constexpr int KS2 = D / 32;            // 32-element k pairs per row
+    constexpr int NB = 2;                  // 16-row blocks in flight per warp
+    const int g8 = lane >> 2, t4 = lane & 3;
+    uint4 qf[KS2];
+#pragma unroll
+    for (int s2 = 0; s2 < KS2; ++s2)
+      qf[s2] = g8 < GS ? *reinterpret_cast<const uint4*>(qs + g8 * D + s2 * 32 + 8 * t4) : make_uint4(0, 0, 0, 0);
+    uint32_t rkeys[CL > 1 ? CL - 1 : 1];   // shared::cluster addresses of the other CTAs' keys
+#pragma unroll
+    for (int o = 0; o < CL - 1; ++o) rkeys[o] = dsmem_addr(S.keys, (r + 1 + o) % CL);
+    const int h0 = 2 * t4;                 // this lane's D columns: heads h0, h0 + 1
+    // rows past the first round: into L2 now, so the second round is an L2 hit
+    constexpr int R1 = kCW * NB * 16;
+    for (int i = tid; i < 2 * (n_sl - R1); i += kCT)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(keys_g + (int64_t)S.sid[R1 + (i >> 1)] * D + (i & 1) * (D / 2)));
+    for (int bk0 = warp * NB; bk0 * 16 < n_sl; bk0 += kCW * NB) {
+      uint4 ra[NB][KS2], rb[NB][KS2];
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        const int r0 = (bk0 + nb) * 16 + g8, r1 = r0 + 8;
+        const T* k0 = keys_g + (int64_t)(r0 < n_sl ? S.sid[r0] : 0) * D + 8 * t4;
+        const T* k1 = keys_g + (int64_t)(r1 < n_sl ? S.sid[r1] : 0) * D + 8 * t4;
+#pragma unroll
+        for (int s2 = 0; s2 < KS2; ++s2) {
+          ra[nb][s2] = r0 < n_sl ? ldg16(reinterpret_cast<const uint4*>(k0 + s2 * 32)) : make_uint4(0, 0, 0, 0);
+          rb[nb][s2] = r1 < n_sl ? ldg16(reinterpret_cast<const uint4*>(k1 + s2 * 32)) : make_uint4(0, 0, 0, 0);
+        }
+      }
+      if (bk0 == warp * NB) cmark(12);
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb) {
+        if (nb == 1 && bk0 == warp * NB) cmark(13);
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int s2 = 0; s2 < KS2; ++s2) {
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {   // 16-element k-steps: (.x .y) then (.z .w) of the pieces
+            const uint32_t a0 = hf ? ra[nb][s2].z : ra[nb][s2].x, a1 = hf ? rb[nb][s2].z : rb[nb][s2].x;
+            const uint32_t a2 = hf ? ra[nb][s2].w : ra[nb][s2].y, a3 = hf ? rb[nb][s2].w : rb[nb][s2].y;
+            const uint32_t b0 = hf ? qf[s2].z : qf[s2].x, b1 = hf ? qf[s2].w : qf[s2].y;
+            float d0, d1, d2, d3;
+            asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                "{%10,%10,%10,%10};"
+                : "=f"(d0), "=f"(d1), "=f"(d2), "=f"(d3)
+                : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(0.f));
+            acc[0] += (double)d0;
+            acc[1] += (double)d1;
+            acc[2] += (double)d2;
+            acc[3] += (double)d3;
+          }
+        }
+        // acc[0..1]: row r0, heads h0, h0+1; acc[2..3]: row r1
+        const int r0 = (bk0 + nb) * 16 + g8, r1 = r0 + 8;
+        float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int hh = h0 + e;
+          if (hh < GS) {
+            const double l0 = acc[e] * scale, l1 = acc[2 + e] * scale;
+            if (r0 < n_sl) lgg[(int64_t)hh * p.lmax + lo + r0] = l0;
+            if (r1 < n_sl) lgg[(int64_t)hh * p.lmax + lo + r1] = l1;
+            m0 = fmaxf(m0, (float)l0);
+            m1 = fmaxf(m1, (float)l1);
+          }
+        }
+        // group max over the row's heads (lanes t4 = 0..3; max commutes with the f32 rounding)
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+          m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+          m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+        }
+        if (t4 < 2) {
+          const int rr = t4 == 0 ? r0 : r1;
+          const float gm = t4 == 0 ? m0 : m1;
+          if (rr < n_sl) {
+            const uint32_t k32 = ~okey32(gm);
+            S.keys[lo + rr] = k32;
+#pragma unroll
+            for (int o = 0; o < CL - 1; ++o) st_cluster_u32(rkeys[o] + 4u * (uint32_t)(lo + rr), k32);
+            kg[lo + rr] = ((uint64_t)k32 << 32) | (uint32_t)(lo + rr);
+          }
+        }
+      }
+      if (bk0 == warp * NB) cmark(14);
+    }
+  } else {
     const double scale = 1.0 / sqrt((double)D);
     const T* keys_g = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
     constexpr int LPR = 8;                 // lanes per row
@@ -768,8 +864,19 @@ static int chain_cl() {   // CTKV_CHAIN_CL=2|8 selects 2- or 8-CTA clusters (A/B
   return v;
 }
 
+static int chain_simt() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("CTKV_CHAIN_SIMT");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v;
+}
+
 template <typename T, int D, int CL, int GS>
-static int launch_chain_t(const DecodeParams& p, cudaStream_t st) {
+static int launch_chain_t(const DecodeParams& p0, cudaStream_t st) {
+  DecodeParams p = p0;
+  p.chain_simt = chain_simt();
   const size_t sm = chain_layout(p, D, CL, nullptr, nullptr);
   auto k = chain_kernel<T, D, CL, GS>;
   static size_t configured = 0;

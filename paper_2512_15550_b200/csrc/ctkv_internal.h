@@ -70,6 +70,7 @@ struct DecodeParams {
   int32_t* selg;    // [U][c'] top-C' slots (ties -> smaller slot)
   int* selctr;      // [U] cosine-chunk completion counters (reset by the last CTA)
   int sel_in_chain; // 1: the chain kernel selects top-C' from gcos itself (scan4)
+  int chain_simt;   // 1: SIMT rerank logits in the chain (CTKV_CHAIN_SIMT=1 A/B), else mma.sync
   // staged io
   const int32_t* rec_in;
   const int32_t* len_in;
