@@ -1628,18 +1628,22 @@ int kernel_timeline(int on) {   // host switch; on < 0 queries
   return v;
 }
 
+// kPrioLow = the scan, kPrioMid = the tail, kPrioHigh = the chain by default;
+// CTKV_PRIO=0 turns priorities off, CTKV_PRIO=xyz (x, y, z in h/m/l) sets the
+// scan's, chain's and tail's levels for A/B runs
 int launch_priority(LaunchPrio pr) {
   static int lo = 1, hi = 0, on = -1;
+  static char lvl[3] = {'l', 'm', 'h'};   // indexed by LaunchPrio
   if (on < 0) {
     const char* e = getenv("CTKV_PRIO");
     on = (e && e[0] == '0') ? 0 : 1;
+    if (e && e[0] && e[1] && e[2]) { lvl[kPrioLow] = e[0]; lvl[kPrioHigh] = e[1]; lvl[kPrioMid] = e[2]; }
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) { lo = 0; hi = 0; }
   }
   if (!on) return lo;   // default (lowest) priority everywhere
   // numerically lower = higher priority; hi..lo
-  if (pr == kPrioHigh) return hi;
-  if (pr == kPrioMid) return (lo + hi) / 2;
-  return lo;
+  const char c = lvl[pr];
+  return c == 'h' ? hi : c == 'm' ? (lo + hi) / 2 : lo;
 }
 
 bool pdl_enabled() {
