@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--build-mode", type=int, default=1, help="0 exact f64, 1 fast")
-    ap.add_argument("--lanes", type=int, default=8,
+    ap.add_argument("--lanes", type=int, default=4,
                     help="micro-batch lanes per GPU (sequence groups on their own streams)")
     return ap.parse_args()
 
