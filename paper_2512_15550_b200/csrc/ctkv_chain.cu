@@ -53,9 +53,8 @@ namespace cg = cooperative_groups;
 // per-CTA phase timestamps (globaltimer, ns), profiling only: [cta][mark]
 constexpr int kCPhaseCtas = 512, kCPhases = 16;
 __device__ unsigned long long g_cphase[kCPhaseCtas][kCPhases];
-__device__ int g_cphase_on;
-__device__ __forceinline__ void cmark(int k) {
-  if (g_cphase_on && threadIdx.x == 0 && blockIdx.x < kCPhaseCtas) {
+__device__ __forceinline__ void cmark(const DecodeParams& p, int k) {
+  if ((p.dbg & 2) && threadIdx.x == 0 && blockIdx.x < kCPhaseCtas) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_cphase[blockIdx.x][k] = t;
@@ -319,7 +318,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   __shared__ int s_state[4];
   __shared__ double hm[GS], hl[GS], hnew[GS], hresc[GS];
 
-  cmark(0);
+  cmark(p, 0);
   ktl_mark(p.tl, 1, false);
   ktl_mark(p.tl, 3, true);   // the last CTA start (slot 3 end = max start)
   pdl_wait();      // the scan's outputs (gcos / slots, static partials) are complete
@@ -332,7 +331,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     sel[tid] = __ldcg(p.selg + (int64_t)u * p.c_prime + tid);
   }
   __syncthreads();
-  cmark(1);
+  cmark(p, 1);
 
   // ---- 2. own lists: first-occurrence survivors ---------------------------------
   // CTA r owns lists j = r, r+CL, ...  An entry of list j survives iff no list
@@ -393,9 +392,9 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
       if ((keepm >> e) & 1u) S.recl[sl * p.rho + o++] = rl[tid * per + e];
     if (tid < CL) cl.map_shared_rank(lcnt, tid)[j] = tot;
   }
-  cmark(2);
+  cmark(p, 2);
   cl.sync();   // #2: survivor counts everywhere, survivors compacted
-  cmark(3);
+  cmark(p, 3);
 
   if (tid == 0) {
     sbase[0] = 0;
@@ -417,7 +416,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     recg[pos] = id;
   }
   __syncthreads();
-  cmark(4);
+  cmark(p, 4);
 
   // ---- 3. rerank logits of the slice (K rows gathered into registers) ----------
   if (!p.chain_simt) {
@@ -459,10 +458,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
           rb[nb][s2] = r1 < n_sl ? ldg16(reinterpret_cast<const uint4*>(k1 + s2 * 32)) : make_uint4(0, 0, 0, 0);
         }
       }
-      if (bk0 == warp * NB) cmark(12);
+      if (bk0 == warp * NB) cmark(p, 12);
 #pragma unroll
       for (int nb = 0; nb < NB; ++nb) {
-        if (nb == 1 && bk0 == warp * NB) cmark(13);
+        if (nb == 1 && bk0 == warp * NB) cmark(p, 13);
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int s2 = 0; s2 < KS2; ++s2) {
@@ -514,7 +513,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
           }
         }
       }
-      if (bk0 == warp * NB) cmark(14);
+      if (bk0 == warp * NB) cmark(p, 14);
     }
   } else {
     const double scale = 1.0 / sqrt((double)D);
@@ -542,11 +541,11 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
           for (int c = 0; c < CPL; ++c) raw[x][c] = make_uint4(0, 0, 0, 0);
         }
       }
-      if (b0 == warp * RPW) cmark(12);   // first round issued
+      if (b0 == warp * RPW) cmark(p, 12);   // first round issued
 #pragma unroll
       for (int x = 0; x < kKUn; ++x) {
         const int t = b0 + x * kCW * RPW + rw;
-        if (x == 1 && b0 == warp * RPW) cmark(13);   // first row of the first round done
+        if (x == 1 && b0 == warp * RPW) cmark(p, 13);   // first row of the first round done
         double a[GS];
 #pragma unroll
         for (int hh = 0; hh < GS; ++hh) {
@@ -591,12 +590,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
           kg[lo + t] = ((uint64_t)k32 << 32) | (uint32_t)(lo + t);
         }
       }
-      if (b0 == warp * RPW) cmark(14);   // first round done
+      if (b0 == warp * RPW) cmark(p, 14);   // first round done
     }
   }
-  cmark(5);
+  cmark(p, 5);
   cl.sync();   // #3: every slice's keys are complete (and its logits/ids in L2)
-  cmark(6);
+  cmark(p, 6);
 
   // CTA 0: prefetch the static partials into area A (its lists are dead)
   if (r == 0) {
@@ -610,14 +609,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   }
 
   // ---- 4. top-rho' boundary over all L keys (pushed here before barrier #3) ----
-  cmark(7);
+  cmark(p, 7);
   const int Rn = L > 0 ? (p.use_rerank ? min(p.rho_prime, L) : L) : 0;
   uint32_t vk = 0xffffffffu;
   int vpos = L;
   if (Rn > 0 && Rn < L)
     chain_select(S.keys, L, Rn, S.hist, reinterpret_cast<uint64_t*>(S.spos), s_state,
                  reinterpret_cast<uint32_t*>(S.scratch), &vk, &vpos);
-  cmark(8);
+  cmark(p, 8);
   // this CTA's share of the selected positions: ranks [Rn*r/CL, Rn*(r+1)/CL)
   // in position order (ordered compaction)
   const int rlo = (int)((int64_t)Rn * r / CL), rhi = (int)((int64_t)Rn * (r + 1) / CL);
@@ -649,7 +648,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   // its CTAs stage their centroid rows while this chain attends and merges
   pdl_trigger();
   const int nmy = rhi - rlo;
-  cmark(9);
+  cmark(p, 9);
 
   // ---- 5. attention over this CTA's selected tokens (online softmax) ------------
   constexpr int VL = CH;                     // lanes per V row (one 16-byte chunk each)
@@ -775,7 +774,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     cpml0[r * gs + tid] = nmy > 0 ? hm[tid] : -INFINITY;
     cpml0[CL * gs + r * gs + tid] = nmy > 0 ? hl[tid] : 0.0;
   }
-  cmark(10);
+  cmark(p, 10);
   cl.sync();   // #4: all sparse partials are in CTA 0
   if (r != 0) {
     ktl_mark(p.tl, 1, true);
@@ -846,7 +845,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   }
   if (p.selected)
     for (int k2 = tid; k2 < p.c_prime; k2 += kCT) p.selected[(int64_t)u * p.c_prime + k2] = sel[k2];
-  cmark(11);
+  cmark(p, 11);
   __syncthreads();
   ktl_mark(p.tl, 1, true);
 }
@@ -877,6 +876,7 @@ template <typename T, int D, int CL, int GS>
 static int launch_chain_t(const DecodeParams& p0, cudaStream_t st) {
   DecodeParams p = p0;
   p.chain_simt = chain_simt();
+  p.dbg = g_host_dbg;
   const size_t sm = chain_layout(p, D, CL, nullptr, nullptr);
   auto k = chain_kernel<T, D, CL, GS>;
   static size_t configured = 0;
@@ -895,7 +895,7 @@ int chain_phase_timing(int on, unsigned long long* out, int n) {
     if (cudaMemcpyFromSymbol(out, g_cphase, sizeof(unsigned long long) * m) != cudaSuccess)
       return CTKV_ECUDA;
   }
-  if (on >= 0 && cudaMemcpyToSymbol(g_cphase_on, &on, sizeof(int)) != cudaSuccess) return CTKV_ECUDA;
+  if (on >= 0) set_host_dbg(2, on);
   return CTKV_OK;
 }
 

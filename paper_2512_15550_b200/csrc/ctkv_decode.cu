@@ -43,12 +43,12 @@ namespace ctkv {
 constexpr int kScanRowsV2 = 256;   // threads (and centroid rows) per v2 scan CTA
 
 // per-CTA scan2 timeline (globaltimer ns), profiling only: [cta][0 start,
-// 1 first rows landed, 2 compute done, 3 end]; on while g_s2tl_on != 0
+// 1 first rows landed, 2 compute done, 3 end]; on while DecodeParams::dbg & 1
 constexpr int kS2TlCtas = 4096;
 __device__ unsigned long long g_s2tl[kS2TlCtas][8];
-__device__ int g_s2tl_on;
-__device__ __forceinline__ void s2mark(int k) {
-  if (g_s2tl_on && threadIdx.x == 0 && blockIdx.x < kS2TlCtas) {
+int g_host_dbg = 0;
+__device__ __forceinline__ void s2mark(const DecodeParams& p, int k) {
+  if ((p.dbg & 1) && threadIdx.x == 0 && blockIdx.x < kS2TlCtas) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_s2tl[blockIdx.x][k] = t;
@@ -302,7 +302,7 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
     const int j = r / CC, c = r % CC;
     if (c >= nc) continue;
     bar_wait(&bars[j], 0);
-    if (r == 0) s2mark(1);
+    if (r == 0) s2mark(p, 1);
     double dot, nrm;
     double cn;
     if (p.cnorm != nullptr) {
@@ -334,20 +334,20 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
   if (p.selg != nullptr) {
     __shared__ int s_last;
     __syncthreads();
-    s2mark(4);
+    s2mark(p, 4);
     if (threadIdx.x == 0) {
       __threadfence();
       s_last = atomicAdd(&p.selctr[u], 1) == cpu - 1;
     }
     __syncthreads();
-    s2mark(5);
+    s2mark(p, 5);
     if (s_last) {
       __threadfence();
-      s2mark(6);
+      s2mark(p, 6);
       block_top_slots(p.gcos + (int64_t)u * p.C, p.C, p.c_prime, p.selg + (int64_t)u * p.c_prime,
                       cosv, reinterpret_cast<int*>(cosv + 64));
       if (threadIdx.x == 0) p.selctr[u] = 0;
-      s2mark(7);
+      s2mark(p, 7);
     }
     return;
   }
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
   __shared__ uint64_t bars[kMaxGroup];
   pdl_trigger();   // the chain kernel may launch once every scan CTA is resident
   ktl_mark(p.tl, 0, false);
-  s2mark(0);
+  s2mark(p, 0);
   const int64_t t0 = p.total ? *p.total : p.id_bound;
   const bool appending = p.k_new != nullptr;
   const int64_t total = t0 + (appending ? 1 : 0);
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
     cos_task<T, D>(p, blockIdx.x, smem, bars);
   else
     static_task<T, D>(p, blockIdx.x - ncos, t0, total, smem, bars);
-  s2mark(2);
+  s2mark(p, 2);
   if (appending && blockIdx.x == 0) {
     T* keys = static_cast<T*>(const_cast<void*>(p.keys));
     T* vals = static_cast<T*>(const_cast<void*>(p.values));
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
   }
   __syncthreads();
   ktl_mark(p.tl, 0, true);
-  s2mark(3);
+  s2mark(p, 3);
 }
 
 int scan2_timeline(int on, unsigned long long* out, int n) {
@@ -535,7 +535,7 @@ int scan2_timeline(int on, unsigned long long* out, int n) {
     const int m = n < kS2TlCtas * 8 ? n : kS2TlCtas * 8;
     if (cudaMemcpyFromSymbol(out, g_s2tl, sizeof(unsigned long long) * m) != cudaSuccess) return CTKV_ECUDA;
   }
-  if (on >= 0 && cudaMemcpyToSymbol(g_s2tl_on, &on, sizeof(int)) != cudaSuccess) return CTKV_ECUDA;
+  if (on >= 0) set_host_dbg(1, on);
   return CTKV_OK;
 }
 
@@ -1516,7 +1516,9 @@ size_t scan_smem_bytes(const DecodeParams& p, int D) {
 
 
 template <typename T, int D>
-static int launch_scan_t(const DecodeParams& p, int nblocks, cudaStream_t st) {
+static int launch_scan_t(const DecodeParams& p0, int nblocks, cudaStream_t st) {
+  DecodeParams p = p0;
+  p.dbg = g_host_dbg;
   const size_t sm = scan2_smem<T, D>(p.gs);
   auto k = scan2_kernel<T, D>;
   static size_t configured = 0;

@@ -70,6 +70,8 @@ struct DecodeParams {
   int32_t* selg;    // [U][c'] top-C' slots (ties -> smaller slot)
   int* selctr;      // [U] cosine-chunk completion counters (reset by the last CTA)
   int sel_in_chain; // 1: the chain kernel selects top-C' from gcos itself (scan4)
+  int dbg;          // debug timestamp marks (host_dbg bits: 1 scan2, 2 chain, 4 scan4): a kernel
+                    // parameter, so marks that are off cost no global load
   int chain_simt;   // 1: SIMT rerank logits in the chain (CTKV_CHAIN_SIMT=1 A/B), else mma.sync
   // staged io
   const int32_t* rec_in;
@@ -101,6 +103,8 @@ int phase_timing(int on, unsigned long long* out, int n);
 int decode_variant();
 int kernel_timeline(int on);
 int scan_variant_v6();
+extern int g_host_dbg;   // debug mark bits the launchers copy into DecodeParams::dbg
+inline void set_host_dbg(int bit, int on) { g_host_dbg = on ? (g_host_dbg | bit) : (g_host_dbg & ~bit); }
 bool tail_supported(const DecodeParams& p, int dtype, int D);
 // the deferred tail of the fused step: order, DCU, sparse ids, cursor/total (ctkv_tail.cu)
 int launch_tail(const DecodeParams& p, int dtype, int D, cudaStream_t st);

@@ -35,7 +35,6 @@ namespace ctkv {
 // per-CTA task timeline (globaltimer, ns), profiling only
 constexpr int kS4TlCtas = 160, kS4TlSlots = 64;
 __device__ unsigned long long g_s4tl[kS4TlCtas][kS4TlSlots];
-__device__ int g_s4tl_on;
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -280,7 +279,7 @@ __global__ void __launch_bounds__(kS4Threads, 1) scan4_kernel(DecodeParams p) {
   const int ntasks = ncos + p.U * p.ns;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* scratch = smem + (size_t)kS4Stages * kS4Stage;
-  if (g_s4tl_on && threadIdx.x == 0 && blockIdx.x < kS4TlCtas) g_s4tl[blockIdx.x][0] = gtimer();
+  if ((p.dbg & 4) && threadIdx.x == 0 && blockIdx.x < kS4TlCtas) g_s4tl[blockIdx.x][0] = gtimer();
   if (threadIdx.x == 0) {
     for (int s = 0; s < kS4Stages; ++s) {
       bar_init(&full[s], 1);                // producer lane 0 (+tx)
@@ -334,7 +333,7 @@ __global__ void __launch_bounds__(kS4Threads, 1) scan4_kernel(DecodeParams p) {
       const unsigned char* st = smem + (size_t)stage * kS4Stage;
       const S4Hdr* hdr = reinterpret_cast<const S4Hdr*>(st + kS4Data + kS4Q + kS4Cn);
       const int task = hdr->task;
-      if (g_s4tl_on && threadIdx.x == 32 && blockIdx.x < kS4TlCtas && 2 + k < kS4TlSlots)
+      if ((p.dbg & 4) && threadIdx.x == 32 && blockIdx.x < kS4TlCtas && 2 + k < kS4TlSlots)
         g_s4tl[blockIdx.x][2 + k] = gtimer();
       if (task >= ntasks) break;
       if (task < ncos) {
@@ -346,7 +345,7 @@ __global__ void __launch_bounds__(kS4Threads, 1) scan4_kernel(DecodeParams p) {
       }
     }
   }
-  if (g_s4tl_on && threadIdx.x == 32 && blockIdx.x < kS4TlCtas) g_s4tl[blockIdx.x][1] = gtimer();
+  if ((p.dbg & 4) && threadIdx.x == 32 && blockIdx.x < kS4TlCtas) g_s4tl[blockIdx.x][1] = gtimer();
 }
 
 int scan4_timeline(int on, unsigned long long* out, int n) {
@@ -354,7 +353,7 @@ int scan4_timeline(int on, unsigned long long* out, int n) {
     const int m = n < kS4TlCtas * kS4TlSlots ? n : kS4TlCtas * kS4TlSlots;
     if (cudaMemcpyFromSymbol(out, g_s4tl, sizeof(unsigned long long) * m) != cudaSuccess) return CTKV_ECUDA;
   }
-  if (on >= 0 && cudaMemcpyToSymbol(g_s4tl_on, &on, sizeof(int)) != cudaSuccess) return CTKV_ECUDA;
+  if (on >= 0) set_host_dbg(4, on);
   return CTKV_OK;
 }
 
@@ -371,7 +370,9 @@ bool scan4_supported(const DecodeParams& p, int dtype, int D) {
 }
 
 template <int D>
-static int launch_scan4_t(const DecodeParams& p, cudaStream_t st) {
+static int launch_scan4_t(const DecodeParams& p0, cudaStream_t st) {
+  DecodeParams p = p0;
+  p.dbg = g_host_dbg;
   const size_t sm = scan4_smem();
   auto k = scan4_kernel<D>;
   static bool set = false;

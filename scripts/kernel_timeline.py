@@ -33,6 +33,7 @@ for li in range(NL):
     del q, k, v
 lib = N.lib()
 lib.ctkv_debug_kernel_timeline(1)
+lib.ctkv_debug_phase_timing(1, None, 0)   # chain phase marks (a launch parameter: on before capture)
 eng = DecodeEngine(built, P.DecodeConfig(4, 512), lanes=lanes)
 
 
@@ -54,8 +55,6 @@ for t in range(6):
             lay, sd, idd, args, ws, wsn = L.call
             lib.ctkv_debug_timeline_rw(lay, L.index.capacity, L.index.rho, 4, ws, None, 1)
         torch.cuda.synchronize()
-    if t == 5:
-        lib.ctkv_debug_phase_timing(1, None, 0)   # chain phase marks under load
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     eng.replay() if t >= 3 else eng.step()
