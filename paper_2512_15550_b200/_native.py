@@ -16,7 +16,8 @@ import torch
 from .errors import ConfigError, DegenerateQueryWarning, ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libctkv.so")
+# CTKV_LIB: an alternative in-tree build of the same library (A/B runs of kernel variants)
+LIB_PATH = os.environ.get("CTKV_LIB") or os.path.join(_HERE, "libctkv.so")
 
 F32, BF16 = 0, 1
 OK, ESHAPE, ECONFIG, EINDEX, ECUDA, EWORKSPACE = range(6)

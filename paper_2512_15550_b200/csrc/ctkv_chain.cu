@@ -419,7 +419,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   cmark(p, 4);
 
   // ---- 3. rerank logits of the slice (K rows gathered into registers) ----------
-  if (!p.chain_simt) {
+  {
     // Tensor-core form: per warp, 16-row blocks of the slice as the A operand
     // of mma.m16n8k16 (bf16 products exact, f32 sum per 16-element k-step,
     // f64 across the k-steps), the gs query heads as the B columns.  The
@@ -514,83 +514,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
         }
       }
       if (bk0 == warp * NB) cmark(p, 14);
-    }
-  } else {
-    const double scale = 1.0 / sqrt((double)D);
-    const T* keys_g = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
-    constexpr int LPR = 8;                 // lanes per row
-    constexpr int CPL = CH / LPR;          // 16-byte chunks per lane (2 at d=128)
-    const int sub = lane % LPR, rw = lane / LPR;
-    constexpr int RPW = 32 / LPR;          // rows per warp pass
-    const uint4* q4 = reinterpret_cast<const uint4*>(qs);
-    // every CTA's area B is free after barrier #2: the keys go to all of them
-    uint32_t rkeys[CL > 1 ? CL - 1 : 1];   // shared::cluster addresses
-#pragma unroll
-    for (int o = 0; o < CL - 1; ++o) rkeys[o] = dsmem_addr(S.keys, (r + 1 + o) % CL);
-    for (int b0 = warp * RPW; b0 < n_sl; b0 += kCW * RPW * kKUn) {
-      uint4 raw[kKUn][CPL];
-#pragma unroll
-      for (int x = 0; x < kKUn; ++x) {
-        const int t = b0 + x * kCW * RPW + rw;
-        if (t < n_sl) {
-          const uint4* r4 = reinterpret_cast<const uint4*>(keys_g + (int64_t)S.sid[t] * D);
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) raw[x][c] = ldg16(r4 + c * LPR + sub);
-        } else {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) raw[x][c] = make_uint4(0, 0, 0, 0);
-        }
-      }
-      if (b0 == warp * RPW) cmark(p, 12);   // first round issued
-#pragma unroll
-      for (int x = 0; x < kKUn; ++x) {
-        const int t = b0 + x * kCW * RPW + rw;
-        if (x == 1 && b0 == warp * RPW) cmark(p, 13);   // first row of the first round done
-        double a[GS];
-#pragma unroll
-        for (int hh = 0; hh < GS; ++hh) {
-          a[hh] = (double)bf16x8_dot(q4[hh * CH + sub], raw[x][0], 0.f);
-#pragma unroll
-          for (int c = 1; c < CPL; ++c) a[hh] += (double)bf16x8_dot(q4[hh * CH + c * LPR + sub], raw[x][c], 0.f);
-        }
-        // transposed reduction over the row's LPR lanes: every level halves
-        // the heads a lane carries (it keeps one half and ships the other),
-        // so a row costs GS - 1 + log2(LPR) double shuffles, not GS * log2(LPR)
-        int hh = 0;
-        int dup = 0;   // lane bits of the levels that only summed (same head)
-#pragma unroll
-        for (int lv = 0, s = LPR / 2; s > 0; ++lv, s >>= 1) {
-          const int H = GS >> lv;   // heads carried into this level
-          if (H > 1) {
-            const bool hi = (sub & s) != 0;
-#pragma unroll
-            for (int i = 0; i < H / 2; ++i) {
-              const double keep = hi ? a[i + H / 2] : a[i];
-              const double send = hi ? a[i] : a[i + H / 2];
-              a[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-            }
-            hh += hi ? H / 2 : 0;
-          } else {
-            a[0] += __shfl_xor_sync(0xffffffffu, a[0], s);
-            dup |= s;
-          }
-        }
-        const double lg = a[0] * scale;
-        if ((sub & dup) == 0 && t < n_sl) lgg[(int64_t)hh * p.lmax + lo + t] = lg;
-        // group max over the heads (max commutes with the f32 rounding)
-        float gm = (float)lg;
-#pragma unroll
-        for (int lv = 0, s = LPR / 2; s > 0; ++lv, s >>= 1)
-          if ((GS >> lv) > 1) gm = fmaxf(gm, __shfl_xor_sync(0xffffffffu, gm, s));
-        if (sub == 0 && t < n_sl) {
-          const uint32_t k32 = ~okey32(gm);
-          S.keys[lo + t] = k32;
-#pragma unroll
-          for (int o = 0; o < CL - 1; ++o) st_cluster_u32(rkeys[o] + 4u * (uint32_t)(lo + t), k32);
-          kg[lo + t] = ((uint64_t)k32 << 32) | (uint32_t)(lo + t);
-        }
-      }
-      if (b0 == warp * RPW) cmark(p, 14);   // first round done
     }
   }
   cmark(p, 5);
@@ -863,19 +786,9 @@ static int chain_cl() {   // CTKV_CHAIN_CL=2|8 selects 2- or 8-CTA clusters (A/B
   return v;
 }
 
-static int chain_simt() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CTKV_CHAIN_SIMT");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v;
-}
-
 template <typename T, int D, int CL, int GS>
 static int launch_chain_t(const DecodeParams& p0, cudaStream_t st) {
   DecodeParams p = p0;
-  p.chain_simt = chain_simt();
   p.dbg = g_host_dbg;
   const size_t sm = chain_layout(p, D, CL, nullptr, nullptr);
   auto k = chain_kernel<T, D, CL, GS>;

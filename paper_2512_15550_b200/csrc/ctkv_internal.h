@@ -72,7 +72,6 @@ struct DecodeParams {
   int sel_in_chain; // 1: the chain kernel selects top-C' from gcos itself (scan4)
   int dbg;          // debug timestamp marks (host_dbg bits: 1 scan2, 2 chain, 4 scan4): a kernel
                     // parameter, so marks that are off cost no global load
-  int chain_simt;   // 1: SIMT rerank logits in the chain (CTKV_CHAIN_SIMT=1 A/B), else mma.sync
   // staged io
   const int32_t* rec_in;
   const int32_t* len_in;
