@@ -451,22 +451,84 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
   for (int k = threadIdx.x; k < gs * D; k += blockDim.x) qs[k] = q[k];
   __syncthreads();
   bar_wait(barK, 0);
+  s2mark(p, 1);
   const double scale = 1.0 / sqrt((double)D);
-  // logits: pair (t, j), consecutive threads -> consecutive tokens
-  for (int pr = threadIdx.x; pr < nt * gs; pr += blockDim.x) {
-    const int t = pr % nt, j = pr / nt;
-    double dot, nrm;
-    row_dot<T, D, false>(qs + j * D, Ks + (size_t)t * D, t, dot, nrm);
-    lg[j * ST + t] = dot * scale;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __shared__ double wmax[kScanRowsV2 / 32][kMaxGroup];   // per-warp head maxima (tensor-core path)
+  bool mma_logits = false;
+  if constexpr (sizeof(T) == 2) {
+    // logits on the tensor cores: warp w takes tokens [16w, 16w+16) as the A
+    // operand of mma.m16n8k16 (f32 per 16-element k-step, f64 across), the
+    // gs heads as B columns; k permuted alike in K and q (as in the chain).
+    // The epilogue also reduces each warp's per-head maxima.
+    mma_logits = true;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    double mloc[2] = {-INFINITY, -INFINITY};
+    for (int blk = warp; blk * 16 < nt; blk += nw) {
+      const int r0 = blk * 16 + g8, r1 = r0 + 8;
+      const T* ra = Ks + (size_t)r0 * D + 8 * t4;
+      const T* rb = ra + 8 * D;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int s2 = 0; s2 < D / 32; ++s2) {
+        const uint4 a = *reinterpret_cast<const uint4*>(ra + s2 * 32);
+        const uint4 b = *reinterpret_cast<const uint4*>(rb + s2 * 32);
+        const uint4 qv = g8 < gs ? *reinterpret_cast<const uint4*>(qs + g8 * D + s2 * 32 + 8 * t4)
+                                 : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          float d0, d1, d2, d3;
+          asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+              "{%10,%10,%10,%10};"
+              : "=f"(d0), "=f"(d1), "=f"(d2), "=f"(d3)
+              : "r"(hf ? a.z : a.x), "r"(hf ? b.z : b.x), "r"(hf ? a.w : a.y), "r"(hf ? b.w : b.y),
+                "r"(hf ? qv.z : qv.x), "r"(hf ? qv.w : qv.y), "f"(0.f));
+          acc[0] += (double)d0;
+          acc[1] += (double)d1;
+          acc[2] += (double)d2;
+          acc[3] += (double)d3;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int h = 2 * t4 + e;
+        if (h < gs) {
+          const double l0 = acc[e] * scale, l1 = acc[2 + e] * scale;
+          if (r0 < nt) { lg[h * ST + r0] = l0; mloc[e] = fmax(mloc[e], l0); }
+          if (r1 < nt) { lg[h * ST + r1] = l1; mloc[e] = fmax(mloc[e], l1); }
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      mloc[0] = fmax(mloc[0], __shfl_xor_sync(0xffffffffu, mloc[0], o));
+      mloc[1] = fmax(mloc[1], __shfl_xor_sync(0xffffffffu, mloc[1], o));
+    }
+    if (g8 == 0)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (2 * t4 + e < gs) wmax[warp][2 * t4 + e] = mloc[e];
+  } else {
+    // logits: pair (t, j), consecutive threads -> consecutive tokens
+    for (int pr = threadIdx.x; pr < nt * gs; pr += blockDim.x) {
+      const int t = pr % nt, j = pr / nt;
+      double dot, nrm;
+      row_dot<T, D, false>(qs + j * D, Ks + (size_t)t * D, t, dot, nrm);
+      lg[j * ST + t] = dot * scale;
+    }
   }
   __syncthreads();
+  s2mark(p, 4);
   // per-head max / exp weights / denominators: one warp per head
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int j = warp; j < gs; j += nw) {
     double m = -INFINITY;
-    for (int t = lane; t < nt; t += 32) m = fmax(m, lg[j * ST + t]);
+    if (mma_logits) {
+      for (int w2 = 0; w2 * 16 < nt && w2 < nw; ++w2) m = fmax(m, wmax[w2][j]);
+    } else {
+      for (int t = lane; t < nt; t += 32) m = fmax(m, lg[j * ST + t]);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
     double l = 0.0;
     for (int t = lane; t < nt; t += 32) {
       const double e = exp(lg[j * ST + t] - m);
@@ -478,7 +540,9 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
     if (lane == 0) { ml[j] = m; ml[gs + j] = l; }
   }
   __syncthreads();
+  s2mark(p, 5);
   bar_wait(barV, 0);
+  s2mark(p, 6);
   // o[j][e] = sum_t w[j][t] * V[t][e]; a thread owns two adjacent elements
   for (int pr = threadIdx.x; pr < gs * (D / 2); pr += blockDim.x) {
     const int j = pr / (D / 2), e = 2 * (pr % (D / 2));
@@ -499,7 +563,7 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(kScanRowsV2) scan2_kernel(DecodeParams p) {
+__global__ void __launch_bounds__(kScanRowsV2, 4) scan2_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[kMaxGroup];
   pdl_trigger();   // the chain kernel may launch once every scan CTA is resident
