@@ -709,6 +709,32 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   __syncthreads();
   double* wj = S.scratch;   // [gs][ns + CL] split weights
   const int nsp = ns + CL;
+  if (nsp <= 32) {   // a warp per head, a lane per split: max, weights, denominator
+    for (int hh = warp; hh < gs; hh += kCW) {
+      const int j = lane;
+      double mj = -INFINITY, lj = 0.0;
+      if (j < ns) {
+        mj = S.spml[j * gs + hh];
+        lj = S.spml[ns * gs + j * gs + hh];
+      } else if (j < nsp) {
+        mj = S.cpml[(j - ns) * gs + hh];
+        lj = S.cpml[CL * gs + (j - ns) * gs + hh];
+      }
+      double M = lj > 0.0 ? mj : -INFINITY;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmax(M, __shfl_xor_sync(0xffffffffu, M, o));
+      const double w = lj > 0.0 ? dexp(mj - M) : 0.0;
+      double Ls = w * lj;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) Ls += __shfl_xor_sync(0xffffffffu, Ls, o);
+      if (j < nsp) wj[hh * nsp + j] = w;
+      if (lane == 0) {
+        hm[hh] = M;
+        hl[hh] = Ls;
+      }
+    }
+    __syncthreads();
+  } else {
   if (tid < gs) {
     const int hh = tid;
     double M = -INFINITY;
@@ -736,6 +762,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     hl[hh] = Ls;
   }
   __syncthreads();
+  }
   bool none = false;
 #pragma unroll 1
   for (int i = tid; i < gs * D; i += kCT) {
