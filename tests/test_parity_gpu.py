@@ -406,3 +406,51 @@ def test_96k_tensor_core_build_matches_exact_within_tie_window():
                 break
     assert hard == 0, f"{hard} rows differ beyond the tie window ({len(bad)} differ at all)"
     assert len(bad) <= 0.01 * 8 * 512
+
+
+# ---------------------------------------------------------------------------
+# bf16 fused decode (scan2 -> cluster chain -> tail) across geometries: group
+# sizes 1/2/8, d = 64, c' below / above the 4-CTA cluster, rho not a multiple
+# of 4 (plain list loads instead of TMA bulk copies), c' = 1
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("h,g,d,C,rho,cp,rp", [
+    (8, 8, 128, 64, 30, 3, 40),
+    (16, 8, 64, 64, 64, 6, 96),
+    (16, 2, 128, 32, 48, 8, 120),
+    (8, 2, 128, 64, 64, 1, 16),
+])
+def test_bf16_fused_decode_geometries(h, g, d, C, rho, cp, rp):
+    rng = np.random.default_rng(1000 * h + 10 * d + C + rho + cp)
+    b, s, T, init, local = 2, 1024, 3, 16, 64
+    q = O.bf16_round(rng.standard_normal((b, h, s + T, d)).astype(np.float32))
+    k = O.bf16_round(rng.standard_normal((b, g, s + T, d)).astype(np.float32))
+    v = O.bf16_round(rng.standard_normal((b, g, s + T, d)).astype(np.float32))
+    store, index = P.prefill(np.ascontiguousarray(q[:, :, :s]), np.ascontiguousarray(k[:, :, :s]),
+                             np.ascontiguousarray(v[:, :, :s]), P.PrefillParams(init, local, C, rho),
+                             dtype=torch.bfloat16, reserve=T, build_mode=0)
+    outs, trace = P.run_decode(store, index, P.DecodeConfig(cp, rp, keep_sets=True),
+                               np.ascontiguousarray(q[:, :, s:]), np.ascontiguousarray(k[:, :, s:]),
+                               np.ascontiguousarray(v[:, :, s:]))
+    ost, oidx = O.prefill(np.ascontiguousarray(q[:, :, :s]), np.ascontiguousarray(k[:, :, :s]),
+                          np.ascontiguousarray(v[:, :, :s]), init, local, C, rho)
+    ref_out, recs = O.run_decode(ost, oidx, q[:, :, s:], k[:, :, s:], v[:, :, s:], cp, rp)
+    hard = hard_order = 0
+    for t in range(T):
+        assert nrel(outs[:, :, t], ref_out[:, :, t]) < 1e-3
+        r = recs[t]
+        for bi in range(b):
+            for gi in range(g):
+                mine_l, ref_l = trace[t].sparse[bi][gi].tolist(), r.sparse[bi][gi].tolist()
+                assert len(mine_l) == len(ref_l)
+                ids = np.asarray(r.recalled[bi][gi])
+                sc = dict(zip(ids.tolist(), np.asarray(r.grouped[bi][gi]).tolist()))
+                if set(mine_l) != set(ref_l):
+                    kth = sorted(sc.values(), reverse=True)[len(ref_l) - 1]
+                    hard += any(abs(sc.get(i, -np.inf) - kth) > TIE_REL * abs(kth)
+                                for i in set(mine_l) ^ set(ref_l))
+                hard_order += sum(abs(sc.get(a, -np.inf) - sc[b_]) > TIE_REL * abs(sc[b_])
+                                  for a, b_ in zip(mine_l, ref_l) if a != b_)
+        assert trace[t].recall_len == r.recall_len
+    assert hard == 0
+    assert hard_order == 0
