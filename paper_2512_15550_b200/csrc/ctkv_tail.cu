@@ -23,12 +23,12 @@
 
 namespace ctkv {
 
-constexpr int kTailT = 512;            // threads per tail CTA
+constexpr int kTailT = 256;            // threads per tail CTA
 constexpr int kTailBins = 1024;        // counting-sort bins
 
 __host__ __device__ inline size_t tail_smem(const DecodeParams& p) {
   const int lmax = p.lmax > 1 ? p.lmax : 1;
-  return (size_t)3 * lmax * 4 + (size_t)2 * kTailBins * 4;
+  return align16((size_t)lmax * 4) + align16((size_t)2 * lmax * 2) + (size_t)2 * kTailBins * 4;
 }
 
 template <typename T, int D>
@@ -40,11 +40,12 @@ __global__ void __launch_bounds__(kTailT) tail_kernel(DecodeParams p) {
   __shared__ int64_t s_slot;
   __shared__ uint32_t s_mm[2 * (kTailT / 32)];
   const int lmax = p.lmax > 1 ? p.lmax : 1;
-  uint32_t* k32 = reinterpret_cast<uint32_t*>(smem);   // [lmax] score keys by position
-  int* binned = reinterpret_cast<int*>(k32 + lmax);    // [lmax] positions grouped by bin
-  int* order = binned + lmax;                          // [lmax] position of rank r
-  int* hist = order + lmax;                            // [kTailBins]
-  int* cur = hist + kTailBins;                         // [kTailBins]
+  // positions fit 16 bits (lmax = c' * rho <= 32768): 8 B per recall slot
+  uint32_t* k32 = reinterpret_cast<uint32_t*>(smem);                          // [lmax] score keys
+  uint16_t* binned = reinterpret_cast<uint16_t*>(smem + align16((size_t)lmax * 4));   // [lmax] by bin
+  uint16_t* order = binned + lmax;                                            // [lmax] rank -> position
+  int* hist = reinterpret_cast<int*>(smem + align16((size_t)lmax * 4) + align16((size_t)2 * lmax * 2));
+  int* cur = hist + kTailBins;                                                // [kTailBins]
   pdl_trigger();
   pdl_wait();
   ktl_mark(p.tl, 2, false);
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kTailT) tail_kernel(DecodeParams p) {
       }
     }
     __syncthreads();
-    for (int i = tid; i < L; i += kTailT) binned[atomicAdd(&cur[bin_of(k32[i])], 1)] = i;
+    for (int i = tid; i < L; i += kTailT) binned[atomicAdd(&cur[bin_of(k32[i])], 1)] = (uint16_t)i;
     __syncthreads();
     for (int i = tid; i < L; i += kTailT) {
       const uint32_t k = k32[i];
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(kTailT) tail_kernel(DecodeParams p) {
         const uint32_t kj = k32[j];
         r += (kj < k) || (kj == k && j < i);
       }
-      order[r] = i;
+      order[r] = (uint16_t)i;
     }
   }
   __syncthreads();
@@ -166,6 +167,7 @@ static int launch_tail_t(const DecodeParams& p, cudaStream_t st) {
 
 bool tail_supported(const DecodeParams& p, int dtype, int D) {
   if (dtype != CTKV_BF16 || (D != 64 && D != 128)) return false;
+  if (p.lmax > 65535) return false;   // 16-bit positions
   return tail_smem(p) <= 200 * 1024;
 }
 
