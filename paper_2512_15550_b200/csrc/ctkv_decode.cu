@@ -331,24 +331,34 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
     gv[c] = m;
   }
   // v6: the unit's last cosine chunk takes the top-C' of all C group maxima
+  // The unit's last chunk is its selector: the other chunks publish with a
+  // release fence and a fire-and-forget increment and exit at once (no
+  // atomic round trip); the selector acquires the count, then takes the
+  // top-C' of all C group maxima.  Lower-numbered CTAs are dispatched first,
+  // so the selector only ever waits for CTAs that are already resident.
   if (p.selg != nullptr) {
-    __shared__ int s_last;
-    __syncthreads();
+    __syncthreads();   // this chunk's gcos written
     s2mark(p, 4);
+    if (chunk != cpu - 1) {
+      if (threadIdx.x == 0)   // release (cumulative over the barrier above) + relaxed increment
+        asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(p.selctr + u)
+                     : "memory");
+      return;
+    }
     if (threadIdx.x == 0) {
-      __threadfence();
-      s_last = atomicAdd(&p.selctr[u], 1) == cpu - 1;
+      int seen;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(p.selctr + u) : "memory");
+        if (seen >= cpu - 1) break;
+        __nanosleep(64);
+      }
+      p.selctr[u] = 0;   // every other chunk has counted: reset for the next step
     }
     __syncthreads();
-    s2mark(p, 5);
-    if (s_last) {
-      __threadfence();
-      s2mark(p, 6);
-      block_top_slots(p.gcos + (int64_t)u * p.C, p.C, p.c_prime, p.selg + (int64_t)u * p.c_prime,
-                      cosv, reinterpret_cast<int*>(cosv + 64));
-      if (threadIdx.x == 0) p.selctr[u] = 0;
-      s2mark(p, 7);
-    }
+    s2mark(p, 6);
+    block_top_slots(p.gcos + (int64_t)u * p.C, p.C, p.c_prime, p.selg + (int64_t)u * p.c_prime,
+                    cosv, reinterpret_cast<int*>(cosv + 64));
+    s2mark(p, 7);
     return;
   }
   // chunk-local top-C' candidates (value desc, slot asc): the global top-C'
