@@ -553,6 +553,37 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
   s2mark(p, 5);
   bar_wait(barV, 0);
   s2mark(p, 6);
+  if constexpr (sizeof(T) == 2) {
+    // o[j][:] = sum_t w[j][t] V[t][:]: a lane owns a 16-byte chunk (8 dims) of
+    // one head for a quarter of the tokens (lanes 0-7 of a quarter read one
+    // 128-byte row segment: conflict-free), quarters summed by shuffles
+    constexpr int CHN = D / 8;
+    const int ch_lo = lane & 7, tq = lane >> 3;
+    const int ntask = (CHN / 8) * gs;
+    for (int task = warp; task < ntask; task += nw) {
+      const int j = task / (CHN / 8), ch = (task % (CHN / 8)) * 8 + ch_lo;
+      float a[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = 0.f;
+      const float* wj = w + j * ST;
+      for (int t = tq; t < nt; t += 4) {
+        float f[8];
+        unpack16<T>(*reinterpret_cast<const uint4*>(Vs + (size_t)t * D + ch * 8), f);
+        const float wt = wj[t];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a[e] = fmaf(wt, f[e], a[e]);
+      }
+#pragma unroll
+      for (int o = 8; o < 32; o <<= 1)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) a[e] += __shfl_xor_sync(0xffffffffu, a[e], o);
+      if (tq == 0) {
+        float4* dst = reinterpret_cast<float4*>(po + j * D + ch * 8);
+        dst[0] = make_float4(a[0], a[1], a[2], a[3]);
+        dst[1] = make_float4(a[4], a[5], a[6], a[7]);
+      }
+    }
+  } else
   // o[j][e] = sum_t w[j][t] * V[t][e]; a thread owns two adjacent elements
   for (int pr = threadIdx.x; pr < gs * (D / 2); pr += blockDim.x) {
     const int j = pr / (D / 2), e = 2 * (pr % (D / 2));
