@@ -29,6 +29,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import torch
 
 from . import _native as N
@@ -162,7 +164,7 @@ class DecodeEngine:
                 if self.world > 1:
                     self._gather(k, li)
 
-    def _enqueue(self, events=None) -> None:
+    def _enqueue(self, events=None, hio=None) -> None:
         if self.layers[0].call is None:
             self._prepare()
         if events is not None:
@@ -172,12 +174,29 @@ class DecodeEngine:
         fork = torch.cuda.Event()
         fork.record(main)
         streams = self._lane_st + self._tail_st + ([self._comm] if self._comm is not None else [])
+        if hio is not None:
+            streams = streams + [self._cin, self._cout]
         for s in streams:
             s.wait_event(fork)
+        if hio is not None:
+            # host inputs: every (layer, lane) slice copied in issue order on
+            # one stream, so the copies run ahead of the layers that use them
+            hq, hk, hv, _ = hio
+            with torch.cuda.stream(self._cin):
+                for c0 in range(0, self.nl, self._cin_chunk):
+                    c1 = min(self.nl, c0 + self._cin_chunk)
+                    self.q[c0:c1].copy_(hq[c0:c1], non_blocking=True)
+                    self.k[c0:c1].copy_(hk[c0:c1], non_blocking=True)
+                    self.v[c0:c1].copy_(hv[c0:c1], non_blocking=True)
+                    for li in range(c0, c1):
+                        for k in range(self.nlanes):
+                            self._cin_ev[k][li].record(self._cin)
         for li in range(self.nl):
             for k in range(self.nlanes):
                 L = self.lane_layers[k][li]
                 ls, ts = self._lane_st[k], self._tail_st[k]
+                if hio is not None:
+                    ls.wait_event(self._cin_ev[k][li])
                 if self._comm is not None and li > 0:
                     ls.wait_event(self._gev[k][li - 1])
                 # phase bits: 1 scan, 2 unit, 8 defer the tail, 4 tail only
@@ -193,6 +212,16 @@ class DecodeEngine:
                     with torch.cuda.stream(self._comm):
                         self._gather(k, li)
                     self._gev[k][li].record(self._comm)
+                if hio is not None and self._comm is None:
+                    # a finished (layer, lane) output leaves while later layers run
+                    self._cout.wait_event(ev)
+                    b0, b1 = k * self.bl, (k + 1) * self.bl
+                    with torch.cuda.stream(self._cout):
+                        hio[3][li, b0:b1].copy_(self.out[li, b0:b1], non_blocking=True)
+            if hio is not None and self._comm is not None:
+                self._cout.wait_event(self._gev[self.nlanes - 1][li])   # all lanes gathered
+                with torch.cuda.stream(self._cout):
+                    hio[3][li].copy_(self.gathered[li], non_blocking=True)
         for s in streams:
             main.wait_stream(s)
 
@@ -230,6 +259,44 @@ class DecodeEngine:
         if self.graph is None:
             raise RuntimeError("capture() first")
         self.graph.replay()
+        self._note()
+
+    # -- host I/O inside the step -------------------------------------------
+
+    def capture_host_io(self, slots: int = 2) -> list:
+        """Capture `slots` step graphs whose inputs come from, and outputs go
+        to, pinned host buffers: each (layer, lane)'s q/k/v slice is copied in
+        on a copy stream ahead of its layer, and its output is copied out as
+        soon as the layer finishes, so the transfers overlap the other
+        layers.  Returns the host buffer sets (q [L,b,h,d], k/v [L,b,g,d],
+        out like `gathered`); with two slots a caller fills one slot's inputs
+        while the other slot's step runs (`replay_host(slot)`)."""
+        if self.layers[0].call is None:
+            self._prepare()
+        dev = self.q.device
+        self._cin = torch.cuda.Stream(device=dev)
+        self._cout = torch.cuda.Stream(device=dev)
+        self._cin_ev = [[torch.cuda.Event() for _ in range(self.nl)] for _ in range(self.nlanes)]
+        self._cin_chunk = max(1, int(os.environ.get("CTKV_HIO_CHUNK", "4")))   # layers per input copy
+        bufs, graphs = [], []
+        torch.cuda.synchronize()
+        for _ in range(slots):
+            hio = (torch.empty(self.q.shape, dtype=self.dtype).pin_memory(),
+                   torch.empty(self.k.shape, dtype=self.dtype).pin_memory(),
+                   torch.empty(self.v.shape, dtype=self.dtype).pin_memory(),
+                   torch.empty(self.gathered.shape, dtype=torch.float32).pin_memory())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._enqueue(hio=hio)
+            bufs.append(hio)
+            graphs.append(g)
+        self._hgraphs = graphs
+        return bufs
+
+    def replay_host(self, slot: int) -> None:
+        """One step through host buffer set `slot` (see capture_host_io); the
+        outputs are in that set's out buffer once the stream is synchronised."""
+        self._hgraphs[slot].replay()
         self._note()
 
     def flags(self) -> int:

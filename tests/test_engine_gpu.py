@@ -33,8 +33,11 @@ def _prefill(q, k, v):
                      dtype=torch.bfloat16, reserve=T + 2, build_mode=0)
 
 
-@pytest.mark.parametrize("lanes,graph", [(1, False), (2, True), (4, True)])
+@pytest.mark.parametrize("lanes,graph", [(1, False), (2, True), (4, True), (4, "host")])
 def test_engine_equals_per_layer_decode(lanes, graph):
+    """graph="host": steps from t = 1 run through capture_host_io's two
+    graph slots (q/k/v copied in from pinned host buffers per (layer, lane)
+    inside the step, outputs copied out as each layer finishes)."""
     torch.cuda.set_device(0)
     data = [_inputs(li) for li in range(NL)]
     cfg = P.DecodeConfig(CP, RP)
@@ -52,7 +55,20 @@ def test_engine_equals_per_layer_decode(lanes, graph):
     eng = DecodeEngine(built, cfg, lanes=lanes)
     dev = eng.q.device
     got = np.zeros((NL, B, H, T, D), np.float32)
+    hbufs = None
     for t in range(T):
+        if graph == "host" and t >= 1:
+            if hbufs is None:
+                hbufs = eng.capture_host_io(2)
+            hq, hk, hv, hout = hbufs[t % 2]
+            for li, (q, k, v) in enumerate(data):
+                hq[li].copy_(torch.from_numpy(np.ascontiguousarray(q[:, :, S + t])))
+                hk[li].copy_(torch.from_numpy(np.ascontiguousarray(k[:, :, S + t])))
+                hv[li].copy_(torch.from_numpy(np.ascontiguousarray(v[:, :, S + t])))
+            eng.replay_host(t % 2)
+            torch.cuda.synchronize()
+            got[:, :, :, t] = hout.numpy()
+            continue
         for li, (q, k, v) in enumerate(data):
             eng.q[li].copy_(torch.from_numpy(np.ascontiguousarray(q[:, :, S + t])).to(dev))
             eng.k[li].copy_(torch.from_numpy(np.ascontiguousarray(k[:, :, S + t])).to(dev))
