@@ -433,10 +433,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     constexpr int KS2 = D / 32;            // 32-element k pairs per row
     constexpr int NB = 2;                  // 16-row blocks in flight per warp
     const int g8 = lane >> 2, t4 = lane & 3;
-    uint4 qf[KS2];
-#pragma unroll
-    for (int s2 = 0; s2 < KS2; ++s2)
-      qf[s2] = g8 < GS ? *reinterpret_cast<const uint4*>(qs + g8 * D + s2 * 32 + 8 * t4) : make_uint4(0, 0, 0, 0);
+    const T* qf_base = qs + (g8 < GS ? g8 : 0) * D + 8 * t4;   // B fragments re-read from smem per k-step
     uint32_t rkeys[CL > 1 ? CL - 1 : 1];   // shared::cluster addresses of the other CTAs' keys
 #pragma unroll
     for (int o = 0; o < CL - 1; ++o) rkeys[o] = dsmem_addr(S.keys, (r + 1 + o) % CL);
@@ -465,11 +462,12 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int s2 = 0; s2 < KS2; ++s2) {
+          const uint4 qv = g8 < GS ? *reinterpret_cast<const uint4*>(qf_base + s2 * 32) : make_uint4(0, 0, 0, 0);
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {   // 16-element k-steps: (.x .y) then (.z .w) of the pieces
             const uint32_t a0 = hf ? ra[nb][s2].z : ra[nb][s2].x, a1 = hf ? rb[nb][s2].z : rb[nb][s2].x;
             const uint32_t a2 = hf ? ra[nb][s2].w : ra[nb][s2].y, a3 = hf ? rb[nb][s2].w : rb[nb][s2].y;
-            const uint32_t b0 = hf ? qf[s2].z : qf[s2].x, b1 = hf ? qf[s2].w : qf[s2].y;
+            const uint32_t b0 = hf ? qv.z : qv.x, b1 = hf ? qv.w : qv.y;
             float d0, d1, d2, d3;
             asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
                 "{%10,%10,%10,%10};"
