@@ -319,6 +319,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   __shared__ double hm[GS], hl[GS], hnew[GS], hresc[GS];
 
   cmark(p, 0);
+  // #0 (split): every CTA of the cluster has started before any DSMEM access
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   ktl_mark(p.tl, 1, false);
   ktl_mark(p.tl, 3, true);   // the last CTA start (slot 3 end = max start)
   pdl_wait();      // the scan's outputs (gcos / slots, static partials) are complete
@@ -361,6 +363,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   for (int i = tid; i < p.bitmap_words; i += kCT) S.bm[i] = 0u;
   __syncthreads();   // barrier initialised, bitmap cleared (and the plain-load stage written)
   if (nown > 0 && bulk) bar_wait(&lbar, 0);
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");   // #0: the survivor counts go remote below
   int jdone = 0;                                        // lists already in the bitmap
   for (int sl = 0; sl < nown; ++sl) {
     const int j = r + CL * sl;
