@@ -319,7 +319,12 @@ def main():
     engine.check()
     use_graph = not a.no_graph
     if use_graph:
-        engine.capture()
+        try:
+            engine.capture()
+        except RuntimeError as exc:   # e.g. a collective that cannot be captured on this stack
+            print(f"bench: graph capture failed ({exc}); eager steps", file=sys.stderr)
+            torch.cuda.synchronize()
+            use_graph = False
     run = engine.replay if use_graph else engine.step
     for _ in range(a.warmup - max(1, a.warmup // 2)):
         load_inputs(engine)
@@ -380,9 +385,16 @@ def main():
     # two graph slots with the host copies inside the step: each (layer,
     # lane)'s inputs are copied in ahead of it and its output copied out as it
     # finishes; the host fills the other slot's inputs while a step runs
-    hbufs = engine.capture_host_io(2)
+    hbufs = None
+    if use_graph:
+        try:
+            hbufs = engine.capture_host_io(2)
+        except RuntimeError as exc:
+            print(f"bench: host-I/O graph capture failed ({exc}); copies around the step", file=sys.stderr)
+            torch.cuda.synchronize()
+    hout = hbufs[0][3] if hbufs else torch.empty(engine.gathered.shape, dtype=torch.float32).pin_memory()
     h2d = (hq[0].numel() + hk[0].numel() + hv[0].numel()) * 2
-    d2h = hbufs[0][3].numel() * 4
+    d2h = hout.numel() * 4
 
     def fill(slot, t):
         bq, bk, bv, _ = hbufs[slot]
@@ -390,16 +402,24 @@ def main():
         bk.copy_(hk[t])
         bv.copy_(hv[t])
 
-    fill(0, 0)
+    if hbufs:
+        fill(0, 0)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0.record()
     for t in range(a.e2e_steps):
-        engine.replay_host(t % 2)
-        if t + 1 < a.e2e_steps:
-            fill((t + 1) % 2, t + 1)
+        if hbufs:
+            engine.replay_host(t % 2)
+            if t + 1 < a.e2e_steps:
+                fill((t + 1) % 2, t + 1)
+        else:
+            engine.q.copy_(hq[t], non_blocking=True)
+            engine.k.copy_(hk[t], non_blocking=True)
+            engine.v.copy_(hv[t], non_blocking=True)
+            run()
+            hout.copy_(engine.gathered, non_blocking=True)
         torch.cuda.current_stream().synchronize()   # the token is needed on the host
     e1.record()
     torch.cuda.synchronize()
