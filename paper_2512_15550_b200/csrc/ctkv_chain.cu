@@ -623,7 +623,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
 #pragma unroll 1
     for (int i = tid; i < GS * n; i += kCT) {
       const int hh = i / n, k = i - hh * n;
-      const double e = dexp(lgs[hh * kCB + k] - hnew[hh]);
+      const double e = (double)expf((float)(lgs[hh * kCB + k] - hnew[hh]));   // f32 exp: ~1e-7 rel. weights
       lgs[hh * kCB + k] = e;
       S.wts[hh * kCB + k] = (float)e;
     }

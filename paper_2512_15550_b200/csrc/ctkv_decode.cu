@@ -541,7 +541,7 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
     }
     double l = 0.0;
     for (int t = lane; t < nt; t += 32) {
-      const double e = exp(lg[j * ST + t] - m);
+      const double e = sizeof(T) == 2 ? (double)expf((float)(lg[j * ST + t] - m)) : exp(lg[j * ST + t] - m);
       w[j * ST + t] = (float)e;
       l += e;
     }
