@@ -51,10 +51,10 @@ for lanes in (8, 1):
             print(f"  cos CTA: start->rows median {np.median(lat):.1f} us; rows->done median {np.median((a[:ncos,2]-a[:ncos,1])/1e3):.1f}; done->end median {np.median((a[:ncos,3]-a[:ncos,2])/1e3):.1f}")
             stl = (a[ncos:, 2] - a[ncos:, 0]) / 1e3
             print(f"  static CTA: start->done median {np.median(stl):.1f} us")
-            st = a[ncos:]
+            sa = a[ncos:]
             for nm, c0_, c1_ in (("start->K landed", 0, 1), ("logits", 1, 4), ("softmax", 4, 5),
                                  ("V wait", 5, 6), ("P.V + store", 6, 2)):
-                print(f"    static {nm:16s} median {np.median((st[:, c1_] - st[:, c0_]) / 1e3):.2f} us")
+                print(f"    static {nm:16s} median {np.median((sa[:, c1_] - sa[:, c0_]) / 1e3):.2f} us")
             last = [i for i in range(ncos) if a[i, 7] > 0]
             for i in last[:8]:
                 print(f"    last cos CTA {i}: rows {r[i,1]:.1f} dots+gcos {r[i,4]:.1f} atomic {r[i,5]:.1f} fence {r[i,6]:.1f} select done {r[i,7]:.1f}")
