@@ -59,7 +59,8 @@ enum ctkv_flag {
   CTKV_FLAG_CAPACITY = 16,       /* device buffer limit hit (see ctkv_status_string) */
   CTKV_FLAG_DUP_IDS = 32,        /* duplicate ids in an attention set (ck/retrieval.py:261-262) */
   CTKV_FLAG_BUILD_FALLBACK = 64, /* build rows re-done on the exact fallback path (info) */
-  CTKV_FLAG_NO_TOKENS = 128      /* nothing attendable: ConfigError (ck/retrieval.py:355) */
+  CTKV_FLAG_NO_TOKENS = 128,     /* nothing attendable: ConfigError (ck/retrieval.py:355) */
+  CTKV_FLAG_INTERNAL = 256       /* a device-side wait timed out (internal error, RuntimeError) */
 };
 
 /* Dimensions shared by every call (ck/tensor_ops.py:25-55 HeadLayout plus

@@ -29,6 +29,7 @@ FLAG_CAPACITY = 16
 FLAG_DUP_IDS = 32
 FLAG_BUILD_FALLBACK = 64
 FLAG_NO_TOKENS = 128
+FLAG_INTERNAL = 256
 BUILD_EXACT, BUILD_FAST = 0, 1
 
 c_i32, c_i64, c_vp, c_size = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
@@ -161,6 +162,8 @@ def raise_flags(flags: int, what: str, *, recall_mixed_is_error: bool = True) ->
         raise ConfigError(f"{what}: no attendable tokens in either partition")
     if flags & FLAG_CAPACITY:
         raise ConfigError(f"{what}: a device buffer limit was exceeded")
+    if flags & FLAG_INTERNAL:
+        raise RuntimeError(f"{what}: a device-side wait timed out (internal error)")
 
 
 def ptr(t) -> int | None:

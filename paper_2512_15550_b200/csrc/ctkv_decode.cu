@@ -347,9 +347,13 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
     }
     if (threadIdx.x == 0) {
       int seen;
-      for (;;) {
+      for (int spin = 0;; ++spin) {
         asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(p.selctr + u) : "memory");
         if (seen >= cpu - 1) break;
+        if (spin > (1 << 24)) {   // ~1 s: never expected; report instead of hanging the GPU
+          set_flag(p.flags, kFlagInternal);
+          break;
+        }
         __nanosleep(64);
       }
       p.selctr[u] = 0;   // every other chunk has counted: reset for the next step

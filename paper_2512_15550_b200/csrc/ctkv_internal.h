@@ -20,6 +20,7 @@ enum : int32_t {
 };
 
 constexpr int32_t kFlagNoTokens = 128;  // nothing attendable (ConfigError)
+constexpr int32_t kFlagInternal = 256;  // a device-side wait timed out (RuntimeError)
 
 struct DecodeParams {
   // layout
