@@ -1,3 +1,5 @@
+"""Recall (union) length per (b, kv-head) unit at cfg2 for one decode query:
+the L that sizes the chain's rerank gather."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
