@@ -96,6 +96,8 @@ class DecodeEngine:
         self._lane_st = [torch.cuda.Stream(device=dev) for _ in range(lanes)] if cuda else []
         self._tail_st = [torch.cuda.Stream(device=dev) for _ in range(lanes)] if cuda else []
         self._ev = ([[torch.cuda.Event() for _ in range(nl)] for _ in range(lanes)] if cuda else [])
+        self._evs = ([[torch.cuda.Event() for _ in range(nl)] for _ in range(lanes)] if cuda else [])
+        self._tail_after_scan = os.environ.get("CTKV_TAIL_AFTER_SCAN", "1") == "1"
         world = plan.world if plan else 1
         self.world = world
         self._comm = torch.cuda.Stream(device=dev) if (cuda and world > 1) else None
@@ -200,13 +202,26 @@ class DecodeEngine:
                 if self._comm is not None and li > 0:
                     ls.wait_event(self._gev[k][li - 1])
                 # phase bits: 1 scan, 2 unit, 8 defer the tail, 4 tail only
-                self._launch(L, 1 | 2 | 8, ls)
+                if self._tail_after_scan:
+                    # the previous layer's tail waits until this layer's scan is
+                    # done, so it shares the GPU with this chain, not this scan
+                    self._launch(L, 1, ls)
+                    if li > 0:
+                        es = self._evs[k][li]
+                        es.record(ls)
+                        ts.wait_event(self._ev[k][li - 1])
+                        ts.wait_event(es)
+                        self._launch(self.lane_layers[k][li - 1], 4, ts)
+                    self._launch(L, 2 | 8, ls)
+                else:
+                    self._launch(L, 1 | 2 | 8, ls)
                 ev = self._ev[k][li]
                 ev.record(ls)
                 # the tail (DCU write, sparse ids, cursor/total advance) is only
                 # read by this layer's next step: run it beside the next layers
-                ts.wait_event(ev)
-                self._launch(L, 4, ts)
+                if not self._tail_after_scan or li == self.nl - 1:
+                    ts.wait_event(ev)
+                    self._launch(L, 4, ts)
                 if self._comm is not None:
                     self._comm.wait_event(ev)
                     with torch.cuda.stream(self._comm):
