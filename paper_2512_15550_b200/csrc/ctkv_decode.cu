@@ -1739,12 +1739,13 @@ int kernel_timeline(int on) {   // host switch; on < 0 queries
   return v;
 }
 
-// kPrioLow = the scan, kPrioMid = the tail, kPrioHigh = the chain by default;
+// kPrioLow = the scan, kPrioMid = the tail, kPrioHigh = the chain; defaults: chain
+// high, scan and tail low (the tail is released after the next scan already);
 // CTKV_PRIO=0 turns priorities off, CTKV_PRIO=xyz (x, y, z in h/m/l) sets the
 // scan's, chain's and tail's levels for A/B runs
 int launch_priority(LaunchPrio pr) {
   static int lo = 1, hi = 0, on = -1;
-  static char lvl[3] = {'l', 'm', 'h'};   // indexed by LaunchPrio
+  static char lvl[3] = {'l', 'l', 'h'};   // indexed by LaunchPrio: scan low, tail low, chain high
   if (on < 0) {
     const char* e = getenv("CTKV_PRIO");
     on = (e && e[0] == '0') ? 0 : 1;
