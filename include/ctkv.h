@@ -176,7 +176,11 @@ int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctk
  * step's phase 1 for the same layer, and may run on another stream
  * concurrently with other layers' work (it writes only this layer's index,
  * total and outputs, and reads this call's workspace).  Paths without a
- * separate tail run it inside phase 2 and treat 4 as a no-op. */
+ * separate tail run it inside phase 2 and treat 4 as a no-op.
+ * 16 (with any of the above): the caller guarantees that the kernel it
+ * launched last on `stream` writes none of this layer's store, index, query
+ * or new K/V (true in the engine, where it is the previous layer's chain);
+ * the scan and chain kernels may then use programmatic dependent launch. */
 int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
                            const ctkv_step_args* A, int32_t phase, void* workspace,
                            size_t workspace_bytes, void* stream);

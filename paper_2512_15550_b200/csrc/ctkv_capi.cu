@@ -210,7 +210,10 @@ int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctk
 int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
                            const ctkv_step_args* A, int32_t phase, void* workspace,
                            size_t workspace_bytes, void* stream) {
-  if (phase < 1 || phase > 15) return CTKV_ECONFIG;
+  if (phase < 1 || phase > 31) return CTKV_ECONFIG;
+  const PdlScope pdl_scope((phase & 16) != 0);   // 16: the caller allows programmatic dependent launch
+  phase &= 15;
+  if (phase < 1) return CTKV_ECONFIG;
   if (int rc = check_layout(L)) return rc;
   if (!A || !A->query || !A->out || !S.keys || !S.values || !S.total) return CTKV_ECONFIG;
   if (I.capacity < 1) return CTKV_ECONFIG;                            // "recall: empty index"

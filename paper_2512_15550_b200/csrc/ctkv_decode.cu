@@ -611,7 +611,7 @@ template <typename T, int D>
 __global__ void __launch_bounds__(kScanRowsV2, 4) scan2_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[kMaxGroup];
-  pdl_trigger();   // the chain kernel may launch once every scan CTA is resident
+  if (p.pdl == 1) pdl_trigger();   // CTKV_PDL=1 A/B: the chain may launch once every scan CTA is resident
   ktl_mark(p.tl, 0, false);
   s2mark(p, 0);
   const int64_t t0 = p.total ? *p.total : p.id_bound;
@@ -1628,6 +1628,7 @@ template <typename T, int D>
 static int launch_scan_t(const DecodeParams& p0, int nblocks, cudaStream_t st) {
   DecodeParams p = p0;
   p.dbg = g_host_dbg;
+  p.pdl = t_pdl_ok ? pdl_mode() : 0;
   const size_t sm = scan2_smem<T, D>(p.gs);
   auto k = scan2_kernel<T, D>;
   static size_t configured = 0;
@@ -1758,14 +1759,23 @@ int launch_priority(LaunchPrio pr) {
   return c == 'h' ? hi : c == 'm' ? (lo + hi) / 2 : lo;
 }
 
-bool pdl_enabled() {
+// Programmatic dependent launch, for callers that allow it (phase bit 16):
+// mode 3 (default) on the chain launch (scan CTAs trigger by exiting, so the
+// chain's launch is processed while the scan drains, without resident CTAs
+// waiting) and on the scan launch (the previous chain triggers after its
+// compaction; the scan's centroid TMA loads start before its griddepcontrol
+// wait); CTKV_PDL=2 the chain only, 1 every kernel with the scan triggering
+// at entry (slower: early-resident CTAs crowd the other lanes), 0 off.
+thread_local int t_pdl_ok = 0;
+int pdl_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("CTKV_PDL");
-    v = (e && e[0] == '1') ? 1 : 0;   // off by default: early-resident CTAs
-  }                                    // crowd the other lanes (2422 vs 2568 tok/s)
-  return v == 1;
+    v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
+  }
+  return v;
 }
+bool pdl_enabled() { return pdl_mode() == 1; }
 
 int decode_variant() {
   static int v = -1;

@@ -71,6 +71,7 @@ struct DecodeParams {
   int32_t* selg;    // [U][c'] top-C' slots (ties -> smaller slot)
   int* selctr;      // [U] cosine-chunk completion counters (reset by the last CTA)
   int sel_in_chain; // 1: the chain kernel selects top-C' from gcos itself (scan4)
+  int pdl;          // CTKV_PDL mode (the scan triggers early only in mode 1)
   int dbg;          // debug timestamp marks (host_dbg bits: 1 scan2, 2 chain, 4 scan4): a kernel
                     // parameter, so marks that are off cost no global load
   // staged io
@@ -130,6 +131,15 @@ int launch_append(int dtype, void* keys, void* vals, const void* kn, const void*
 // stream predecessor finishes; it calls pdl_wait() (griddepcontrol.wait)
 // before touching anything the predecessor produced.  CTKV_PDL=1 enables.
 bool pdl_enabled();
+int pdl_mode();
+// Programmatic dependent launch is used only inside a ctkv_decode_step_phase
+// call whose caller set phase bit 16 (see include/ctkv.h); this host-thread
+// flag carries that permission to launch_k for the duration of the call.
+extern thread_local int t_pdl_ok;
+struct PdlScope {
+  explicit PdlScope(bool ok) { t_pdl_ok = ok ? 1 : 0; }
+  ~PdlScope() { t_pdl_ok = 0; }
+};
 // Launch priorities (CTA dispatch order when several kernels wait for SMs):
 // the latency-critical chain kernels go first, the bandwidth-bound scans
 // last.  CTKV_PRIO=0 disables.
@@ -148,7 +158,8 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   attr[n].id = cudaLaunchAttributePriority;
   attr[n].val.priority = launch_priority(pr);
   ++n;
-  if (pdl_enabled()) {
+  const int pm = t_pdl_ok ? pdl_mode() : 0;   // 2: chain launches; 3: chain and scan launches
+  if (pm == 1 || (pm >= 2 && pr == kPrioHigh) || (pm == 3 && pr == kPrioLow)) {
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;

@@ -201,20 +201,21 @@ class DecodeEngine:
                     ls.wait_event(self._cin_ev[k][li])
                 if self._comm is not None and li > 0:
                     ls.wait_event(self._gev[k][li - 1])
-                # phase bits: 1 scan, 2 unit, 8 defer the tail, 4 tail only
+                # phase bits: 1 scan, 2 unit, 8 defer the tail, 4 tail only, 16 PDL allowed
+                # (the previous kernel on a lane stream is the previous layer's chain)
                 if self._tail_after_scan:
                     # the previous layer's tail waits until this layer's scan is
                     # done, so it shares the GPU with this chain, not this scan
-                    self._launch(L, 1, ls)
+                    self._launch(L, 1 | 16, ls)
                     if li > 0:
                         es = self._evs[k][li]
                         es.record(ls)
                         ts.wait_event(self._ev[k][li - 1])
                         ts.wait_event(es)
                         self._launch(self.lane_layers[k][li - 1], 4, ts)
-                    self._launch(L, 2 | 8, ls)
+                    self._launch(L, 2 | 8 | 16, ls)
                 else:
-                    self._launch(L, 1 | 2 | 8, ls)
+                    self._launch(L, 1 | 2 | 8 | 16, ls)
                 ev = self._ev[k][li]
                 ev.record(ls)
                 # the tail (DCU write, sparse ids, cursor/total advance) is only
