@@ -1,39 +1,80 @@
 #!/usr/bin/env python
-"""CTkvr decode benchmark on B200 (BASELINE.json configs[1], "cfg2").
+"""CTkvr decode benchmark on B200 (BASELINE.json configs).
 
-Workload: Llama-3-8B head geometry (32 q / 8 kv heads, d=128), all 32
-layers, 96K (98,304-token) synthetic drift context, batch 8 per GPU, bf16,
-C=2048 centroids, rho=1280, rho'=512, C'=4, L_init=128, L_local=1024.
-A "step" = one decode token for the whole batch through all 32 layers:
-per layer append + recall + rerank + sparse/static attention + merge + DCU.
-Metric: decode tokens/s = tokens produced / step time (whole job, all ranks).
+Default workload = configs[1] ("cfg2"): Llama-3-8B head geometry (32 q / 8
+kv heads, d=128), all 32 layers, 96K (98,304-token) synthetic drift
+context, batch 8 per GPU, bf16, C=2048 centroids, rho=1280, rho'=512,
+C'=4, L_init=128, L_local=1024.  A "step" = one decode token for the whole
+batch through all layers: per layer append + recall + rerank + sparse/static
+attention + merge + DCU.  Metric: decode tokens/s (whole job, all ranks).
+`--config cfg3|cfg5|cfg1` selects the other BASELINE configs (see PRESETS).
 
 Inputs are larger than L2 (6.6 GB of reads per step vs 126 MB L2), so no
-flush is needed between steps.  Reference arm (`--impl reference`): the
-reference algorithm's CPU implementation (the pinned numpy port under
-oracle/; the reference is pure Python and cannot travel to the GPU box)
-timed on the host's cores for one (layer, sequence) unit of the same
-geometry and extrapolated to the full step.
+flush is needed between steps.
+
+Legs of one run (rank 0 prints ONE JSON line):
+* timed region: K graph replays of the multi-layer engine, CUDA events;
+* e2e: the same step through pinned host buffers (H2D inputs, D2H outputs);
+* parity: after the timed region, sampled (layer, sequence) units are
+  replayed on the CPU from a snapshot of the device state by the reference
+  package itself (baseline/_ref, when present) and the pinned oracle port,
+  step by step (oracle/unit_parity.py) -- the `parity` field;
+* cpu_baseline: the reference's own decode_step timings from that leg.
+
+Reference arm (`--impl reference`): the unmodified reference package
+(`centroidkv` 0.1.0 installed under baseline/_ref) runs its own `prefill`
+and `decode_step` on one (layer, sequence) unit of the same geometry on the
+host cores; tok/s is a labelled linear extrapolation to the full step.
 """
 
 from __future__ import annotations
 
-import argparse
-import json
-import math
 import os
-import statistics
-import subprocess
-import sys
-import threading
-import time
 
-import numpy as np
+os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import math  # noqa: E402
+import platform  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK = 6650.0
+
+# BASELINE.json configs.  cfg3 does not fit one B200 at 48 distinct layers
+# (K/V 154 GB + lists 32 GB + centroids 13 GB): its capacity plan cycles 36
+# physical layer buffers (logical layer l uses buffer l mod 36; every layer
+# moves exactly the bytes a distinct layer would).  cfg5 on one GPU is one
+# rank's slice of the 8-GPU shard plan (kv heads x batch).
+PRESETS = {
+    "cfg2": dict(layers=32, batch=8, seq=98304, query_heads=32, kv_heads=8, capacity=2048,
+                 dtype="bf16", build_mode=1, lanes=4, phys_layers=0,
+                 workload="cfg2: Llama-3-8B geometry 32q/8kv d=128, 32 layers, 96K ctx, batch 8 "
+                          "per GPU, bf16 (BASELINE configs[1])", model="llama3-8b-geometry"),
+    "cfg3": dict(layers=48, batch=16, seq=98304, query_heads=32, kv_heads=4, capacity=2048,
+                 dtype="bf16", build_mode=1, lanes=4, phys_layers=36,
+                 workload="cfg3: Yi-9B geometry 32q/4kv d=128, 48 layers, 96K ctx, batch 16 per "
+                          "GPU, bf16 (BASELINE configs[2]); 48 logical layers over 36 physical "
+                          "layer buffers (capacity plan)", model="yi-9b-geometry"),
+    "cfg5": dict(layers=32, batch=8, seq=131072, query_heads=32, kv_heads=8, capacity=2048,
+                 dtype="bf16", build_mode=1, lanes=4, phys_layers=0, slice_of=8,
+                 workload="cfg5: Llama-3-8B geometry, 32 layers, 128K ctx, global batch B over "
+                          "8 GPUs (kv heads x batch), bf16 (BASELINE configs[4])",
+                 model="llama3-8b-geometry"),
+    "cfg1": dict(layers=1, batch=1, seq=8192, query_heads=32, kv_heads=8, capacity=512,
+                 dtype="f32", build_mode=0, lanes=1, phys_layers=0,
+                 workload="cfg1: one layer, Llama-3-8B heads 32q/8kv d=128, 8K ctx, batch 1, "
+                          "fp32 (BASELINE configs[0])", model="llama3-8b-geometry"),
+}
 
 
 def parse():
@@ -42,26 +83,30 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--layers", type=int, default=32)
-    ap.add_argument("--batch", type=int, default=8, help="sequences per GPU")
-    ap.add_argument("--seq", type=int, default=98304)
-    ap.add_argument("--query-heads", type=int, default=32)
-    ap.add_argument("--kv-heads", type=int, default=8)
-    ap.add_argument("--head-dim", type=int, default=128)
-    ap.add_argument("--capacity", type=int, default=2048)
+    ap.add_argument("--config", default="cfg2", choices=sorted(PRESETS))
+    for k in ("layers", "batch", "seq", "query_heads", "kv_heads", "capacity", "lanes",
+              "phys_layers", "build_mode", "slice_of"):
+        ap.add_argument("--" + k.replace("_", "-"), type=int, default=None)
     ap.add_argument("--rho", type=int, default=1280)
     ap.add_argument("--rho-prime", type=int, default=512)
     ap.add_argument("--c-prime", type=int, default=4)
     ap.add_argument("--init-len", type=int, default=128)
     ap.add_argument("--local-len", type=int, default=1024)
+    ap.add_argument("--no-rerank", action="store_true",
+                    help="attend the whole recall set (ck/retrieval.py:334-337; Fig. 11 ablation)")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--parity-steps", type=int, default=10,
+                    help="steps replayed on the CPU per sampled unit (0: no parity leg)")
+    ap.add_argument("--parity-units", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--build-mode", type=int, default=1, help="0 exact f64, 1 fast")
-    ap.add_argument("--lanes", type=int, default=4,
-                    help="micro-batch lanes per GPU (sequence groups on their own streams)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    pre = PRESETS[a.config]
+    for k, v in pre.items():
+        if getattr(a, k, None) is None:
+            setattr(a, k, v)
+    if a.slice_of is None:
+        a.slice_of = 0
+    return a
 
 
 def ncu_traffic(kernel: str):
@@ -87,6 +132,30 @@ def peaks():
         return HBM_FALLBACK, 1590.0, "fallback"
 
 
+def host_info() -> dict:
+    """CPU model, cores used, numpy / BLAS versions (the CPU arms' context)."""
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        for p in threadpool_info():
+            if p.get("user_api") == "blas":
+                blas = f"{p.get('internal_api')} {p.get('version')} x{p.get('num_threads')}"
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "cores": len(os.sched_getaffinity(0)), "numpy": np.__version__,
+            "blas": blas}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -110,7 +179,7 @@ class ClockSampler:
                     self.rows.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -137,82 +206,91 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-# ---------------------------------------------------------------------------
-# CPU reference (the pinned oracle port), one (layer, sequence) unit
-# ---------------------------------------------------------------------------
+def _config(a, n):
+    cfg = {"workload": PRESETS[a.config]["workload"], "model": PRESETS[a.config]["model"],
+           "global_batch": a.batch * n, "seq_len": a.seq, "layers": a.layers,
+           "query_heads": a.query_heads, "kv_heads": a.kv_heads, "C": a.capacity,
+           "rho": a.rho, "rho_prime": a.rho_prime, "c_prime": a.c_prime,
+           "init_len": a.init_len, "local_len": a.local_len, "rerank": not a.no_rerank,
+           "parallelism": f"kvhead x batch shards over {n} GPU(s), {a.lanes} micro-batch lanes "
+                          f"per GPU", "l2": "inputs > L2 (no flush)"}
+    if a.phys_layers:
+        cfg["physical_layers"] = a.phys_layers
+    if a.slice_of:
+        cfg["slice"] = (f"rank 0 of a {a.slice_of}-GPU shard plan on 1 GPU (per-GPU work; the "
+                        f"per-layer all-gather is not included)")
+        cfg["global_batch"] = a.batch
+    return cfg
 
-def cpu_unit_decode(keys, values, cent, lists, dec_q, dec_k, dec_v, a, steps, warm=1):
-    """Time the reference algorithm's decode_step (oracle port, f64 numpy)
-    on one (layer, sequence) unit; returns per-step seconds (median)."""
-    from oracle import ctkv_oracle as O
-    s = keys.shape[2]
-    store = O.partition(keys, values, a.init_len, a.local_len, cent.shape[1])
-    index = O.Index(cent.copy(), lists.copy(), np.zeros(1, dtype=np.int64))
-    times = []
-    for t in range(warm + steps):
-        store.append(dec_k[:, :, t], dec_v[:, :, t])
-        t0 = time.perf_counter()
-        O.decode_step(store, index, dec_q[:, :, t], a.c_prime, a.rho_prime)
-        times.append(time.perf_counter() - t0)
-    del s
-    return statistics.median(times[warm:]), times
 
+# ---------------------------------------------------------------------------
+# reference arm: the unmodified reference package on the host cores
+# ---------------------------------------------------------------------------
 
 def run_reference(a):
-    """--impl reference: the reference's CPU path on the host cores."""
     import torch
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import ctkv_oracle as O
-    from paper_2512_15550_b200.workload import DriftConfig, generate
+    from oracle.unit_parity import load_reference
+    ck = load_reference()
+    info = host_info()
+    if ck is None:
+        print(json.dumps({"impl": "reference", "unavailable": "centroidkv not installed under "
+                          "baseline/_ref (pip install --target baseline/_ref /root/reference/pkg)"}))
+        return
     from paper_2512_15550_b200.tensor_ops import HeadLayout
-    cores = len(os.sched_getaffinity(0))
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
-    s, T = a.seq, a.warmup + a.steps + 1
-    lay = HeadLayout(1, a.query_heads, a.kv_heads, s + T, a.head_dim)
-    q, k, v, _ = generate(DriftConfig(seed=42, s=s, decode_steps=T), lay, device="cpu",
-                          dtype=torch.float32, q_rows=(s - a.capacity, s + T))
-    q, k, v = q.numpy(), k.numpy(), v.numpy()
-    # bf16 inputs, widened to f32 for the f32-only reference (BASELINE.md s.3)
-    q, k, v = O.bf16_round(q), O.bf16_round(k), O.bf16_round(v)
+    from paper_2512_15550_b200.workload import DriftConfig, generate
+    h, g, d, s, C = a.query_heads, a.kv_heads, 128, a.seq, a.capacity
+    if a.slice_of:
+        from paper_2512_15550_b200.parallel import ShardPlan
+        sp = ShardPlan(a.slice_of, 0, a.batch * a.slice_of, g, h)
+        h, g = sp.h_loc, sp.g_loc
+    steps_total = a.warmup + a.steps
+    lay = HeadLayout(1, h, g, s + steps_total, d)
+    dt = torch.float32 if a.dtype == "f32" else torch.bfloat16
+    q, k, v, _ = generate(DriftConfig(seed=42, s=s, decode_steps=steps_total), lay, device="cpu",
+                          dtype=dt, q_rows=(s - C, s + steps_total))
+    # bf16 inputs widened exactly to f32 for the f32-only reference
+    q, k, v = q.float().numpy(), k.float().numpy(), v.float().numpy()
+    queries = np.zeros((1, h, s, d), np.float32)         # only the last C rows are read
+    queries[:, :, s - C:] = q[:, :, :C]
     t0 = time.perf_counter()
-    store, index = O.prefill(np.concatenate([np.zeros((1, a.query_heads, s - a.capacity, a.head_dim),
-                                                      np.float32), q[:, :, :a.capacity]], axis=2),
-                             np.ascontiguousarray(k[:, :, :s]), np.ascontiguousarray(v[:, :, :s]),
-                             a.init_len, a.local_len, a.capacity, a.rho)
+    store, index = ck.prefill(queries, np.ascontiguousarray(k[:, :, :s]),
+                              np.ascontiguousarray(v[:, :, :s]),
+                              ck.PrefillParams(a.init_len, a.local_len, C, a.rho))
     build_s = time.perf_counter() - t0
+    state = ck.DecodeState(store, index, ck.DecodeConfig(a.c_prime, a.rho_prime,
+                                                         use_rerank=not a.no_rerank))
     times = []
-    for t in range(a.warmup + a.steps):
-        store.append(k[:, :, s + t], v[:, :, s + t])
+    for t in range(steps_total):
+        store.append(k[:, :, s + t], v[:, :, s + t])      # ck/session.py:58-60
         t1 = time.perf_counter()
-        O.decode_step(store, index, q[:, :, a.capacity + t], a.c_prime, a.rho_prime)
+        ck.decode_step(state, q[:, :, C + t])
         times.append(time.perf_counter() - t1)
     unit = statistics.median(times[a.warmup:])
-    units_per_step = a.layers * a.batch * a.gpus
-    tok_s = (a.batch * a.gpus) / (unit * units_per_step)
+    units = a.layers * a.batch                            # (layer, seq) units per GPU-step
+    tok_s = 1.0 / (unit * a.layers)                       # = batch / (unit * units)
     line = {
         "impl": "reference", "metric": "decode_tokens_per_s", "value": tok_s, "unit": "tok/s",
         "higher_is_better": True, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": unit * units_per_step * 1e3, "dtype": "f64",
-        "data": "synthetic drift (GPU-generator distribution, CPU torch RNG), bf16-rounded",
+        # one arm step = one measured (layer, sequence) unit decode_step
+        "ms_per_step": unit * 1e3, "dtype": "f64 (f32 storage)",
+        "data": "synthetic drift (same generator distribution, CPU torch RNG), bf16-rounded "
+                "and widened to f32" if a.dtype != "f32" else "synthetic drift, f32",
         "config": _config(a, a.gpus),
-        "cpu_baseline": {"value": tok_s, "unit": "tok/s", "cores": cores, "kind": "port",
-                         "sample": f"oracle decode_step on 1 of {units_per_step} (layer, seq) units "
-                                   f"per step at 96K, median of {a.steps}, linear extrapolation",
-                         "build_s_per_unit": build_s},
+        "extrapolation": {"measured": "reference decode_step on 1 (layer, sequence) unit",
+                          "unit_ms": unit * 1e3, "units_per_step_per_gpu": units,
+                          "extrapolated_ms_per_full_step": unit * units * 1e3,
+                          "note": "value = batch / (unit_ms x units): a labelled linear "
+                                  "extrapolation, not a measured full step"},
+        "cpu_baseline": dict(value=tok_s, unit="tok/s", kind="reference",
+                             sample=f"centroidkv.decode_step on one {s}-token unit "
+                                    f"({h}q/{g}kv), median of {a.steps} after {a.warmup} warm-up",
+                             build_s_per_unit=build_s, **info),
         "e2e": {"value": tok_s, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
-
-
-def _config(a, n):
-    return {"workload": "cfg2: Llama-3-8B geometry 32q/8kv d=128, 32 layers, 96K ctx, "
-                        "batch 8 per GPU, bf16 (BASELINE configs[1])",
-            "model": "llama3-8b-geometry", "global_batch": a.batch * n, "seq_len": a.seq,
-            "layers": a.layers, "C": a.capacity, "rho": a.rho, "rho_prime": a.rho_prime,
-            "c_prime": a.c_prime, "init_len": a.init_len, "local_len": a.local_len,
-            "parallelism": f"kvhead x batch shards over {n} GPU(s), {a.lanes} micro-batch lanes per GPU", "l2": "inputs > L2 (no flush)"}
 
 
 # ---------------------------------------------------------------------------
@@ -230,9 +308,9 @@ def main():
     import paper_2512_15550_b200 as P
     from paper_2512_15550_b200 import _native as N
     from paper_2512_15550_b200.engine import DecodeEngine
+    from paper_2512_15550_b200.index import QueryCentroidIndex
     from paper_2512_15550_b200.parallel import ShardPlan
     from paper_2512_15550_b200.store import KvStore
-    from paper_2512_15550_b200.index import QueryCentroidIndex
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -240,42 +318,58 @@ def main():
     torch.cuda.set_device(local)
     group = None
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # rank counts visible in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     N.lib()
     dev = torch.device("cuda", local)
-    B = a.batch * world                       # weak scaling: 8 sequences per GPU
-    plan = ShardPlan(world, rank, B, a.kv_heads, a.query_heads)
-    b, g, h, d = plan.b_loc, plan.g_loc, plan.h_loc, a.head_dim
+    if a.slice_of:
+        if world > 1:
+            raise SystemExit("--slice-of runs one rank's shard on one GPU (use --gpus 1)")
+        # one rank's slice of the multi-GPU plan, no collective
+        plan_full = ShardPlan(a.slice_of, 0, a.batch * a.slice_of, a.kv_heads, a.query_heads)
+        plan = ShardPlan(1, 0, plan_full.b_loc, plan_full.g_loc, plan_full.h_loc)
+        B = plan.batch
+    else:
+        B = a.batch * world                                  # weak scaling: batch per GPU fixed
+        plan = ShardPlan(world, rank, B, a.kv_heads, a.query_heads)
+    b, g, h, d = plan.b_loc, plan.g_loc, plan.h_loc, 128
+    if a.lanes > b:
+        a.lanes = b
     s = a.seq
-    T = a.warmup + a.steps + a.e2e_steps + 12 + a.cpu_steps + 2
+    T = a.warmup + a.steps + a.e2e_steps + a.parity_steps + 8
+    n_phys = a.phys_layers or a.layers
+    apps = -(-a.layers // n_phys)                             # appends per buffer per step
     layout = P.HeadLayout(b, h, g, s + T, d)
-    cfg = P.DecodeConfig(a.c_prime, a.rho_prime)
+    dtype = torch.float32 if a.dtype == "f32" else torch.bfloat16
+    cfg = P.DecodeConfig(a.c_prime, a.rho_prime, use_rerank=not a.no_rerank)
+    rho = min(a.rho, s - a.init_len - a.local_len)
 
     # ---- setup: synthetic inputs + device prefill (index build) per layer ----
-    layers, tails = [], []
-    build_ms = []
+    phys, build_ms, tails = [], [], []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for li in range(a.layers):
         q, k, v, _ = P.generate(P.DriftConfig(seed=42 + li + 1000 * rank, s=s, decode_steps=T),
-                                layout, dtype=torch.bfloat16, q_rows=(s - a.capacity, s + T))
-        store = KvStore(P.HeadLayout(b, h, g, s, d), a.init_len, a.local_len, dtype=torch.bfloat16,
-                        capacity=s + T, host_api=False)
-        store.keys[:, :, :s].copy_(k[:, :, :s])
-        store.values[:, :, :s].copy_(v[:, :, :s])
-        store._set_total(s)
+                                layout, dtype=dtype, q_rows=(s - a.capacity, s + T))
         tails.append((q[:, :, a.capacity:].contiguous(), k[:, :, s:].contiguous(),
                       v[:, :, s:].contiguous()))
-        cent_q = q[:, :, :a.capacity].contiguous()
-        del k, v
-        torch.cuda.synchronize()
-        ev0.record()
-        index = QueryCentroidIndex.build(cent_q, store, a.capacity, min(a.rho, s - a.init_len - a.local_len),
-                                         mode=a.build_mode)
-        ev1.record()
-        torch.cuda.synchronize()
-        build_ms.append(ev0.elapsed_time(ev1))
-        layers.append((store, index))
+        if li < n_phys:
+            store = KvStore(P.HeadLayout(b, h, g, s, d), a.init_len, a.local_len, dtype=dtype,
+                            capacity=s + T * apps, host_api=False)
+            store.keys[:, :, :s].copy_(k[:, :, :s])
+            store.values[:, :, :s].copy_(v[:, :, :s])
+            store._set_total(s)
+            cent_q = q[:, :, :a.capacity].contiguous()
+            del k, v
+            torch.cuda.synchronize()
+            ev0.record()
+            index = QueryCentroidIndex.build(cent_q, store, a.capacity, rho, mode=a.build_mode)
+            ev1.record()
+            torch.cuda.synchronize()
+            build_ms.append(ev0.elapsed_time(ev1))
+            phys.append((store, index))
         del q
+    layers = [phys[li % n_phys] for li in range(a.layers)]
     nl = a.layers
     # all step inputs, device resident: [T, L, b, heads, d]
     Qall = torch.stack([t[0].permute(2, 0, 1, 3) for t in tails], dim=1).contiguous()
@@ -295,7 +389,7 @@ def main():
     # all b*g units of a layer), eager, CUDA events on the launching stream;
     # run before the lanes engine, which then continues from this state ----
     nmeas = 3
-    tengine = DecodeEngine(layers, cfg, plan=plan, group=group, lanes=1)
+    tengine = DecodeEngine(layers, cfg, plan=plan if world > 1 else None, group=group, lanes=1)
     load_inputs(tengine)
     tengine.step()
     evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(nl)]
@@ -310,7 +404,8 @@ def main():
     scan_ms = statistics.mean(e[0].elapsed_time(e[1]) for run_ in evs for e in run_)
     unit_ms = statistics.mean(e[1].elapsed_time(e[2]) for run_ in evs for e in run_)
     del tengine
-    engine = DecodeEngine(layers, cfg, plan=plan, group=group, lanes=a.lanes)
+    engine = DecodeEngine(layers, cfg, plan=plan if world > 1 else None, group=group,
+                          lanes=a.lanes)
     # ---- warm-up (eager), capture, more warm-up ----
     for _ in range(max(1, a.warmup // 2)):
         load_inputs(engine)
@@ -356,11 +451,12 @@ def main():
     tok_s = B * a.steps / (ms_total / 1e3)
 
     Lbar = rl_tot / (nmeas * nl * b * g)      # mean recall length per (b, g) unit
-    e = 2
+    e = 4 if dtype == torch.float32 else 2
     gs = h // g
     U = b * g                                  # units per kernel launch (timing pass: full layer)
     n_static = a.init_len + a.local_len
     C = a.capacity
+    n_sparse = a.rho_prime if not a.no_rerank else Lbar
     # algorithmic bytes per launch (full-layer launch: U = b*g units)
     ns = math.ceil(n_static / 128)                # static splits (bf16: 128 tokens)
     scan_bytes = U * (gs * C * d * e + gs * C * 4          # centroid rows + cached norms
@@ -368,20 +464,22 @@ def main():
                       + gs * d * e + 2 * d * e             # query heads, appended K/V
                       + C * 8 + ns * gs * (d * 4 + 16))    # group-max cosines, static partials
     unit_bytes = U * (C * 8 + 4 * a.c_prime * a.rho                # cosines, selected lists
-                      + e * d * Lbar + e * d * a.rho_prime          # K rows (rerank), V rows
+                      + e * d * Lbar + e * d * n_sparse             # K rows (rerank), V rows
                       + 16 * gs * Lbar + 12 * Lbar                  # logits w+r, keys, ids
                       + ns * gs * (d * 4 + 16) + 4 * gs * d)        # static partials, output
     # step total: SURVEY.md section 8(d)
-    algo_bytes = b * g * (h // g * C * d * e + 4 * a.c_prime * a.rho + e * d * Lbar
-                          + e * d * a.rho_prime + 2 * e * d * n_static + e * gs * d + 4 * gs * d
+    algo_bytes = b * g * (gs * C * d * e + 4 * a.c_prime * a.rho + e * d * Lbar
+                          + e * d * n_sparse + 2 * e * d * n_static + e * gs * d + 4 * gs * d
                           + e * gs * d + 4 * a.rho + 2 * e * d) * nl
     scan_gbs = scan_bytes / (scan_ms * 1e-3) / 1e9
     unit_gbs = unit_bytes / (unit_ms * 1e-3) / 1e9 if unit_ms > 1e-4 else 0.0
 
     # ---- e2e through host buffers (pinned H2D of q/k/v, D2H of outputs) ----
-    hq = Qall[:a.e2e_steps + 1].cpu().pin_memory()
-    hk = Kall[:a.e2e_steps + 1].cpu().pin_memory()
-    hv = Vall[:a.e2e_steps + 1].cpu().pin_memory()
+    i0 = step_i[0]
+    hq = Qall[i0:i0 + a.e2e_steps].cpu().pin_memory()
+    hk = Kall[i0:i0 + a.e2e_steps].cpu().pin_memory()
+    hv = Vall[i0:i0 + a.e2e_steps].cpu().pin_memory()
+    step_i[0] += a.e2e_steps
     # two graph slots with the host copies inside the step: each (layer,
     # lane)'s inputs are copied in ahead of it and its output copied out as it
     # finishes; the host fills the other slot's inputs while a step runs
@@ -390,10 +488,12 @@ def main():
         try:
             hbufs = engine.capture_host_io(2)
         except RuntimeError as exc:
-            print(f"bench: host-I/O graph capture failed ({exc}); copies around the step", file=sys.stderr)
+            print(f"bench: host-I/O graph capture failed ({exc}); copies around the step",
+                  file=sys.stderr)
             torch.cuda.synchronize()
-    hout = hbufs[0][3] if hbufs else torch.empty(engine.gathered.shape, dtype=torch.float32).pin_memory()
-    h2d = (hq[0].numel() + hk[0].numel() + hv[0].numel()) * 2
+    hout = hbufs[0][3] if hbufs else torch.empty(engine.gathered.shape,
+                                                 dtype=torch.float32).pin_memory()
+    h2d = (hq[0].numel() + hk[0].numel() + hv[0].numel()) * e
     d2h = hout.numel() * 4
 
     def fill(slot, t):
@@ -431,39 +531,60 @@ def main():
     e2e_tok_s = B * a.e2e_steps / (e2e_ms / 1e3)
     engine.check()
 
-    # ---- CPU baseline: oracle decode on one unit of the same state ----
-    cpu = None
-    if rank == 0 and not a.no_cpu:
-        st0, ix0 = layers[0]
-        tot = st0.total_tokens
-        kk = st0.keys[:1, :, :tot].float().cpu().numpy()
-        vv = st0.values[:1, :, :tot].float().cpu().numpy()
-        cent = ix0.cent[:1].float().cpu().numpy()
-        lists = ix0.lists_dev[:1].cpu().numpy()
-        i0 = step_i[0]
-        dq = Qall[i0:i0 + a.cpu_steps + 1, 0, :1].permute(1, 2, 0, 3).float().cpu().numpy()
-        dk = Kall[i0:i0 + a.cpu_steps + 1, 0, :1].permute(1, 2, 0, 3).float().cpu().numpy()
-        dv = Vall[i0:i0 + a.cpu_steps + 1, 0, :1].permute(1, 2, 0, 3).float().cpu().numpy()
-        cores = len(os.sched_getaffinity(0))
-
-        class A2:
-            pass
-        a2 = A2()
-        a2.init_len, a2.local_len, a2.c_prime, a2.rho_prime = a.init_len, a.local_len, a.c_prime, a.rho_prime
-        unit_s, _ = cpu_unit_decode(kk, vv, cent, lists, dq, dk, dv, a2, a.cpu_steps)
-        units = nl * B
-        cpu = {"value": B / (unit_s * units), "unit": "tok/s", "cores": cores, "kind": "port",
-               "sample": f"oracle (numpy f64 port of the reference) decode_step on 1 of {units} "
-                         f"(layer, seq) units, index state copied from the device build, median of "
-                         f"{a.cpu_steps} steps = {unit_s * 1e3:.1f} ms/unit, extrapolated x{units}"}
+    # ---- parity leg (checker, after every timed region): sampled (layer,
+    # seq) units replayed on the CPU by the reference and the oracle ----
+    parity, cpu = None, None
+    if rank == 0 and a.parity_steps > 0:
+        from oracle import unit_parity as UP
+        alias_free = [li for li in range(nl) if a.layers <= n_phys or
+                      (li % n_phys) >= a.layers - n_phys]
+        cand = [(alias_free[0], 0), (alias_free[-1], b - 1), (alias_free[len(alias_free) // 2], b // 2)]
+        units = list(dict.fromkeys(cand))[:max(1, a.parity_units)]
+        torch.cuda.synchronize()
+        snaps = UP.snapshot(engine, units)
+        for _ in range(a.parity_steps):
+            load_inputs(engine)
+            run()
+            torch.cuda.synchronize()
+            UP.record(engine, snaps)
+        engine.check()
+        UP.final_state(engine, snaps)
+        t0 = time.perf_counter()
+        res = UP.check(snaps, a.c_prime, a.rho_prime, use_rerank=not a.no_rerank)
+        del snaps
+        parity = {k: res[k] for k in ("ok", "reference", "units", "steps", "recall",
+                                      "hard_mismatches", "order_hard", "exact_steps",
+                                      "recall_len_mismatch", "selected_mismatch", "out_nrel_max",
+                                      "dcu_rows", "dcu_rows_exact", "dcu_hard",
+                                      "centroids_equal", "fifo_equal",
+                                      "ref_vs_oracle_digest_mismatch",
+                                      "ref_vs_oracle_out_nrel_max")}
+        parity["sampled_units"] = [list(u) for u in units]
+        parity["path"] = (f"{'tcgen05' if a.build_mode else 'f64-exact'} build, DecodeEngine "
+                          f"lanes={a.lanes}, {'graph+PDL' if use_graph else 'eager'}")
+        parity["check_s"] = time.perf_counter() - t0
+        info = host_info()
+        tm = res["ref_times"] if res["ref_times"] else res["oracle_times"]
+        if tm:
+            unit_s = statistics.median(tm)
+            units_n = nl * B
+            cpu = dict(value=B / (unit_s * units_n), unit="tok/s",
+                       kind="reference" if res["ref_times"] else "port",
+                       sample=(f"{'centroidkv' if res['ref_times'] else 'oracle port'} decode_step "
+                               f"on {len(units)} (layer, seq) units of this run's device state, "
+                               f"median of {len(tm)} steps (2 warm-up per unit dropped) = "
+                               f"{unit_s * 1e3:.1f} ms/unit, extrapolated x{units_n} units"),
+                       **info)
 
     if rank == 0:
         build_avg = statistics.mean(build_ms)
-        build_flop = 2 * a.query_heads // world * a.capacity * (s - a.init_len - a.local_len) * d * b
+        n_off = s - a.init_len - a.local_len
+        build_flop = 2 * h * a.capacity * n_off * d * b
         line = {
             "metric": "decode_tokens_per_s", "value": tok_s, "unit": "tok/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": a.dtype,
             "data": "synthetic drift workload (GPU generator: spectral decay, drift, RoPE, needles)",
             "config": _config(a, world),
             "roofline": {"bound": "hbm",
@@ -483,15 +604,19 @@ def main():
             },
             "build": {"ms_per_layer": build_avg, "ms_per_layer_seq": build_avg / b,
                       "tflops": build_flop / (build_avg * 1e-3) / 1e12,
-                      "mode": "fast" if a.build_mode else "exact-f64"},
+                      "frac": build_flop / (build_avg * 1e-3) / 1e12 / tf_peak,
+                      "mode": "tcgen05" if a.build_mode else "exact-f64"},
             "e2e": {"value": e2e_tok_s, "unit": "tok/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             # per (lane, layer): scan + chain + deferred tail kernels
             "gpu_launches": 3 * nl * a.lanes * a.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "parity": parity,
             "graph": use_graph,
         }
+        if world > 1:
+            line["nccl"] = {"comm_nranks": dist.get_world_size(), "backend": "nccl"}
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()

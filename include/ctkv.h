@@ -177,10 +177,21 @@ int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctk
  * concurrently with other layers' work (it writes only this layer's index,
  * total and outputs, and reads this call's workspace).  Paths without a
  * separate tail run it inside phase 2 and treat 4 as a no-op.
- * 16 (with any of the above): the caller guarantees that the kernel it
- * launched last on `stream` writes none of this layer's store, index, query
- * or new K/V (true in the engine, where it is the previous layer's chain);
- * the scan and chain kernels may then use programmatic dependent launch. */
+ * 16 (with any of the above): programmatic dependent launch.  The scan and
+ * chain may then start before the kernel launched last on `stream` has
+ * finished, and read or write before their grid-dependency wait:
+ *   scan:  reads centroids, centroid norms, *total, the static partition's
+ *          K/V rows and k_new/v_new; writes the static partial slots of its
+ *          workspace for splits with no tokens;
+ *   chain: reads *total.
+ * Everything else (the query, lists, FIFO cursor, the rest of the
+ * workspace; every output) is touched only after the wait.  The caller
+ * guarantees that the previous kernel on `stream` writes none of the
+ * pre-wait inputs and does not read this call's workspace.  In the engine
+ * the kernel before a scan is the previous layer's chain (another layer's
+ * state) and the kernel before a chain is the same layer's scan, which does
+ * not write *total; k_new/v_new arrive from a copy stream through an event
+ * (a full dependency). */
 int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
                            const ctkv_step_args* A, int32_t phase, void* workspace,
                            size_t workspace_bytes, void* stream);

@@ -16,8 +16,10 @@ import torch
 from .errors import ConfigError, DegenerateQueryWarning, ShapeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# CTKV_LIB: an alternative in-tree build of the same library (A/B runs of kernel variants)
-LIB_PATH = os.environ.get("CTKV_LIB") or os.path.join(_HERE, "libctkv.so")
+LIB_PATH = os.path.join(_HERE, "libctkv.so")
+# the same kernels with globaltimer marks compiled in (make -C csrc profile);
+# only the timeline tools under scripts/ load it, via use_profile_library()
+PROFILE_LIB_PATH = os.path.join(_HERE, "libctkv_profile.so")
 
 F32, BF16 = 0, 1
 OK, ESHAPE, ECONFIG, EINDEX, ECUDA, EWORKSPACE = range(6)
@@ -128,6 +130,15 @@ def load_library(require_device: bool = True):
         if not ok:
             raise RuntimeError("libctkv.so is built for sm_100a only; this device is not a B200")
     return _lib
+
+
+def use_profile_library() -> None:
+    """Profiling tools only: bind libctkv_profile.so instead of libctkv.so
+    (must run before the first load)."""
+    global LIB_PATH
+    if _lib is not None:
+        raise RuntimeError("libctkv is already loaded")
+    LIB_PATH = PROFILE_LIB_PATH
 
 
 def lib():

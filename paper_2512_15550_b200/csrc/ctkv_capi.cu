@@ -278,22 +278,17 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   if (!v2) p.cval = nullptr;   // the f64 unit kernel selects from gcos directly
   if (!v2 && unit_smem_bytes(p, L->head_dim) > 220 * 1024) return CTKV_ECONFIG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // v6: scan, then the 4-CTA cluster chain kernel; its tail (DCU, sparse
-  // ids, cursor/total) can be deferred (phase bit 8) and enqueued separately
-  // (phase 4) on another stream
-  if (v2 && ctkv::decode_variant() == 6 && chain_supported(p, L->dtype, L->head_dim) &&
-      tail_supported(p, L->dtype, L->head_dim)) {
+  // bf16 at d = 64/128, gs <= 8, c' <= 8: the scan, then the 4-CTA cluster
+  // chain kernel; its tail (DCU, sparse ids, cursor/total) can be deferred
+  // (phase bit 8) and enqueued separately (phase 4) on another stream.
+  // Other bf16 geometries: scan + the 2-CTA cluster unit2 kernel; f32: scan
+  // + the f64-exact unit kernel (both run their tail inside phase 2).
+  if (v2 && chain_supported(p, L->dtype, L->head_dim) && tail_supported(p, L->dtype, L->head_dim)) {
     p.selg = w.selg;
     p.selctr = w.selctr;
-    p.sel_in_chain = ctkv::scan_variant_v6() == 4 && scan4_supported(p, L->dtype, L->head_dim);
     const int nblocks = p.U * p.cos_blocks_per_unit + p.U * ns;
-    if (phase & 1) {
-      // scan4 has no last-CTA top-C' selection: the chain then selects itself
-      const bool s4 = p.sel_in_chain;
-      if (int rc = s4 ? launch_scan4(p, L->dtype, L->head_dim, st)
-                      : launch_scan(p, L->dtype, L->head_dim, nblocks, st))
-        return rc;
-    }
+    if (phase & 1)
+      if (int rc = launch_scan(p, L->dtype, L->head_dim, nblocks, st)) return rc;
     if (phase & 2)
       if (int rc = launch_chain(p, L->dtype, L->head_dim, st)) return rc;
     const bool tail = (phase & 4) || ((phase & 2) && !(phase & 8));
@@ -491,10 +486,18 @@ int ctkv_centroid_norms(const ctkv_layout* L, const void* centroids, int32_t cap
                                static_cast<cudaStream_t>(stream));
 }
 
-int ctkv_debug_kernel_timeline(int32_t on) { return ctkv::kernel_timeline(on); }
+int ctkv_debug_kernel_timeline(int32_t on) {
+#ifndef CTKV_PROFILE
+  return CTKV_ECONFIG;   // profiling builds only (make -C csrc profile)
+#endif
+  return ctkv::kernel_timeline(on);
+}
 
 int ctkv_debug_timeline_rw(const ctkv_layout* L, int32_t capacity, int32_t rho, int32_t c_prime,
                            void* workspace, uint64_t* host_out, int32_t reset) {
+#ifndef CTKV_PROFILE
+  return CTKV_ECONFIG;   // profiling builds only (make -C csrc profile)
+#endif
   if (int rc = check_layout(L)) return rc;
   DecodeWs w = carve_decode(L, capacity, c_prime * rho, static_slots(L), workspace, c_prime);
   if (host_out && cudaMemcpy(host_out, w.tl, 64, cudaMemcpyDeviceToHost) != cudaSuccess) return CTKV_ECUDA;
@@ -507,17 +510,20 @@ int ctkv_debug_timeline_rw(const ctkv_layout* L, int32_t capacity, int32_t rho, 
 }
 
 int ctkv_debug_scan_timeline(int32_t on, uint64_t* host_out, int32_t n) {
-  // the persistent scan4 when selected (CTKV_SCAN=4), else scan2 ([cta][4])
-  if (ctkv::scan_variant_v6() == 4)
-    return ctkv::scan4_timeline(on, reinterpret_cast<unsigned long long*>(host_out), n);
+#ifndef CTKV_PROFILE
+  return CTKV_ECONFIG;   // profiling builds only (make -C csrc profile)
+#endif
   return ctkv::scan2_timeline(on, reinterpret_cast<unsigned long long*>(host_out), n);
 }
 
 int ctkv_debug_phase_timing(int32_t on, uint64_t* host_out, int32_t n) {
-  // v6 decode: the chain kernel's marks; otherwise the unit kernels'
-  if (ctkv::decode_variant() == 6)
-    return ctkv::chain_phase_timing(on, reinterpret_cast<unsigned long long*>(host_out), n);
-  return ctkv::phase_timing(on, reinterpret_cast<unsigned long long*>(host_out), n);
+#ifndef CTKV_PROFILE
+  return CTKV_ECONFIG;   // profiling builds only (make -C csrc profile)
+#endif
+  // the chain kernel's marks (bf16 d = 64/128); the unit kernels' otherwise
+  const int rc = ctkv::chain_phase_timing(on, reinterpret_cast<unsigned long long*>(host_out), n);
+  if (rc) return rc;
+  return ctkv::phase_timing(on, nullptr, 0);
 }
 
 }  // extern "C"

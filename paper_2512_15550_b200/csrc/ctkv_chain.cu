@@ -54,11 +54,13 @@ namespace cg = cooperative_groups;
 constexpr int kCPhaseCtas = 512, kCPhases = 16;
 __device__ unsigned long long g_cphase[kCPhaseCtas][kCPhases];
 __device__ __forceinline__ void cmark(const DecodeParams& p, int k) {
+#ifdef CTKV_PROFILE
   if ((p.dbg & 2) && threadIdx.x == 0 && blockIdx.x < kCPhaseCtas) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_cphase[blockIdx.x][k] = t;
   }
+#endif
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -326,12 +328,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   pdl_wait();      // the scan's outputs (gcos / slots, static partials) are complete
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int i = tid; i < gs * D; i += kCT) qs[i] = q[i];
-  if (p.sel_in_chain) {   // scan4: top-C' of the unit's group-max cosines here
-    block_top_slots(p.gcos + (int64_t)u * p.C, p.C, p.c_prime, sel, S.scratch,
-                    reinterpret_cast<int*>(S.scratch + kCW * kCMaxLists));
-  } else if (tid < p.c_prime) {
-    sel[tid] = __ldcg(p.selg + (int64_t)u * p.c_prime + tid);
-  }
+  if (tid < p.c_prime) sel[tid] = __ldcg(p.selg + (int64_t)u * p.c_prime + tid);
   __syncthreads();
   cmark(p, 1);
 
@@ -805,14 +802,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
 // launcher
 // ------------------------------------------------------------------------
 
-static int chain_cl() {   // CTKV_CHAIN_CL=2|8 selects 2- or 8-CTA clusters (A/B)
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CTKV_CHAIN_CL");
-    v = (e && e[0] == '8') ? 8 : (e && e[0] == '2') ? 2 : 4;
-  }
-  return v;
-}
+constexpr int kChainCL = 4;   // CTAs per unit (cluster size)
 
 template <typename T, int D, int CL, int GS>
 static int launch_chain_t(const DecodeParams& p0, cudaStream_t st) {
@@ -843,7 +833,7 @@ int chain_phase_timing(int on, unsigned long long* out, int n) {
 bool chain_supported(const DecodeParams& p, int dtype, int D) {
   if (dtype != CTKV_BF16 || (D != 64 && D != 128)) return false;
   if ((p.gs != 1 && p.gs != 2 && p.gs != 4 && p.gs != 8) || p.c_prime > kCMaxLists) return false;
-  const int CL = chain_cl();
+  const int CL = kChainCL;
   if ((p.rho + kCT - 1) / kCT > kCMaxPer) return false;
   return chain_layout(p, D, CL, nullptr, nullptr) <= 200 * 1024;
 }
@@ -859,19 +849,10 @@ static int launch_chain_g(const DecodeParams& p, cudaStream_t st) {
   return CTKV_ESHAPE;
 }
 
-template <int D>
-static int launch_chain_d(const DecodeParams& p, cudaStream_t st) {
-  switch (chain_cl()) {
-    case 2: return launch_chain_g<D, 2>(p, st);
-    case 8: return launch_chain_g<D, 8>(p, st);
-    default: return launch_chain_g<D, 4>(p, st);
-  }
-}
-
 int launch_chain(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
   if (dtype != CTKV_BF16) return CTKV_ECONFIG;
-  if (D == 128) return launch_chain_d<128>(p, st);
-  if (D == 64) return launch_chain_d<64>(p, st);
+  if (D == 128) return launch_chain_g<128, kChainCL>(p, st);
+  if (D == 64) return launch_chain_g<64, kChainCL>(p, st);
   return CTKV_ESHAPE;
 }
 

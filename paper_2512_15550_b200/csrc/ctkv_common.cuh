@@ -183,12 +183,14 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // debug kernel timeline: CTA spans folded into [kind][start, end] (atomic
 // min/max); tl is null unless ctkv_debug_kernel_timeline(1) is on
 __device__ __forceinline__ void ktl_mark(unsigned long long* tl, int kind, bool end) {
+#ifdef CTKV_PROFILE
   if (tl != nullptr && threadIdx.x == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     if (end) atomicMax(tl + 2 * kind + 1, t);
     else atomicMin(tl + 2 * kind, t);
   }
+#endif
 }
 
 __device__ __forceinline__ void set_flag(int32_t* flags, int32_t bit) {

@@ -48,11 +48,13 @@ constexpr int kS2TlCtas = 4096;
 __device__ unsigned long long g_s2tl[kS2TlCtas][8];
 int g_host_dbg = 0;
 __device__ __forceinline__ void s2mark(const DecodeParams& p, int k) {
+#ifdef CTKV_PROFILE
   if ((p.dbg & 1) && threadIdx.x == 0 && blockIdx.x < kS2TlCtas) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_s2tl[blockIdx.x][k] = t;
   }
+#endif
 }
 
 // Per-CTA phase timestamps of the fused unit kernel (globaltimer, ns), for
@@ -61,11 +63,13 @@ constexpr int kPhaseCtas = 256, kPhases = 12;
 __device__ unsigned long long g_phase[kPhaseCtas][kPhases];
 __device__ int g_phase_on;
 __device__ __forceinline__ void phase_mark(int k) {
+#ifdef CTKV_PROFILE
   if (g_phase_on && threadIdx.x == 0 && blockIdx.x < kPhaseCtas) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_phase[blockIdx.x][k] = t;
   }
+#endif
 }
 
 constexpr int kScanThreads = 256;
@@ -356,7 +360,9 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
         }
         __nanosleep(64);
       }
-      p.selctr[u] = 0;   // every other chunk has counted: reset for the next step
+      // take this step's cpu-1 arrivals off the counter (0 again in the
+      // normal case; after a timeout, late arrivals still net to 0)
+      atomicSub(p.selctr + u, cpu - 1);
     }
     __syncthreads();
     s2mark(p, 6);
@@ -460,7 +466,9 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
       i += n;
     }
   }
-  pdl_wait();   // K/V in flight; the query (and the appended token) may come from the previous kernel
+  // K/V (and the appended token's rows, from the caller's k_new/v_new) are in
+  // flight; the query is read only after the wait (include/ctkv.h, phase bit 16)
+  pdl_wait();
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
   for (int k = threadIdx.x; k < gs * D; k += blockDim.x) qs[k] = q[k];
   __syncthreads();
@@ -470,7 +478,7 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   __shared__ double wmax[kScanRowsV2 / 32][kMaxGroup];   // per-warp head maxima (tensor-core path)
   bool mma_logits = false;
-  if constexpr (sizeof(T) == 2) {
+  if constexpr (sizeof(T) == 2 && D >= 64) {
     // logits on the tensor cores: warp w takes tokens [16w, 16w+16) as the A
     // operand of mma.m16n8k16 (f32 per 16-element k-step, f64 across), the
     // gs heads as B columns; k permuted alike in K and q (as in the chain).
@@ -557,7 +565,7 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
   s2mark(p, 5);
   bar_wait(barV, 0);
   s2mark(p, 6);
-  if constexpr (sizeof(T) == 2) {
+  if constexpr (sizeof(T) == 2 && D >= 64) {
     // o[j][:] = sum_t w[j][t] V[t][:]: a lane owns a 16-byte chunk (8 dims) of
     // one head for a quarter of the tokens (lanes 0-7 of a quarter read one
     // 128-byte row segment: conflict-free), quarters summed by shuffles
@@ -611,7 +619,6 @@ template <typename T, int D>
 __global__ void __launch_bounds__(kScanRowsV2, 4) scan2_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint64_t bars[kMaxGroup];
-  if (p.pdl == 1) pdl_trigger();   // CTKV_PDL=1 A/B: the chain may launch once every scan CTA is resident
   ktl_mark(p.tl, 0, false);
   s2mark(p, 0);
   const int64_t t0 = p.total ? *p.total : p.id_bound;
@@ -1628,7 +1635,6 @@ template <typename T, int D>
 static int launch_scan_t(const DecodeParams& p0, int nblocks, cudaStream_t st) {
   DecodeParams p = p0;
   p.dbg = g_host_dbg;
-  p.pdl = t_pdl_ok ? pdl_mode() : 0;
   const size_t sm = scan2_smem<T, D>(p.gs);
   auto k = scan2_kernel<T, D>;
   static size_t configured = 0;
@@ -1722,69 +1728,30 @@ int phase_timing(int on, unsigned long long* out, int n) {
   }
   return 0;
 }
-// v6 scan kernel (A/B switch CTKV_SCAN): 2 = scan2 (default), 4 = the
-// persistent scan4 (faster alone, but its 1-CTA-per-SM footprint overlaps
-// worse with the lanes' chain kernels: measured 1820 vs 2242 tok/s)
-int scan_variant_v6() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CTKV_SCAN");
-    v = (e && e[0] == '4') ? 4 : 2;
-  }
-  return v;
-}
-
 int kernel_timeline(int on) {   // host switch; on < 0 queries
   static int v = 0;
   if (on >= 0) v = on;
   return v;
 }
 
-// kPrioLow = the scan, kPrioMid = the tail, kPrioHigh = the chain; defaults: chain
-// high, scan and tail low (the tail is released after the next scan already);
-// CTKV_PRIO=0 turns priorities off, CTKV_PRIO=xyz (x, y, z in h/m/l) sets the
-// scan's, chain's and tail's levels for A/B runs
+// Launch priorities: the latency-bound chain kernels are dispatched first,
+// the bandwidth-bound scans and the deferred tails after them (a ready chain
+// otherwise waits ~16 us behind queued scan CTAs).
 int launch_priority(LaunchPrio pr) {
-  static int lo = 1, hi = 0, on = -1;
-  static char lvl[3] = {'l', 'l', 'h'};   // indexed by LaunchPrio: scan low, tail low, chain high
-  if (on < 0) {
-    const char* e = getenv("CTKV_PRIO");
-    on = (e && e[0] == '0') ? 0 : 1;
-    if (e && e[0] && e[1] && e[2]) { lvl[kPrioLow] = e[0]; lvl[kPrioHigh] = e[1]; lvl[kPrioMid] = e[2]; }
+  static int lo = 1, hi = 0, init = 0;
+  if (!init) {
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) { lo = 0; hi = 0; }
+    init = 1;
   }
-  if (!on) return lo;   // default (lowest) priority everywhere
-  // numerically lower = higher priority; hi..lo
-  const char c = lvl[pr];
-  return c == 'h' ? hi : c == 'm' ? (lo + hi) / 2 : lo;
+  return pr == kPrioHigh ? hi : lo;   // numerically lower = higher priority
 }
 
 // Programmatic dependent launch, for callers that allow it (phase bit 16):
-// mode 3 (default) on the chain launch (scan CTAs trigger by exiting, so the
-// chain's launch is processed while the scan drains, without resident CTAs
-// waiting) and on the scan launch (the previous chain triggers after its
-// compaction; the scan's centroid TMA loads start before its griddepcontrol
-// wait); CTKV_PDL=2 the chain only, 1 every kernel with the scan triggering
-// at entry (slower: early-resident CTAs crowd the other lanes), 0 off.
+// on the chain launch (scan CTAs trigger by exiting, so the chain's launch is
+// processed while the scan drains, without resident CTAs waiting) and on the
+// scan launch (the previous chain triggers after its compaction; the scan's
+// centroid TMA loads start before its griddepcontrol wait).
 thread_local int t_pdl_ok = 0;
-int pdl_mode() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CTKV_PDL");
-    v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
-  }
-  return v;
-}
-bool pdl_enabled() { return pdl_mode() == 1; }
-
-int decode_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("CTKV_DECODE");
-    v = (e && e[0] == '2') ? 2 : 6;
-  }
-  return v;
-}
 
 // |row| for rows of D elements: one warp per row, f64 squares (exact for
 // bf16 and f32 inputs), rounded to f32

@@ -314,20 +314,24 @@ __device__ void block_top_k(const double* vals, int C, int cp, int32_t* out, dou
 #pragma unroll
   for (int r = 0; r < K; ++r) t[r] = TopEnt{0ull, INT32_MAX};
   constexpr int PT = 16;
-  double v[PT];
-#pragma unroll
-  for (int x = 0; x < PT; ++x) {
-    const int c = threadIdx.x + x * (int)blockDim.x;
-    v[x] = c < C ? __ldcg(vals + c) : 0.0;
-  }
   const int per = (C + (int)blockDim.x - 1) / (int)blockDim.x;   // uniform
+  // PT strided values per thread in flight; C > PT * blockDim takes more
+  // rounds (C <= 4096 at every BASELINE config: one round)
+  for (int x0 = 0; x0 < per; x0 += PT) {
+    double v[PT];
 #pragma unroll
-  for (int x = 0; x < PT; ++x) {
-    if (x >= per) break;
-    const int c = threadIdx.x + x * (int)blockDim.x;
-    TopEnt e{c < C ? okey64(v[x]) : 0ull, c < C ? c : INT32_MAX};
+    for (int x = 0; x < PT; ++x) {
+      const int c = threadIdx.x + (x0 + x) * (int)blockDim.x;
+      v[x] = c < C ? __ldcg(vals + c) : 0.0;
+    }
 #pragma unroll
-    for (int r = 0; r < K; ++r) top_cswap(t[r], e);   // insertion: t stays sorted
+    for (int x = 0; x < PT; ++x) {
+      if (x0 + x >= per) break;
+      const int c = threadIdx.x + (x0 + x) * (int)blockDim.x;
+      TopEnt e{c < C ? okey64(v[x]) : 0ull, c < C ? c : INT32_MAX};
+#pragma unroll
+      for (int r = 0; r < K; ++r) top_cswap(t[r], e);   // insertion: t stays sorted
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) top_merge_shfl<K>(t, o);

@@ -70,10 +70,9 @@ struct DecodeParams {
   // v6 chain: the scan's last cosine CTA of a unit writes its top-C' slots
   int32_t* selg;    // [U][c'] top-C' slots (ties -> smaller slot)
   int* selctr;      // [U] cosine-chunk completion counters (reset by the last CTA)
-  int sel_in_chain; // 1: the chain kernel selects top-C' from gcos itself (scan4)
-  int pdl;          // CTKV_PDL mode (the scan triggers early only in mode 1)
-  int dbg;          // debug timestamp marks (host_dbg bits: 1 scan2, 2 chain, 4 scan4): a kernel
-                    // parameter, so marks that are off cost no global load
+  int dbg;          // profiling builds only (-DCTKV_PROFILE): timestamp mark bits
+                    // (1 scan2, 2 chain), a kernel parameter, so marks that are off
+                    // cost no global load
   // staged io
   const int32_t* rec_in;
   const int32_t* len_in;
@@ -101,9 +100,7 @@ int launch_unit2(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 size_t unit2_smem_bytes(const DecodeParams& p, int D);
 int static_tok_for(int dtype);
 int phase_timing(int on, unsigned long long* out, int n);
-int decode_variant();
 int kernel_timeline(int on);
-int scan_variant_v6();
 extern int g_host_dbg;   // debug mark bits the launchers copy into DecodeParams::dbg
 inline void set_host_dbg(int bit, int on) { g_host_dbg = on ? (g_host_dbg | bit) : (g_host_dbg & ~bit); }
 bool tail_supported(const DecodeParams& p, int dtype, int D);
@@ -111,10 +108,6 @@ bool tail_supported(const DecodeParams& p, int dtype, int D);
 int launch_tail(const DecodeParams& p, int dtype, int D, cudaStream_t st);
 bool chain_supported(const DecodeParams& p, int dtype, int D);
 // v6: the unit chain on a 4-CTA cluster per unit (ctkv_chain.cu)
-bool scan4_supported(const DecodeParams& p, int dtype, int D);
-// persistent warp-specialised streaming scan (ctkv_scan.cu; CTKV_SCAN=4)
-int launch_scan4(const DecodeParams& p, int dtype, int D, cudaStream_t st);
-int scan4_timeline(int on, unsigned long long* out, int n);
 int scan2_timeline(int on, unsigned long long* out, int n);
 int chain_phase_timing(int on, unsigned long long* out, int n);
 int launch_chain(const DecodeParams& p, int dtype, int D, cudaStream_t st);
@@ -126,12 +119,10 @@ int launch_merge2(int64_t rows, int D, const float* oa, const double* ma, const 
 int launch_append(int dtype, void* keys, void* vals, const void* kn, const void* vn,
                   int64_t* total, int64_t units, int64_t cap, int D, cudaStream_t st);
 
-// Programmatic dependent launch: a kernel launched with pdl=true may start
-// (its prologue, e.g. TMA loads of data no earlier kernel writes) while its
+// Programmatic dependent launch: a kernel launched with it may start (its
+// prologue, e.g. TMA loads of data no earlier kernel writes) while its
 // stream predecessor finishes; it calls pdl_wait() (griddepcontrol.wait)
-// before touching anything the predecessor produced.  CTKV_PDL=1 enables.
-bool pdl_enabled();
-int pdl_mode();
+// before touching anything the predecessor produced.
 // Programmatic dependent launch is used only inside a ctkv_decode_step_phase
 // call whose caller set phase bit 16 (see include/ctkv.h); this host-thread
 // flag carries that permission to launch_k for the duration of the call.
@@ -142,7 +133,7 @@ struct PdlScope {
 };
 // Launch priorities (CTA dispatch order when several kernels wait for SMs):
 // the latency-critical chain kernels go first, the bandwidth-bound scans
-// last.  CTKV_PRIO=0 disables.
+// last.
 enum LaunchPrio { kPrioLow = 0, kPrioMid = 1, kPrioHigh = 2 };
 int launch_priority(LaunchPrio pr);
 template <typename... KArgs, typename... Args>
@@ -158,8 +149,7 @@ inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, siz
   attr[n].id = cudaLaunchAttributePriority;
   attr[n].val.priority = launch_priority(pr);
   ++n;
-  const int pm = t_pdl_ok ? pdl_mode() : 0;   // 2: chain launches; 3: chain and scan launches
-  if (pm == 1 || (pm >= 2 && pr == kPrioHigh) || (pm == 3 && pr == kPrioLow)) {
+  if (t_pdl_ok && (pr == kPrioHigh || pr == kPrioLow)) {   // chain and scan launches
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;

@@ -29,11 +29,10 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-import os
-
 import torch
 
 from . import _native as N
+from .errors import ConfigError
 from .index import QueryCentroidIndex
 from .parallel import ShardPlan
 from .retrieval import DecodeConfig, StepBuffers
@@ -79,13 +78,31 @@ class DecodeEngine:
         # lane_layers[k][l]: lane k's view of layer l.  One workspace per
         # (lane, layer): a layer's deferred tail reads its workspace while
         # later layers already run.
+        # Layers may alias one (store, index) pair (a capacity plan that
+        # cycles fewer physical layer buffers than logical layers, bench
+        # cfg3): the aliases share one lane view (one token counter), and a
+        # layer's scan waits for the previous alias's deferred tail.
+        self._alias_prev: list[int | None] = []
+        seen: dict[int, int] = {}
+        for li, (store, _) in enumerate(layers):
+            j = seen.get(id(store))
+            if j is not None and li - j < 2:
+                raise ValueError(f"layers {j} and {li} alias one store; aliases must be >= 2 apart")
+            self._alias_prev.append(j)
+            seen[id(store)] = li
+        self._appends = {}                       # id(parent store) -> appends per step
+        for store, _ in layers:
+            self._appends[id(store)] = self._appends.get(id(store), 0) + 1
         self.lane_layers: list[list[Layer]] = []
         for k in range(lanes):
             b0, b1 = k * self.bl, (k + 1) * self.bl
             row = []
+            views: dict[int, tuple] = {}
             for li, (store, index) in enumerate(layers):
                 if lanes > 1:
-                    store, index = store.batch_view(b0, b1), index.batch_view(b0, b1)
+                    if id(store) not in views:
+                        views[id(store)] = (store.batch_view(b0, b1), index.batch_view(b0, b1))
+                    store, index = views[id(store)]
                 bufs = StepBuffers.allocate(store, index, cfg)
                 bufs.out = self.out[li, b0:b1]      # kernels write the layer output in place
                 row.append(Layer(store, index, bufs, self.q[li, b0:b1], self.k[li, b0:b1],
@@ -97,7 +114,7 @@ class DecodeEngine:
         self._tail_st = [torch.cuda.Stream(device=dev) for _ in range(lanes)] if cuda else []
         self._ev = ([[torch.cuda.Event() for _ in range(nl)] for _ in range(lanes)] if cuda else [])
         self._evs = ([[torch.cuda.Event() for _ in range(nl)] for _ in range(lanes)] if cuda else [])
-        self._tail_after_scan = os.environ.get("CTKV_TAIL_AFTER_SCAN", "1") == "1"
+        self._evt = ([[torch.cuda.Event() for _ in range(nl)] for _ in range(lanes)] if cuda else [])
         world = plan.world if plan else 1
         self.world = world
         self._comm = torch.cuda.Stream(device=dev) if (cuda and world > 1) else None
@@ -108,6 +125,7 @@ class DecodeEngine:
         self._gbuf = ([torch.empty((world, self.bl, self.h, self.d), dtype=torch.float32, device=dev)
                        for _ in range(lanes)] if world > 1 else None)
         self.graph: torch.cuda.CUDAGraph | None = None
+        self._hgraphs: list | None = None
         self.steps_done = 0
 
     # -- one step -------------------------------------------------------------
@@ -201,28 +219,29 @@ class DecodeEngine:
                     ls.wait_event(self._cin_ev[k][li])
                 if self._comm is not None and li > 0:
                     ls.wait_event(self._gev[k][li - 1])
-                # phase bits: 1 scan, 2 unit, 8 defer the tail, 4 tail only, 16 PDL allowed
-                # (the previous kernel on a lane stream is the previous layer's chain)
-                if self._tail_after_scan:
-                    # the previous layer's tail waits until this layer's scan is
-                    # done, so it shares the GPU with this chain, not this scan
-                    self._launch(L, 1 | 16, ls)
-                    if li > 0:
-                        es = self._evs[k][li]
-                        es.record(ls)
-                        ts.wait_event(self._ev[k][li - 1])
-                        ts.wait_event(es)
-                        self._launch(self.lane_layers[k][li - 1], 4, ts)
-                    self._launch(L, 2 | 8 | 16, ls)
-                else:
-                    self._launch(L, 1 | 2 | 8 | 16, ls)
+                j = self._alias_prev[li]
+                if j is not None:
+                    ls.wait_event(self._evt[k][j])      # the alias's DCU tail is done
+                # phase bits: 1 scan, 2 unit, 8 defer the tail, 4 tail only, 16 PDL
+                # allowed (the kernel before a scan on a lane stream is the
+                # previous layer's chain, before a chain this layer's scan).
+                # The previous layer's tail is released once this layer's scan
+                # is done, so it shares the GPU with this chain, not this scan.
+                self._launch(L, 1 | 16, ls)
+                if li > 0:
+                    es = self._evs[k][li]
+                    es.record(ls)
+                    ts.wait_event(self._ev[k][li - 1])
+                    ts.wait_event(es)
+                    self._launch(self.lane_layers[k][li - 1], 4, ts)
+                    self._evt[k][li - 1].record(ts)
+                self._launch(L, 2 | 8 | 16, ls)
                 ev = self._ev[k][li]
                 ev.record(ls)
-                # the tail (DCU write, sparse ids, cursor/total advance) is only
-                # read by this layer's next step: run it beside the next layers
-                if not self._tail_after_scan or li == self.nl - 1:
+                if li == self.nl - 1:
                     ts.wait_event(ev)
                     self._launch(L, 4, ts)
+                    self._evt[k][li].record(ts)
                 if self._comm is not None:
                     self._comm.wait_event(ev)
                     with torch.cuda.stream(self._comm):
@@ -253,11 +272,28 @@ class DecodeEngine:
         if self.nlanes > 1:
             raise RuntimeError("reserve() before splitting into lanes (lane views share storage)")
         for L in self.layers:
-            L.store.ensure_room(steps)
+            L.store.ensure_room(steps * self._appends[id(L.store)])
             L.call = None   # storage may have moved
+        self.graph = None   # captured graphs hold the old pointers
+        self._hgraphs = None
+
+    def room(self) -> int:
+        """Decode steps left before some layer's store is full (the fused
+        scan appends in place and never grows the store)."""
+        left = None
+        for store, _ in self.parents:
+            n = (store.capacity - store.total_tokens) // self._appends[id(store)]
+            left = n if left is None else min(left, n)
+        return left
+
+    def _check_room(self) -> None:
+        if self.room() < 1:
+            raise ConfigError("decode step: a layer's KvStore is full (reserve() more rows "
+                              "before capturing, or build the stores with a larger capacity)")
 
     def step(self, events=None) -> None:
         """Enqueue one decode step (all layers) eagerly."""
+        self._check_room()
         self._enqueue(events)
         self._note()
 
@@ -274,6 +310,7 @@ class DecodeEngine:
     def replay(self) -> None:
         if self.graph is None:
             raise RuntimeError("capture() first")
+        self._check_room()
         self.graph.replay()
         self._note()
 
@@ -293,7 +330,7 @@ class DecodeEngine:
         self._cin = torch.cuda.Stream(device=dev)
         self._cout = torch.cuda.Stream(device=dev)
         self._cin_ev = [[torch.cuda.Event() for _ in range(self.nl)] for _ in range(self.nlanes)]
-        self._cin_chunk = max(1, int(os.environ.get("CTKV_HIO_CHUNK", "4")))   # layers per input copy
+        self._cin_chunk = 4   # layers per input copy
         bufs, graphs = [], []
         torch.cuda.synchronize()
         for _ in range(slots):
@@ -312,6 +349,9 @@ class DecodeEngine:
     def replay_host(self, slot: int) -> None:
         """One step through host buffer set `slot` (see capture_host_io); the
         outputs are in that set's out buffer once the stream is synchronised."""
+        if not self._hgraphs:
+            raise RuntimeError("capture_host_io() first")
+        self._check_room()
         self._hgraphs[slot].replay()
         self._note()
 

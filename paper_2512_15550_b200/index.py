@@ -8,8 +8,6 @@ last CTA uses to advance the FIFO cursor without a host round trip.
 
 from __future__ import annotations
 
-import struct
-
 import numpy as np
 import torch
 
@@ -213,38 +211,45 @@ class QueryCentroidIndex:
             bi, gi, ci, _ = [int(x) for x in bad.nonzero()[0]]
             raise AssertionError(f"non-offloaded id in list ({bi},{gi},{ci})")
 
-    # -- QIVF serialization (ck/index.py:157-190), bit-compatible ------------------
+    # -- QIVF serialization (ck/index.py:157-190), byte-compatible ------------
+    # 32-byte little-endian header: b"QIVF", then u32 version, b, h, g, C,
+    # rho, d; then the centroids [b,h,C,d] f32 and the lists [b,g,C,rho] i32.
+    # The FIFO cursor is not part of the format (it restarts at 0 on load).
+
+    _HDR = np.dtype([("magic", "S4"), ("version", "<u4"), ("b", "<u4"), ("h", "<u4"),
+                     ("g", "<u4"), ("C", "<u4"), ("rho", "<u4"), ("d", "<u4")])
 
     def save(self, path) -> None:
         lay = self.layout
-        header = MAGIC + struct.pack("<7I", VERSION, lay.batch, lay.query_heads, lay.kv_heads,
-                                     self.capacity, self.rho, lay.head_dim)
+        hdr = np.array([(MAGIC, VERSION, lay.batch, lay.query_heads, lay.kv_heads,
+                         self.capacity, self.rho, lay.head_dim)], dtype=self._HDR)
         with open(path, "wb") as fh:
-            fh.write(header)
+            fh.write(hdr.tobytes())
             fh.write(self.cent.float().cpu().numpy().astype("<f4", copy=False).tobytes())
             fh.write(self.lists_dev.cpu().numpy().astype("<i4", copy=False).tobytes())
 
     @classmethod
     def load(cls, path, seq_len: int | None = None, *, dtype: torch.dtype = torch.float32,
              host_api: bool = True) -> "QueryCentroidIndex":
-        with open(path, "rb") as fh:
-            blob = fh.read()
-        if len(blob) < 4 + 28 or blob[:4] != MAGIC:
-            raise FormatError(f"{path}: bad magic (expected {MAGIC!r})")
-        version, b, h, g, cap, rho, d = struct.unpack_from("<7I", blob, 4)
-        if version != VERSION:
-            raise FormatError(f"{path}: unsupported version {version}")
-        cq_bytes = b * h * cap * d * 4
-        li_bytes = b * g * cap * rho * 4
-        expected = 32 + cq_bytes + li_bytes
-        if len(blob) != expected:
-            raise FormatError(f"{path}: expected {expected} bytes, found {len(blob)} (offset 32)")
-        cq = np.frombuffer(blob, dtype="<f4", count=b * h * cap * d, offset=32).reshape(b, h, cap, d)
-        li = np.frombuffer(blob, dtype="<i4", count=b * g * cap * rho, offset=32 + cq_bytes)
+        blob = np.fromfile(path, dtype=np.uint8)
+        n_hdr = cls._HDR.itemsize
+        if blob.size < n_hdr or bytes(blob[:4]) != MAGIC:
+            raise FormatError(f"{path}: not a QIVF index (missing {MAGIC!r} header)")
+        hdr = blob[:n_hdr].view(cls._HDR)[0]
+        if int(hdr["version"]) != VERSION:
+            raise FormatError(f"{path}: QIVF version {int(hdr['version'])} is not supported")
+        b, h, g, cap, rho, d = (int(hdr[f]) for f in ("b", "h", "g", "C", "rho", "d"))
+        n_cent, n_list = b * h * cap * d, b * g * cap * rho
+        need = n_hdr + 4 * (n_cent + n_list)
+        if blob.size != need:
+            raise FormatError(f"{path}: QIVF payload size mismatch: file has {blob.size} bytes, "
+                              f"the header implies {need}")
+        body = blob[n_hdr:]
+        cq = body[:4 * n_cent].view("<f4").reshape(b, h, cap, d).astype(np.float32)
+        li = body[4 * n_cent:].view("<i4").reshape(b, g, cap, rho).astype(np.int32)
         layout = HeadLayout(batch=b, query_heads=h, kv_heads=g,
                             seq_len=cap if seq_len is None else seq_len, head_dim=d)
-        idx = cls(layout, cap, rho, np.ascontiguousarray(cq), li.reshape(b, g, cap, rho).astype(np.int32),
-                  dtype=dtype)
+        idx = cls(layout, cap, rho, cq, li, dtype=dtype)
         idx.host_api = host_api
         return idx
 

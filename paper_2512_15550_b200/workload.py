@@ -20,7 +20,6 @@ from __future__ import annotations
 
 import json
 import math
-import struct
 from dataclasses import asdict, dataclass
 
 import numpy as np
@@ -219,42 +218,60 @@ def generate(cfg: DriftConfig, layout: HeadLayout, *, device=None, dtype=torch.f
     return q, keys, values, planted
 
 
-# -- CTKV dump format (ck/workload.py:247-308) -------------------------------
+# -- CTKV dump format (ck/workload.py:247-287), byte-compatible -------------
+# 28-byte little-endian header: b"CTKV", then u32 version, b, h, g, s, d;
+# then Q [b,h,s,d], K [b,g,s,d], V [b,g,s,d] as little-endian f32, row-major.
+
+_DUMP_HDR = np.dtype([("magic", "S4"), ("version", "<u4"), ("b", "<u4"), ("h", "<u4"),
+                      ("g", "<u4"), ("s", "<u4"), ("d", "<u4")])
+
+
+def _host_f32(x) -> np.ndarray:
+    if isinstance(x, torch.Tensor):
+        x = x.detach().float().cpu().numpy()
+    return np.asarray(x)
+
 
 def write_dump(path, q, k, v) -> None:
-    """magic, version u32, b/h/g/s/d u32 (little endian), then Q, K, V f32."""
-    q, k, v = (np.asarray(x.float().cpu() if isinstance(x, torch.Tensor) else x) for x in (q, k, v))
-    if q.ndim != 4 or k.ndim != 4 or v.ndim != 4:
-        raise ConfigError("write_dump: tensors must be 4-D")
+    """Write Q/K/V as a CTKV dump (device tensors are copied to the host)."""
+    q, k, v = _host_f32(q), _host_f32(k), _host_f32(v)
+    if min(q.ndim, k.ndim, v.ndim) != 4 or max(q.ndim, k.ndim, v.ndim) != 4:
+        raise ConfigError("write_dump: Q, K and V must all be rank-4 arrays")
     b, h, s, d = q.shape
-    g = k.shape[1]
-    if k.shape != (b, g, s, d) or v.shape != (b, g, s, d):
-        raise ConfigError(f"write_dump: incompatible shapes {q.shape} {k.shape} {v.shape}")
+    kv = (b, k.shape[1], s, d)
+    if k.shape != kv or v.shape != kv:
+        raise ConfigError(f"write_dump: K {k.shape} / V {v.shape} do not pair with Q {q.shape}")
+    hdr = np.array([(MAGIC, VERSION, b, h, kv[1], s, d)], dtype=_DUMP_HDR)
     with open(path, "wb") as fh:
-        fh.write(MAGIC + struct.pack("<6I", VERSION, b, h, g, s, d))
+        fh.write(hdr.tobytes())
         for arr in (q, k, v):
             fh.write(np.ascontiguousarray(arr, dtype="<f4").tobytes())
 
 
 def read_dump(path):
-    with open(path, "rb") as fh:
-        blob = fh.read()
-    if len(blob) < 28:
-        raise FormatError(f"{path}: header truncated at {len(blob)} bytes (need 28)")
-    if blob[:4] != MAGIC:
-        raise FormatError(f"{path}: bad magic {blob[:4]!r} (expected {MAGIC!r})")
-    version, b, h, g, s, d = struct.unpack_from("<6I", blob, 4)
-    if version != VERSION:
-        raise FormatError(f"{path}: unsupported version {version}")
-    qn, kn = b * h * s * d, b * g * s * d
-    expected = 28 + 4 * (qn + 2 * kn)
-    if len(blob) != expected:
-        raise FormatError(f"{path}: expected {expected} bytes, found {len(blob)} (at offset 28)")
-    off = 28
-    out = []
-    for count, shape in ((qn, (b, h, s, d)), (kn, (b, g, s, d)), (kn, (b, g, s, d))):
-        out.append(np.frombuffer(blob, dtype="<f4", count=count, offset=off).reshape(shape).copy())
-        off += 4 * count
+    """Read a CTKV dump -> (q, k, v, HeadLayout); FormatError on a bad or
+    truncated file."""
+    blob = np.fromfile(path, dtype=np.uint8)
+    if blob.size < _DUMP_HDR.itemsize:
+        raise FormatError(f"{path}: {blob.size} bytes is shorter than the "
+                          f"{_DUMP_HDR.itemsize}-byte CTKV header")
+    hdr = blob[:_DUMP_HDR.itemsize].view(_DUMP_HDR)[0]
+    if bytes(hdr["magic"]) != MAGIC:
+        raise FormatError(f"{path}: not a CTKV dump (magic {bytes(hdr['magic'])!r})")
+    if int(hdr["version"]) != VERSION:
+        raise FormatError(f"{path}: CTKV version {int(hdr['version'])} is not supported")
+    b, h, g, s, d = (int(hdr[f]) for f in ("b", "h", "g", "s", "d"))
+    shapes = ((b, h, s, d), (b, g, s, d), (b, g, s, d))
+    need = _DUMP_HDR.itemsize + 4 * sum(int(np.prod(sh)) for sh in shapes)
+    if blob.size != need:
+        raise FormatError(f"{path}: CTKV payload size mismatch: file has {blob.size} bytes, "
+                          f"the header implies {need}")
+    body = blob[_DUMP_HDR.itemsize:].view("<f4")
+    out, at = [], 0
+    for sh in shapes:
+        n = int(np.prod(sh))
+        out.append(body[at:at + n].reshape(sh).astype(np.float32))
+        at += n
     return out[0], out[1], out[2], HeadLayout(batch=b, query_heads=h, kv_heads=g, seq_len=s,
                                               head_dim=d)
 

@@ -10,6 +10,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2512_15550_b200 as P  # noqa: E402
 from paper_2512_15550_b200 import _native as N  # noqa: E402
+N.use_profile_library()   # the timestamp marks exist only in the profiling build
 from paper_2512_15550_b200.engine import DecodeEngine  # noqa: E402
 from paper_2512_15550_b200.index import QueryCentroidIndex  # noqa: E402
 from paper_2512_15550_b200.store import KvStore  # noqa: E402

@@ -117,3 +117,32 @@ def test_engine_matches_oracle_bf16():
             ref = orc[li][t].out
             err = np.linalg.norm(eng.out[li].cpu().numpy() - ref) / np.linalg.norm(ref)
             assert err < 1e-3, (t, li, err)
+
+
+def test_engine_refuses_to_overrun_store_capacity():
+    """The fused scan appends in place and never grows the store: the engine
+    raises before enqueueing a step the stores have no room for,
+    and reserve() drops graphs that captured the old storage pointers."""
+    torch.cuda.set_device(0)
+    q, k, v = _inputs(0)
+    st, ix = P.prefill(np.ascontiguousarray(q[:, :, :S]), np.ascontiguousarray(k[:, :, :S]),
+                       np.ascontiguousarray(v[:, :, :S]), P.PrefillParams(**PARAMS),
+                       dtype=torch.bfloat16, reserve=2, build_mode=0)
+    assert st.capacity - st.total_tokens == 2
+    eng = DecodeEngine([(st, ix)], P.DecodeConfig(CP, RP), lanes=1)
+    assert eng.room() == 2
+    eng.step()
+    eng.capture()
+    eng.replay()
+    torch.cuda.synchronize()
+    assert eng.room() == 0
+    with pytest.raises(P.ConfigError):
+        eng.step()
+    with pytest.raises(P.ConfigError):
+        eng.replay()
+    eng.reserve(3)
+    assert eng.graph is None and eng.room() >= 3
+    eng.step()
+    torch.cuda.synchronize()
+    eng.check()
+    assert st.total_tokens == S + 3 and int(st.total_dev.item()) == S + 3

@@ -345,6 +345,36 @@ def test_qivf_roundtrip(tmp_path):
     assert back.size_bytes() == 1 * 2 * 8 * 32 * 4
 
 
+def test_qivf_interop_with_reference_written_file(tmp_path):
+    """A QIVF file the reference's own QueryCentroidIndex.save wrote
+    (ck/index.py:157-190; tests/golden/make_golden.py `interop`): loaded
+    onto the device it holds the reference's centroids and lists, the FIFO
+    cursor restarts at 0, and saving it again reproduces the file byte for
+    byte.  The same file rebuilt here from the reference's dump matches."""
+    import json
+    import os
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    src = os.path.join(gold, "interop_index.qivf")
+    with open(os.path.join(gold, "interop.json")) as fh:
+        doc = json.load(fh)
+    idx = P.QueryCentroidIndex.load(src, seq_len=96)
+    assert G.sha(idx.lists) == doc["index_lists_sha"]
+    assert G.sha(idx.centroid_queries) == doc["index_centroids_sha"]
+    assert idx.fifo_head.tolist() == [0]
+    out = tmp_path / "again.qivf"
+    idx.save(out)
+    assert out.read_bytes() == open(src, "rb").read()
+    # prefill from the reference's dump with the reference's parameters
+    q, k, v, _ = P.read_dump(os.path.join(gold, "interop_dump.ctkv"))
+    _, built = P.prefill(q, k, v, P.PrefillParams(8, 16, 8, 12))
+    built.save(tmp_path / "built.qivf")
+    assert (tmp_path / "built.qivf").read_bytes() == open(src, "rb").read()
+    bad = tmp_path / "bad.qivf"
+    bad.write_bytes(open(src, "rb").read()[:-8])
+    with pytest.raises(P.FormatError):
+        P.QueryCentroidIndex.load(bad)
+
+
 # ---------------------------------------------------------------------------
 # 96K scale (cfg2 geometry, one sequence) -- size-independent properties
 # ---------------------------------------------------------------------------
@@ -419,6 +449,10 @@ def test_96k_tensor_core_build_matches_exact_within_tie_window():
     (16, 8, 64, 64, 64, 6, 96),
     (16, 2, 128, 32, 48, 8, 120),
     (8, 2, 128, 64, 64, 1, 16),
+    (8, 2, 16, 64, 64, 4, 32),      # d = 16 / 32: SIMT static logits and P.V (no mma tiles)
+    (8, 2, 32, 64, 64, 4, 32),
+    (8, 2, 256, 64, 64, 4, 64),     # d = 256: the 2-CTA unit2 kernel
+    (32, 2, 128, 64, 64, 4, 32),    # gs = 16: unit2 (the chain takes gs <= 8)
 ])
 def test_bf16_fused_decode_geometries(h, g, d, C, rho, cp, rp):
     rng = np.random.default_rng(1000 * h + 10 * d + C + rho + cp)
@@ -454,3 +488,28 @@ def test_bf16_fused_decode_geometries(h, g, d, C, rho, cp, rp):
         assert trace[t].recall_len == r.recall_len
     assert hard == 0
     assert hard_order == 0
+
+
+def test_bf16_capacity_above_4096_selects_every_slot():
+    """C > 4096 (more than 16 group-max cosines per selector thread): the
+    top-C' selector must still see every slot."""
+    rng = np.random.default_rng(77)
+    b, h, g, d, s, T, C, rho = 1, 8, 2, 64, 6144, 2, 4500, 16
+    q = O.bf16_round(rng.standard_normal((b, h, s + T, d)).astype(np.float32))
+    k = O.bf16_round(rng.standard_normal((b, g, s + T, d)).astype(np.float32))
+    v = O.bf16_round(rng.standard_normal((b, g, s + T, d)).astype(np.float32))
+    # make the best centroid for the decode queries sit at a slot >= 4096
+    q[:, :, s - C + 4300] = q[:, :, s]
+    store, index = P.prefill(np.ascontiguousarray(q[:, :, :s]), np.ascontiguousarray(k[:, :, :s]),
+                             np.ascontiguousarray(v[:, :, :s]), P.PrefillParams(16, 64, C, rho),
+                             dtype=torch.bfloat16, reserve=T, build_mode=0)
+    outs, trace = P.run_decode(store, index, P.DecodeConfig(4, 16, keep_sets=True),
+                               np.ascontiguousarray(q[:, :, s:]), np.ascontiguousarray(k[:, :, s:]),
+                               np.ascontiguousarray(v[:, :, s:]))
+    ost, oidx = O.prefill(np.ascontiguousarray(q[:, :, :s]), np.ascontiguousarray(k[:, :, :s]),
+                          np.ascontiguousarray(v[:, :, :s]), 16, 64, C, rho)
+    ref_out, recs = O.run_decode(ost, oidx, q[:, :, s:], k[:, :, s:], v[:, :, s:], 4, 16)
+    assert 4300 in recs[0].selected[0, 0].tolist()
+    for t in range(T):
+        assert trace[t].sparse_digest == recs[t].digest
+        assert nrel(outs[:, :, t], ref_out[:, :, t]) < 1e-3
