@@ -554,7 +554,8 @@ def main():
         del snaps
         parity = {k: res[k] for k in ("ok", "reference", "units", "steps", "recall",
                                       "hard_mismatches", "order_hard", "exact_steps",
-                                      "recall_len_mismatch", "selected_mismatch", "out_nrel_max",
+                                      "recall_len_mismatch", "selected_ties", "selected_hard",
+                                      "out_nrel_max",
                                       "dcu_rows", "dcu_rows_exact", "dcu_hard",
                                       "centroids_equal", "fifo_equal",
                                       "ref_vs_oracle_digest_mismatch",

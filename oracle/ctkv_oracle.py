@@ -242,10 +242,14 @@ class Recall:
     recall_len: np.ndarray         # [b,g]
     alpha: np.ndarray              # [b,g]
     degenerate: bool = False
+    cosines: np.ndarray | None = None   # [b,g,C] f64 group-max cosines
 
 
-def recall(index: Index, q: np.ndarray, c_prime: int) -> Recall:
-    """Alg. 2 lines 1-4 (ck/retrieval.py:132-168)."""
+def recall(index: Index, q: np.ndarray, c_prime: int, force_selected=None) -> Recall:
+    """Alg. 2 lines 1-4 (ck/retrieval.py:132-168).  `force_selected[b, g]`
+    (parity checkers only) replaces the top-C' slots of a unit whose
+    selection differs from the device's inside the tie window, so the rest
+    of the step is compared from equal state."""
     C = index.capacity
     if C == 0:
         raise ValueError("empty index")
@@ -262,6 +266,8 @@ def recall(index: Index, q: np.ndarray, c_prime: int) -> Recall:
         row = []
         for gi in range(g):
             slots = topk_desc(grouped[bi, gi], c_prime)
+            if force_selected is not None and force_selected[bi][gi] is not None:
+                slots = np.asarray(force_selected[bi][gi], dtype=np.int64)
             selected[bi, gi] = slots
             flat = index.lists[bi, gi, slots].reshape(-1)
             flat = flat[flat != EMPTY].astype(np.int64)
@@ -275,7 +281,7 @@ def recall(index: Index, q: np.ndarray, c_prime: int) -> Recall:
             denom = c_prime * index.rho
             alpha[bi, gi] = ids.size / denom if denom else 0.0
         recalled.append(row)
-    return Recall(selected, recalled, rlen, alpha, degenerate)
+    return Recall(selected, recalled, rlen, alpha, degenerate, grouped)
 
 
 def head_logits(store: Store, q: np.ndarray, ids_bg: list):
@@ -388,15 +394,17 @@ class StepRecord:
     rerank_len: int
     digest: str
     merged: Partial | None = None
+    cosines: np.ndarray | None = None
 
 
 def decode_step(store: Store, index: Index, q: np.ndarray, c_prime: int, rho_prime: int,
-                use_dcu: bool = True, use_rerank: bool = True) -> StepRecord:
+                use_dcu: bool = True, use_rerank: bool = True,
+                force_selected=None) -> StepRecord:
     """One decode step (ck/retrieval.py:304-378) without the flat oracle."""
     q = np.asarray(q, dtype=np.float32)
     if q.ndim == 4:
         q = q[:, :, 0, :]
-    rec = recall(index, q, c_prime)
+    rec = recall(index, q, c_prime, force_selected)
     total = int(rec.recall_len.sum())
     sparse_p, grouped, sparse, rr_len, dig = None, None, None, 0, ""
     if total > 0:
@@ -425,7 +433,7 @@ def decode_step(store: Store, index: Index, q: np.ndarray, c_prime: int, rho_pri
     if use_dcu and total > 0:
         fifo_update(index, q, grouped, rec.recalled)
     return StepRecord(merged.out, rec.selected, rec.recalled, sparse, grouped, total,
-                      float(rec.alpha.mean()), rr_len, dig, merged)
+                      float(rec.alpha.mean()), rr_len, dig, merged, rec.cosines)
 
 
 # ---------------------------------------------------------------------------

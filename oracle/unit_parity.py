@@ -140,7 +140,7 @@ def check(snaps, c_prime: int, rho_prime: int, *, use_rerank: bool = True,
                out_nrel_max=0.0, dcu_rows=0, dcu_rows_exact=0, dcu_hard=0,
                centroids_equal=True, fifo_equal=True, reference=None,
                ref_vs_oracle_digest_mismatch=0, ref_vs_oracle_out_nrel_max=0.0,
-               ref_times=[], oracle_times=[])
+               selected_ties=0, selected_hard=0, ref_times=[], oracle_times=[])
     if ref_pkg is not None:
         res["reference"] = f"centroidkv {getattr(ref_pkg, '__version__', '?')} (real package)"
     for sn in snaps:
@@ -161,20 +161,47 @@ def check(snaps, c_prime: int, rho_prime: int, *, use_rerank: bool = True,
         fin = sn["lists_final"][0]          # the device's post-DCU lists (no slot is
         for si, st in enumerate(sn["steps"]):   # rewritten within a run: steps < C)
             slot = int(oix.fifo_head[0] % oix.capacity)
+            pre = (oix.centroids.copy(), oix.lists.copy(), oix.fifo_head.copy())
             ost.append(st["k"], st["v"])
             t0 = time.perf_counter()
             r = O.decode_step(ost, oix, st["q"], c_prime, rho_prime, use_rerank=use_rerank)
             if si >= timing_warmup:
                 res["oracle_times"].append(time.perf_counter() - t0)
+            # top-C' slots: a difference inside the tie window of the f64
+            # group-max cosines is counted once and the device's slots are
+            # injected (the oracle step is redone with them)
+            forced = None
+            for gi in range(g):
+                mine, ref = st["selected"][gi], r.selected[0, gi]
+                if np.array_equal(mine, ref):
+                    continue
+                cosg = r.cosines[0, gi]
+                kth = cosg[ref[-1]]
+                tie = all(abs(cosg[c] - kth) <= TIE_REL * abs(kth)
+                          for c in set(mine.tolist()) ^ set(ref.tolist()))
+                tie &= all(abs(cosg[a] - cosg[b_]) <= TIE_REL * abs(cosg[b_])
+                           for a, b_ in zip(mine.tolist(), ref.tolist()) if a != b_)
+                res["selected_ties" if tie else "selected_hard"] += 1
+                forced = forced or [[None] * g]
+                forced[0][gi] = mine
+            if forced is not None:
+                ost.total -= 1                      # redo the step from the pre-step state
+                oix.centroids, oix.lists, oix.fifo_head = pre
+                ost.append(st["k"], st["v"])
+                r = O.decode_step(ost, oix, st["q"], c_prime, rho_prime, use_rerank=use_rerank,
+                                  force_selected=forced)
             if rst is not None:
                 rst.append(st["k"], st["v"])       # ck/session.py:58-60
                 t0 = time.perf_counter()
                 rout, rrow = ref_pkg.decode_step(rstate, st["q"])
                 if si >= timing_warmup:
                     res["ref_times"].append(time.perf_counter() - t0)
-                res["ref_vs_oracle_digest_mismatch"] += int(rrow.sparse_digest != r.digest)
-                res["ref_vs_oracle_out_nrel_max"] = max(res["ref_vs_oracle_out_nrel_max"],
-                                                        _nrel(rout, r.out))
+                if forced is None:
+                    res["ref_vs_oracle_digest_mismatch"] += int(rrow.sparse_digest != r.digest)
+                    res["ref_vs_oracle_out_nrel_max"] = max(res["ref_vs_oracle_out_nrel_max"],
+                                                            _nrel(rout, r.out))
+                else:                               # keep the reference on the injected path
+                    rix.lists[0, :, slot] = oix.lists[0, :, slot]
             res["steps"] += 1
             res["out_nrel_max"] = max(res["out_nrel_max"], _nrel(st["out"], r.out[0]))
             rlen = np.array([len(x) for x in r.recalled[0]], np.int64)
@@ -222,6 +249,7 @@ def check(snaps, c_prime: int, rho_prime: int, *, use_rerank: bool = True,
         res["fifo_equal"] &= bool(np.array_equal(sn["fifo_final"], oix.fifo_head))
     res["recall"] = res["sparse_hits"] / max(res["sparse_total"], 1)
     res["ok"] = bool(res["hard_mismatches"] == 0 and res["order_hard"] == 0
+                     and res["selected_hard"] == 0
                      and res["recall_len_mismatch"] == 0 and res["dcu_hard"] == 0
                      and res["centroids_equal"] and res["fifo_equal"]
                      and res["ref_vs_oracle_digest_mismatch"] == 0)

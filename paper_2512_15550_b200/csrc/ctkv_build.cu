@@ -94,7 +94,10 @@ __global__ void __launch_bounds__(kSThreads) scores_kernel(
       ACC m = acc[0][j] * scale;
 #pragma unroll
       for (int hh = 1; hh < GS; ++hh) m = fmax(m, acc[hh][j] * scale);
-      O[(int64_t)(c0 + tc) * out_ld + col] = (float)m;
+      float* o = O + (int64_t)(c0 + tc) * out_ld + col;
+      // grouped == 2: second half of a 16-head group, max into the first's
+      // (rounding to f32 is monotonic, so this equals f32 of the f64 max)
+      *o = grouped == 2 ? fmaxf(*o, (float)m) : (float)m;
     } else {
 #pragma unroll
       for (int hh = 0; hh < GS; ++hh)
@@ -273,15 +276,27 @@ static int scores_dispatch(int gs, dim3 grid_in, cudaStream_t st, const T* cent,
   scores_kernel<T, G, ACC><<<grid, kSThreads, 0, st>>>(cent, cus, crs, chs, keys, kus, krs, d, \
                                                        nc, n, grouped, out, ous, old_);        \
   break;
+#define CTKV_SC_16(CENT, GROUPED, OUT)                                                        \
+  grid.x = (unsigned)((n + STile<8>::SK - 1) / STile<8>::SK);                                  \
+  scores_kernel<T, 8, ACC><<<grid, kSThreads, 0, st>>>(CENT, cus, crs, chs, keys, kus, krs, d, \
+                                                       nc, n, GROUPED, OUT, ous, old_);
   dim3 grid = grid_in;
   switch (gs) {
     case 1: CTKV_SC(1)
     case 2: CTKV_SC(2)
     case 4: CTKV_SC(4)
     case 8: CTKV_SC(8)
+    case 16: {
+      // two 8-head passes: heads 0-7, then 8-15 max-combined (grouped) or
+      // written after the first eight heads' rows (per head)
+      CTKV_SC_16(cent, grouped, out)
+      CTKV_SC_16(cent + 8 * chs, grouped ? 2 : 0, grouped ? out : out + 8 * (int64_t)nc * old_)
+      break;
+    }
     default: return CTKV_ESHAPE;
   }
 #undef CTKV_SC
+#undef CTKV_SC_16
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
 

@@ -175,7 +175,7 @@ int ctkv_build_lists(const ctkv_layout* L, const void* centroids, const void* ke
     return CTKV_ECONFIG;
   if (rho > 8192) return CTKV_ECONFIG;
   const int gs = L->query_heads / L->kv_heads;
-  if (gs != 1 && gs != 2 && gs != 4 && gs != 8) return CTKV_ESHAPE;
+  if (gs != 1 && gs != 2 && gs != 4 && gs != 8 && gs != 16) return CTKV_ESHAPE;
   BuildParams p{};
   p.b = L->batch;
   p.h = L->query_heads;
@@ -457,7 +457,7 @@ int ctkv_scores(const ctkv_layout* L, const void* q, int64_t m, const void* k, i
   l2.head_dim = 16;
   if (int rc = check_layout(&l2)) return rc;
   const int gs = L->query_heads / L->kv_heads;
-  if (gs != 1 && gs != 2 && gs != 4 && gs != 8) return CTKV_ESHAPE;
+  if (gs != 1 && gs != 2 && gs != 4 && gs != 8 && gs != 16) return CTKV_ESHAPE;
   if (m < 0 || n < 0) return CTKV_ESHAPE;
   if (m == 0 || n == 0) return CTKV_OK;
   return launch_scores(L->dtype, L->batch, L->query_heads, L->kv_heads, L->head_dim, q, m, k, n,

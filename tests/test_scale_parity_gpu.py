@@ -85,6 +85,7 @@ def test_bench_path_matches_reference_at_96k(b, h, g, units):
     assert res["ref_vs_oracle_digest_mismatch"] == 0, summary
     assert res["recall"] >= 0.99, summary
     assert res["hard_mismatches"] == 0 and res["order_hard"] == 0, summary
+    assert res["selected_hard"] == 0, summary       # top-C' slots: ties only
     assert res["recall_len_mismatch"] == 0, summary
     assert res["out_nrel_max"] < 1e-3, summary
     assert res["dcu_hard"] == 0 and res["centroids_equal"] and res["fifo_equal"], summary
