@@ -217,9 +217,11 @@ def _config(a, n):
     if a.phys_layers:
         cfg["physical_layers"] = a.phys_layers
     if a.slice_of:
-        cfg["slice"] = (f"rank 0 of a {a.slice_of}-GPU shard plan on 1 GPU (per-GPU work; the "
-                        f"per-layer all-gather is not included)")
+        cfg["slice"] = (f"rank 0 of a {a.slice_of}-GPU kv-head x batch shard plan, run on 1 GPU; "
+                        f"value = global batch / slice step time (every rank runs an identical "
+                        f"slice; the per-layer all-gather is not included)")
         cfg["global_batch"] = a.batch
+        cfg["parallelism"] = f"1-GPU slice of {a.slice_of}-GPU shards, {a.lanes} lanes"
     return cfg
 
 
@@ -269,8 +271,9 @@ def run_reference(a):
         ck.decode_step(state, q[:, :, C + t])
         times.append(time.perf_counter() - t1)
     unit = statistics.median(times[a.warmup:])
-    units = a.layers * a.batch                            # (layer, seq) units per GPU-step
-    tok_s = 1.0 / (unit * a.layers)                       # = batch / (unit * units)
+    hsplit = a.kv_heads // g                              # 8 for a cfg5 kv-head slice, else 1
+    units = a.layers * a.batch * hsplit                   # units per step of the whole job
+    tok_s = 1.0 / (unit * a.layers * hsplit)              # = batch / (unit * units)
     line = {
         "impl": "reference", "metric": "decode_tokens_per_s", "value": tok_s, "unit": "tok/s",
         "higher_is_better": True, "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
@@ -326,16 +329,18 @@ def main():
     if a.slice_of:
         if world > 1:
             raise SystemExit("--slice-of runs one rank's shard on one GPU (use --gpus 1)")
-        # one rank's slice of the multi-GPU plan, no collective
-        plan_full = ShardPlan(a.slice_of, 0, a.batch * a.slice_of, a.kv_heads, a.query_heads)
+        # one rank's slice of the multi-GPU plan (--batch = the GLOBAL batch B),
+        # no collective; B / step time = the job's throughput if every rank
+        # runs its identical slice in parallel (the all-gather excluded)
+        plan_full = ShardPlan(a.slice_of, 0, a.batch, a.kv_heads, a.query_heads)
         plan = ShardPlan(1, 0, plan_full.b_loc, plan_full.g_loc, plan_full.h_loc)
-        B = plan.batch
+        B = a.batch
     else:
         B = a.batch * world                                  # weak scaling: batch per GPU fixed
         plan = ShardPlan(world, rank, B, a.kv_heads, a.query_heads)
     b, g, h, d = plan.b_loc, plan.g_loc, plan.h_loc, 128
-    if a.lanes > b:
-        a.lanes = b
+    while b % a.lanes:
+        a.lanes -= 1
     s = a.seq
     T = a.warmup + a.steps + a.e2e_steps + a.parity_steps + 8
     n_phys = a.phys_layers or a.layers
@@ -458,7 +463,7 @@ def main():
     C = a.capacity
     n_sparse = a.rho_prime if not a.no_rerank else Lbar
     # algorithmic bytes per launch (full-layer launch: U = b*g units)
-    ns = math.ceil(n_static / 128)                # static splits (bf16: 128 tokens)
+    ns = math.ceil(n_static / (64 if e == 4 else 128))   # static splits (f32: 64 tokens)
     scan_bytes = U * (gs * C * d * e + gs * C * 4          # centroid rows + cached norms
                       + 2 * n_static * d * e               # static K, V
                       + gs * d * e + 2 * d * e             # query heads, appended K/V
@@ -568,7 +573,7 @@ def main():
         tm = res["ref_times"] if res["ref_times"] else res["oracle_times"]
         if tm:
             unit_s = statistics.median(tm)
-            units_n = nl * B
+            units_n = nl * B * (a.kv_heads // g)   # whole-job (layer, seq) units of g kv heads
             cpu = dict(value=B / (unit_s * units_n), unit="tok/s",
                        kind="reference" if res["ref_times"] else "port",
                        sample=(f"{'centroidkv' if res['ref_times'] else 'oracle port'} decode_step "

@@ -145,29 +145,24 @@ __device__ void find_bin(const int* hist, int nbins, int k, int* s_bin, int* s_a
   }
 }
 
+// Exact top-k of one row v[0..n) (value desc, index asc) into dst[0..k),
+// ids + add; the whole block cooperates.  smem: hist [kTBins] int, cand
+// [next_pow2(k)] u64, then (kSmemRow) the row's n u32 keys.
 template <bool kSmemRow>
-__global__ void __launch_bounds__(kTThreads) topk_rows_kernel(const float* __restrict__ vals,
-                                                              int64_t n, int64_t ld, int k,
-                                                              int32_t* __restrict__ idx_out,
-                                                              int64_t out_ld, int32_t add,
-                                                              int64_t rows_per_group,
-                                                              int64_t group_stride,
-                                                              const int32_t* row_map) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int64_t row = blockIdx.x;
-  const float* v = vals + row * ld;
+__device__ void topk_row_body(const float* __restrict__ v, int64_t n, int k,
+                              int32_t* __restrict__ dst, int32_t add, unsigned char* smem) {
   int* hist = reinterpret_cast<int*>(smem);                        // [kTBins]
   uint64_t* cand = reinterpret_cast<uint64_t*>(hist + kTBins);     // [next_pow2(k)]
   const int kp = next_pow2(k);
   uint32_t* rowk = reinterpret_cast<uint32_t*>(cand + kp);         // [n] (kSmemRow)
-  __shared__ int s_bin, s_above, s_cnt, s_tie_taken;
+  __shared__ int s_bin, s_above, s_cnt;
   const int tid = threadIdx.x;
   auto key_at = [&](int64_t i) -> uint32_t {
     if (kSmemRow) return rowk[i];
-    return okey32(__ldg(v + i));
+    return okey32(v[i]);
   };
   if (kSmemRow) {
-    for (int64_t i = tid; i < n; i += kTThreads) rowk[i] = okey32(__ldg(v + i));
+    for (int64_t i = tid; i < n; i += kTThreads) rowk[i] = okey32(v[i]);
   }
   // radix passes: 11 / 11 / 10 bits
   uint32_t prefix = 0;
@@ -194,7 +189,7 @@ __global__ void __launch_bounds__(kTThreads) topk_rows_kernel(const float* __res
   const uint32_t T = prefix;          // the k-th largest key
   const int need = k - above;         // ties at T to take (>= 1)
   const int ties = hist[T & 1023];    // pass-3 histogram count of key == T
-  if (tid == 0) { s_cnt = 0; s_tie_taken = 0; }
+  if (tid == 0) s_cnt = 0;
   __syncthreads();
   for (int64_t i = tid; i < n; i += kTThreads) {
     const uint32_t key = key_at(i);
@@ -220,9 +215,75 @@ __global__ void __launch_bounds__(kTThreads) topk_rows_kernel(const float* __res
   __syncthreads();
   for (int i = k + tid; i < kp; i += kTThreads) cand[i] = ~0ull;
   bitonic_sort_u64(cand, kp);
+  for (int i = tid; i < k; i += kTThreads) dst[i] = (int32_t)(cand[i] & 0xffffffffu) + add;
+  __syncthreads();
+}
+
+template <bool kSmemRow>
+__global__ void __launch_bounds__(kTThreads) topk_rows_kernel(const float* __restrict__ vals,
+                                                              int64_t n, int64_t ld, int k,
+                                                              int32_t* __restrict__ idx_out,
+                                                              int64_t out_ld, int32_t add,
+                                                              int64_t rows_per_group,
+                                                              int64_t group_stride,
+                                                              const int32_t* row_map) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t row = blockIdx.x;
   int32_t* dst = row_map ? idx_out + (int64_t)row_map[row] * out_ld
                         : idx_out + (row / rows_per_group) * group_stride + (row % rows_per_group) * out_ld;
-  for (int i = tid; i < k; i += kTThreads) dst[i] = (int32_t)(cand[i] & 0xffffffffu) + add;
+  topk_row_body<kSmemRow>(vals + row * ld, n, k, dst, add, smem);
+}
+
+// Exact fallback of the tensor-core build for the rows its select pass could
+// not finish (candidate count outside [rho, cap]): a fixed grid walks the
+// device-side failure list (no host round trip, so the build stays
+// graph-capturable); per row, f32 SIMT group-max scores of every offloaded
+// key into this CTA's scratch row, then the exact top-rho of that row.
+__global__ void __launch_bounds__(kTThreads) build_fallback_kernel(
+    const __nv_bfloat16* __restrict__ cent, const __nv_bfloat16* __restrict__ keys,
+    const int32_t* __restrict__ fail_n, const int32_t* __restrict__ fail_rows, int C, int gs,
+    int h, int g, int d, int64_t cap, int64_t off, int64_t n, float scale,
+    float* __restrict__ scratch, int rho, int32_t* __restrict__ lists, int32_t* flags) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ float qs[16 * 256];
+  const int nf = *fail_n;
+  if (nf > 0 && blockIdx.x == 0 && threadIdx.x == 0) set_flag(flags, kFlagBuildFallback);
+  float* sc = scratch + (int64_t)blockIdx.x * n;
+  for (int f = blockIdx.x; f < nf; f += gridDim.x) {
+    const int r = fail_rows[f];
+    const int u = r / C, c = r % C;
+    const int bi = u / g, gi = u % g;
+    for (int i = threadIdx.x; i < gs * d; i += blockDim.x) {
+      const int j = i / d, e = i % d;
+      qs[i] = __bfloat162float(cent[(((int64_t)bi * h + gi * gs + j) * C + c) * d + e]);
+    }
+    __syncthreads();
+    for (int64_t key = threadIdx.x; key < n; key += blockDim.x) {
+      const __nv_bfloat16* kr = keys + ((int64_t)u * cap + off + key) * d;
+      float m = -INFINITY;
+      for (int j = 0; j < gs; ++j) {
+        float a = 0.f;
+        for (int e = 0; e < d; ++e) a = fmaf(qs[j * d + e], __bfloat162float(kr[e]), a);
+        m = fmaxf(m, a);
+      }
+      sc[key] = m * scale;
+    }
+    __syncthreads();
+    topk_row_body<false>(sc, n, rho, lists + (int64_t)r * rho, (int32_t)off, smem);
+  }
+}
+
+int launch_build_fallback(const void* cent, const void* keys, const int32_t* fail_n,
+                          const int32_t* fail_rows, int C, int gs, int h, int g, int d, int64_t cap,
+                          int64_t off, int64_t n, float scale, float* scratch, int grid, int rho,
+                          int32_t* lists, int32_t* flags, cudaStream_t st) {
+  const size_t sm = sizeof(int) * kTBins + sizeof(uint64_t) * next_pow2(rho);
+  if (sm > 200 * 1024 || gs * d > 16 * 256) return CTKV_ECONFIG;
+  cudaFuncSetAttribute(build_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  build_fallback_kernel<<<grid, kTThreads, sm, st>>>(
+      static_cast<const __nv_bfloat16*>(cent), static_cast<const __nv_bfloat16*>(keys), fail_n,
+      fail_rows, C, gs, h, g, d, cap, off, n, scale, scratch, rho, lists, flags);
+  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
 
 // ------------------------------------------------------------------------

@@ -6,21 +6,29 @@
 // one work item the resident B operand, accumulators live in TMEM (two
 // 256-column buffers so the epilogue of tile i overlaps the MMAs of tile
 // i+1).  Warp roles: 0 = TMA producer, 1 = MMA issuer (+TMEM owner),
-// 2..9 = epilogue (tcgen05.ld -> group max -> scale -> filter/store).
+// 2..17 = epilogue: 4 warps per TMEM lane quadrant, each owning CB/4
+// centroids x gs heads = 64 accumulator columns, read with one batch of
+// tcgen05.ld and a single wait, group max + scale in registers.
+// A work item is (unit, centroid block, key split); small problems split the
+// keys so every SM has work (candidate counters are global, warp-aggregated).
 //
 // Top-rho per row without materialising the 6.4 GB/layer score matrix:
-//   1. sample pass  -- the same GEMM against every S-th key, scores stored;
-//   2. threshold    -- per row the k_s-th largest sample score, with k_s
-//                      chosen so the full row has ~rho + 6 sigma candidates
-//                      above it with overwhelming probability;
+//   1. sample pass  -- the same GEMM against every S-th key; the epilogue
+//                      stores only the top 16 bits of each score's
+//                      order-preserving key (2 B per sampled score);
+//   2. threshold    -- per row the k_s-th largest sample key (2-pass radix
+//                      select), widened to its 16-bit bin's lower edge, with
+//                      k_s chosen so the full row has ~rho + 6 sigma
+//                      candidates above it with overwhelming probability;
 //   3. filter pass  -- the full GEMM; the epilogue keeps (score, key) pairs
-//                      >= threshold in a per-row buffer (the CTA owns its
-//                      rows, so counters are shared-memory atomics);
-//   4. select       -- per row, sort the <= cap candidates by (score desc,
+//                      >= threshold in a per-row buffer;
+//   4. select       -- per row, order the <= cap candidates by (score desc,
 //                      key asc) and write the first rho ids -- exact top-rho
 //                      of the tensor-core scores whenever rho <= count <= cap;
 //   5. fallback     -- rows outside [rho, cap] (rare) are recomputed in full
-//                      and radix-selected, so the result is exact always.
+//                      and radix-selected by a fixed-grid kernel that reads
+//                      the failure count on the device (no host sync; the
+//                      whole build is stream-ordered and graph-capturable).
 #include <cuda.h>
 
 #include <cfloat>
@@ -42,8 +50,8 @@ namespace tc {
 constexpr int kBM = 128;          // keys per tile (UMMA M)
 constexpr int kBN = 256;          // gs * CB centroid-head rows (UMMA N)
 constexpr int kStages = 4;        // A pipeline depth
-constexpr int kThreads = 320;     // 10 warps
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;     // 4 per TMEM lane quadrant
+constexpr int kThreads = 64 + 32 * kEpiWarps;   // producer + MMA + epilogue
 constexpr int kAtomBytes = kBM * 128;  // one 128-row x 64-element bf16 swizzle atom
 
 enum Mode : int { kStore = 0, kFilter = 1 };
@@ -118,6 +126,53 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, float* v) {
+  uint32_t r[2];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+               : "=r"(r[0]), "=r"(r[1])
+               : "r"(taddr));
+  v[0] = __uint_as_float(r[0]);
+  v[1] = __uint_as_float(r[1]);
+}
+__device__ __forceinline__ void tmem_ld1(uint32_t taddr, float* v) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  v[0] = __uint_as_float(r);
+}
+// NC consecutive accumulator columns of this warp's 32 TMEM lanes (no wait)
+template <int NC>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
+  if constexpr (NC >= 16) {
+#pragma unroll
+    for (int i = 0; i < NC / 16; ++i) tmem_ld16(taddr + 16 * i, v + 16 * i);
+  } else if constexpr (NC == 8) {
+    tmem_ld8(taddr, v);
+  } else if constexpr (NC == 4) {
+    tmem_ld4(taddr, v);
+  } else if constexpr (NC == 2) {
+    tmem_ld2(taddr, v);
+  } else {
+    static_assert(NC == 1, "column count");
+    tmem_ld1(taddr, v);
+  }
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -138,19 +193,25 @@ struct Params {
   int items;               // U * n_cblocks
   float scale;
   int mode;
-  // store mode
-  float* out;              // [U][C][n]
+  int ksplit;              // key splits per (unit, centroid block)
+  int64_t tiles_per_split;
+  // store mode (sample pass)
+  uint16_t* out16;         // [U][C][n] top 16 bits of the score keys
   // filter mode
   const float* thresh;     // [U*C]
-  int32_t* counts;         // [U*C]
+  int32_t* counts;         // [U*C] (zeroed before the pass)
   uint64_t* cand;          // [U*C][cap]
   int cap;
 };
 
-template <int KATOMS>
+template <int KATOMS, int GS>
 __global__ void __launch_bounds__(kThreads, 1)
     scores_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                      Params p) {
+  constexpr int CB = kBN / GS;     // centroids per item
+  constexpr int NC = CB / 4;       // centroids per epilogue warp (64 / GS)
+  constexpr int W = 16 / GS > 0 ? 16 / GS : 1;   // centroids per register chunk (16 values)
+  constexpr int NCH = NC / W;                     // 4 chunks per tile
   extern __shared__ uint8_t smem_raw[];
   // 1 KB alignment for the 128B swizzle atoms
   const uint32_t raw = smem_u32(smem_raw);
@@ -171,11 +232,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bfull = bar0 + 8u * (2 * kStages + 4);
   const uint32_t bempty = bar0 + 8u * (2 * kStages + 5);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
-  float* s_thr = reinterpret_cast<float*>(tmem_slot + 4);    // [CB]
-  int* s_cnt = reinterpret_cast<int*>(s_thr + 256);          // [CB]
+  float* s_thr = reinterpret_cast<float*>(tmem_slot + 4);    // [kEpiWarps][NC]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (p.n + kBM - 1) / kBM;
+  // item = ((u * ksplit + ks) * n_cblocks + cb): CTAs running side by side
+  // share a unit's key range (L2 reuse of the A tiles)
+  auto decode = [&](int it, int& u, int& cb, int64_t& t0, int64_t& t1) {
+    cb = it % p.n_cblocks;
+    const int r = it / p.n_cblocks;
+    u = r / p.ksplit;
+    const int ks = r % p.ksplit;
+    t0 = (int64_t)ks * p.tiles_per_split;
+    t1 = t0 + p.tiles_per_split < ntiles ? t0 + p.tiles_per_split : ntiles;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -209,19 +279,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0, item_phase = 0;
       for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
-        const int u = it / p.n_cblocks, cb = it % p.n_cblocks;
+        int u, cb;
+        int64_t t0, t1;
+        decode(it, u, cb, t0, t1);
         const int bi = u / p.g, gi = u % p.g;
         // B: centroid rows (head j, centroids cb*CB ..) of this unit, all K atoms
         mbar_wait(bempty, item_phase ^ 1);
         mbar_expect_tx(bfull, kBBytes);
         for (int ka = 0; ka < KATOMS; ++ka)
-          for (int j = 0; j < p.gs; ++j) {
-            const int32_t row = ((bi * p.h + gi * p.gs + j) * p.C) + cb * p.CB;
-            tma_load_2d(sB + ka * kBAtom + j * p.CB * 128, &mapB, bfull, ka * 64, row);
+          for (int j = 0; j < GS; ++j) {
+            const int32_t row = ((bi * p.h + gi * GS + j) * p.C) + cb * CB;
+            tma_load_2d(sB + ka * kBAtom + j * CB * 128, &mapB, bfull, ka * 64, row);
           }
         item_phase ^= 1;
         const int64_t row0 = p.key_row0 + (int64_t)u * p.key_unit_rows;
-        for (int64_t t = 0; t < ntiles; ++t) {
+        for (int64_t t = t0; t < t1; ++t) {
           mbar_wait(empty(stage), phase ^ 1);
           mbar_expect_tx(full(stage), kABytes);
           for (int ka = 0; ka < KATOMS; ++ka)
@@ -237,10 +309,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0, item_phase = 0;
       for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+        int u, cb;
+        int64_t t0, t1;
+        decode(it, u, cb, t0, t1);
         mbar_wait(bfull, item_phase);
         item_phase ^= 1;
         tc_fence_after();
-        for (int64_t t = 0; t < ntiles; ++t) {
+        for (int64_t t = t0; t < t1; ++t) {
           mbar_wait(tempty(acc), acc_phase ^ 1);
           mbar_wait(full(stage), phase);
           tc_fence_after();
@@ -262,67 +337,83 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ===================== epilogue (8 warps) =====================
-    const int ew = warp - 2;               // 0..7
-    const int quad = warp & 3;             // TMEM lane quadrant this warp may touch
-    const int half = ew >> 2;              // which half of the CB centroids
-    const int hcb = p.CB / 2;              // centroids per epilogue warp
+    // ===================== epilogue (16 warps) =====================
+    // warp ew = warp - 2 reads TMEM lanes 32*(warp % 4) (the quadrant its
+    // hardware warp slot may touch) and centroids [part*NC, part*NC + NC)
+    const int ew = warp - 2;
+    const int quad = warp & 3;
+    const int part = ew >> 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
-      const int u = it / p.n_cblocks, cb = it % p.n_cblocks;
-      const int64_t rowbase = (int64_t)u * p.C + (int64_t)cb * p.CB;
+      int u, cb;
+      int64_t t0, t1;
+      decode(it, u, cb, t0, t1);
+      const int64_t rowbase = (int64_t)u * p.C + (int64_t)cb * CB + part * NC;
+      // this warp's NC row thresholds (its private smem slice: no cross-warp sync)
+      float* thr = s_thr + ew * NC;
       if (p.mode == kFilter) {
-        named_bar(1, kEpiWarps * 32);      // previous item's counters are flushed
-        for (int i = threadIdx.x - 64; i < p.CB; i += kEpiWarps * 32) {
-          s_thr[i] = p.thresh[rowbase + i];
-          s_cnt[i] = 0;
-        }
-        named_bar(1, kEpiWarps * 32);
+        __syncwarp();
+        for (int c = lane; c < NC; c += 32) thr[c] = __ldg(p.thresh + rowbase + c);
+        __syncwarp();
       }
-      for (int64_t t = 0; t < ntiles; ++t) {
+      for (int64_t t = t0; t < t1; ++t) {
         mbar_wait(tfull(acc), acc_phase);
         tc_fence_after();
         const int64_t key = t * kBM + quad * 32 + lane;
         const bool valid = key < p.n;
-        const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + acc * kBN;
-        for (int c0 = half * hcb; c0 < (half + 1) * hcb; c0 += 16) {
-          float m[16], v[16];
-          tmem_ld16(tbase + c0, m);
-          for (int j = 1; j < p.gs; ++j) {
-            tmem_ld16(tbase + j * p.CB + c0, v);
-            tmem_ld_wait();
+        const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + acc * kBN + part * NC;
+        // four column chunks of W centroids x GS heads (16 live values; the
+        // TMEM read of 4 B per score, 64 B/clk per SM, is this kernel's bound,
+        // so loads stay in flight across the 4 warps per SM sub-partition);
+        // the accumulator goes back to the MMA warp once the last chunk has
+        // landed in registers
+#pragma unroll 1
+        for (int ch = 0; ch < NCH; ++ch) {
+          float v[GS][W];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) m[i] = fmaxf(m[i], v[i]);
-          }
+          for (int j = 0; j < GS; ++j) tmem_ld_cols<W>(tbase + j * CB + ch * W, v[j]);
           tmem_ld_wait();
+          if (ch == NCH - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty(acc));
+          }
+#pragma unroll
+          for (int c = 0; c < W; ++c) {
+            float m = v[0][c];
+#pragma unroll
+            for (int j = 1; j < GS; ++j) m = fmaxf(m, v[j][c]);
+            v[0][c] = m * p.scale;
+          }
+          const int64_t row0 = rowbase + ch * W;
           if (p.mode == kStore) {
             if (valid) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
-                p.out[(rowbase + c0 + i) * p.n + key] = m[i] * p.scale;
+              for (int c = 0; c < W; ++c)
+                p.out16[(row0 + c) * p.n + key] = (uint16_t)(okey32(v[0][c]) >> 16);
             }
-          } else if (valid) {
+          } else {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float s = m[i] * p.scale;
-              if (s >= s_thr[c0 + i]) {
-                const int pos = atomicAdd(&s_cnt[c0 + i], 1);
+            for (int c = 0; c < W; ++c) {
+              const bool hit = valid && v[0][c] >= thr[ch * W + c];
+              const unsigned bal = __ballot_sync(0xffffffffu, hit);
+              if (bal == 0u) continue;
+              // one counter reservation per (warp, row): the leader adds the popcount
+              const int leader = __ffs(bal) - 1;
+              int base0 = 0;
+              if (lane == leader) base0 = atomicAdd(p.counts + row0 + c, __popc(bal));
+              base0 = __shfl_sync(0xffffffffu, base0, leader);
+              if (hit) {
+                const int pos = base0 + __popc(bal & ((1u << lane) - 1u));
                 if (pos < p.cap)
-                  p.cand[(rowbase + c0 + i) * p.cap + pos] =
-                      ((uint64_t)(~okey32(s)) << 32) | (uint32_t)key;
+                  p.cand[(row0 + c) * p.cap + pos] =
+                      ((uint64_t)(~okey32(v[0][c])) << 32) | (uint32_t)key;
               }
             }
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty(acc));
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      }
-      if (p.mode == kFilter) {
-        named_bar(1, kEpiWarps * 32);
-        for (int i = threadIdx.x - 64; i < p.CB; i += kEpiWarps * 32) p.counts[rowbase + i] = s_cnt[i];
       }
     }
   }
@@ -348,18 +439,19 @@ __global__ void gather_sample_kernel(const uint4* __restrict__ keys, uint4* __re
   }
 }
 
-// per row: k-th largest of n sample scores (row resident in smem)
-__global__ void __launch_bounds__(256) kth_value_kernel(const float* __restrict__ S, int64_t n,
+// per row: the k-th largest of n 16-bit sample keys (row resident in smem),
+// as the lower edge of its 16-bit bin: every score whose key is >= it passes
+__global__ void __launch_bounds__(256) kth_value_kernel(const uint16_t* __restrict__ S, int64_t n,
                                                         int k, float* __restrict__ thr) {
-  extern __shared__ uint32_t keys_s[];
+  extern __shared__ uint16_t keys_s[];
   __shared__ int hist[2048];
   __shared__ int s_bin, s_above;
-  const float* row = S + (int64_t)blockIdx.x * n;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) keys_s[i] = okey32(row[i]);
+  const uint16_t* row = S + (int64_t)blockIdx.x * n;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) keys_s[i] = row[i];
   uint32_t prefix = 0;
   int above = 0;
-  const int shifts[3] = {21, 10, 0}, widths[3] = {11, 11, 10};
-  for (int pass = 0; pass < 3; ++pass) {
+  const int shifts[2] = {5, 0}, widths[2] = {11, 5};
+  for (int pass = 0; pass < 2; ++pass) {
     const int sh = shifts[pass], nb = 1 << widths[pass], hsh = sh + widths[pass];
     for (int i = threadIdx.x; i < 2048; i += blockDim.x) hist[i] = 0;
     __syncthreads();
@@ -369,7 +461,7 @@ __global__ void __launch_bounds__(256) kth_value_kernel(const float* __restrict_
     }
     __syncthreads();
     if (threadIdx.x < 32) {
-      // lane L owns the L-th block of bins from the top
+      // lane L owns the L-th block of bins from the top (nb >= 32)
       const int lane = threadIdx.x, per = nb / 32, hi = nb - lane * per, want = k - above;
       int sum = 0;
       for (int b = hi - 1; b >= hi - per; --b) sum += hist[b];
@@ -393,7 +485,7 @@ __global__ void __launch_bounds__(256) kth_value_kernel(const float* __restrict_
     prefix |= (uint32_t)s_bin << sh;
     above += s_above;
   }
-  if (threadIdx.x == 0) thr[blockIdx.x] = okey32_inv(prefix);
+  if (threadIdx.x == 0) thr[blockIdx.x] = okey32_inv(prefix << 16);
 }
 
 // per row: exact top-rho of the candidates in (score desc, key asc) order, or
@@ -479,34 +571,6 @@ __global__ void __launch_bounds__(kSelT) select_kernel(const uint64_t* __restric
   }
 }
 
-// full-row scores for fallback rows: one CTA per (row, 256-key block)
-__global__ void __launch_bounds__(256) row_scores_kernel(const __nv_bfloat16* __restrict__ cent,
-                                                         const __nv_bfloat16* __restrict__ keys,
-                                                         const int32_t* __restrict__ rows, int C,
-                                                         int gs, int h, int g, int d, int64_t cap,
-                                                         int64_t off, int64_t n, float scale,
-                                                         float* __restrict__ out) {
-  __shared__ float qs[16 * 256];
-  const int r = rows[blockIdx.y];
-  const int u = r / C, c = r % C;
-  const int bi = u / g, gi = u % g;
-  for (int i = threadIdx.x; i < gs * d; i += blockDim.x) {
-    const int j = i / d, e = i % d;
-    qs[i] = __bfloat162float(cent[(((int64_t)bi * h + gi * gs + j) * C + c) * d + e]);
-  }
-  __syncthreads();
-  const int64_t key = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (key >= n) return;
-  const __nv_bfloat16* kr = keys + ((int64_t)u * cap + off + key) * d;
-  float m = -INFINITY;
-  for (int j = 0; j < gs; ++j) {
-    float a = 0.f;
-    for (int e = 0; e < d; ++e) a = fmaf(qs[j * d + e], __bfloat162float(kr[e]), a);
-    m = fmaxf(m, a);
-  }
-  out[(int64_t)blockIdx.y * n + key] = m * scale;
-}
-
 // ---- host -----------------------------------------------------------------
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -543,7 +607,7 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int d, int
 
 static size_t smem_bytes(int katoms) {
   return 1024 + (size_t)kStages * katoms * kAtomBytes + (size_t)katoms * kBN * 128 + 8 * 16 + 16 +
-         256 * 4 * 2;
+         sizeof(float) * kEpiWarps * 64;
 }
 
 static int num_sms() {
@@ -556,20 +620,48 @@ static int num_sms() {
   return n;
 }
 
-static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int katoms,
-                       cudaStream_t st) {
-  const size_t sm = smem_bytes(katoms);
+template <int KATOMS, int GS>
+static int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
+                         cudaStream_t st) {
+  const size_t sm = smem_bytes(KATOMS);
   const int grid = std::min(p.items, num_sms());
-  if (katoms == 2) {
-    cudaFuncSetAttribute(scores_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    scores_tc_kernel<2><<<grid, kThreads, sm, st>>>(ma, mb, p);
-  } else if (katoms == 1) {
-    cudaFuncSetAttribute(scores_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    scores_tc_kernel<1><<<grid, kThreads, sm, st>>>(ma, mb, p);
-  } else {
-    return CTKV_ESHAPE;
-  }
+  auto k = scores_tc_kernel<KATOMS, GS>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k<<<grid, kThreads, sm, st>>>(ma, mb, p);
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+}
+
+template <int KATOMS>
+static int launch_gemm_k(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p,
+                         cudaStream_t st) {
+  switch (p.gs) {
+    case 1: return launch_gemm_t<KATOMS, 1>(ma, mb, p, st);
+    case 2: return launch_gemm_t<KATOMS, 2>(ma, mb, p, st);
+    case 4: return launch_gemm_t<KATOMS, 4>(ma, mb, p, st);
+    case 8: return launch_gemm_t<KATOMS, 8>(ma, mb, p, st);
+    case 16: return launch_gemm_t<KATOMS, 16>(ma, mb, p, st);
+  }
+  return CTKV_ESHAPE;
+}
+
+// work items: (unit, centroid block, key split); split the keys until every
+// SM has ~8 items (load balance at small batch x C), keeping >= 16 tiles each
+static void set_items(Params& gp) {
+  const int64_t ntiles = (gp.n + kBM - 1) / kBM;
+  const int base = gp.U * gp.n_cblocks;
+  int ks = (8 * num_sms() + base - 1) / base;
+  ks = (int)std::max<int64_t>(1, std::min<int64_t>(ks, ntiles / 16));
+  gp.tiles_per_split = (ntiles + ks - 1) / ks;
+  gp.ksplit = (int)((ntiles + gp.tiles_per_split - 1) / gp.tiles_per_split);
+  gp.items = base * gp.ksplit;
+}
+
+static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, Params p, int katoms,
+                       cudaStream_t st) {
+  set_items(p);
+  if (katoms == 2) return launch_gemm_k<2>(ma, mb, p, st);
+  if (katoms == 1) return launch_gemm_k<1>(ma, mb, p, st);
+  return CTKV_ESHAPE;
 }
 
 struct Plan {
@@ -588,8 +680,9 @@ static Plan make_plan(const BuildParams& p) {
   pl.ks = (int)std::ceil(mean + 6.0 * std::sqrt(mean)) + 1;
   if (pl.ks > pl.ns) pl.ks = (int)pl.ns;
   const int64_t expect = (int64_t)pl.ks * pl.S;
-  // candidates above the sample threshold: ~expect +- S*sqrt(ks); 8 sigma of
-  // headroom (rows beyond it take the exact fallback)
+  // candidates above the sample threshold: ~expect +- S*sqrt(ks) (plus the
+  // 16-bit bin the threshold is widened to); 8 sigma of headroom (rows beyond
+  // it take the exact fallback)
   const int64_t head = (int64_t)std::ceil(8.0 * pl.S * std::sqrt((double)pl.ks));
   pl.cap = (int)std::min<int64_t>(((std::max<int64_t>(expect + head, p.rho + 1024) + 255) / 256) * 256,
                                   1 << 14);
@@ -607,41 +700,62 @@ bool build_tc_supported(const BuildParams& p, int dtype) {
   const int CB = tc::kBN / p.gs;
   if (p.C % CB != 0) return false;
   if (p.n_off < 4096 || p.rho < 1) return false;
+  if (tc::make_plan(p).ns * 2 > 200 * 1024) return false;   // kth row in smem
   return true;
 }
 
-size_t build_tc_workspace_bytes(const BuildParams& p) {
+namespace {
+struct TcWs {
+  __nv_bfloat16* skeys;
+  uint16_t* skey16;
+  float* thr;
+  int32_t* counts;
+  uint64_t* cand;
+  int32_t* fail_n;
+  int32_t* fail_rows;
+  float* scratch;      // fallback rows (aliases the sample keys + scores)
+  int scratch_rows;
+  size_t bytes;
+};
+
+TcWs carve_tc(const BuildParams& p, void* base) {
   const tc::Plan pl = tc::make_plan(p);
   const int64_t U = (int64_t)p.b * p.g;
-  size_t b = 0;
   auto a256 = [](size_t x) { return (x + 255) & ~size_t(255); };
-  b += a256((size_t)U * pl.ns * p.d * 2);               // sample keys
-  b += a256((size_t)U * p.C * pl.ns * 4);               // sample scores
-  b += a256((size_t)U * p.C * 4) * 2;                   // thresholds + counts
-  b += a256((size_t)U * p.C * pl.cap * 8);              // candidates
-  b += a256((size_t)U * p.C * 4 + 16);                  // fail list
-  return b;
+  size_t off = 0;
+  auto take = [&](size_t b) {
+    char* q = base ? static_cast<char*>(base) + off : nullptr;
+    off += a256(b);
+    return q;
+  };
+  TcWs w;
+  const size_t sk = (size_t)U * pl.ns * p.d * 2, ss = (size_t)U * p.C * pl.ns * 2;
+  // the fallback scratch reuses the sample region (dead after the thresholds)
+  const size_t fb_min = (size_t)8 * p.n_off * 4;
+  const size_t shared = std::max(a256(sk) + a256(ss), fb_min);
+  char* sh = take(shared);
+  w.skeys = reinterpret_cast<__nv_bfloat16*>(sh);
+  w.skey16 = reinterpret_cast<uint16_t*>(sh ? sh + a256(sk) : nullptr);
+  w.scratch = reinterpret_cast<float*>(sh);
+  w.scratch_rows = (int)std::min<int64_t>(148, (int64_t)(shared / ((size_t)p.n_off * 4)));
+  w.thr = reinterpret_cast<float*>(take((size_t)U * p.C * 4));
+  w.counts = reinterpret_cast<int32_t*>(take((size_t)U * p.C * 4));
+  w.cand = reinterpret_cast<uint64_t*>(take((size_t)U * p.C * pl.cap * 8));
+  w.fail_n = reinterpret_cast<int32_t*>(take((size_t)U * p.C * 4 + 16));
+  w.fail_rows = w.fail_n ? w.fail_n + 4 : nullptr;
+  w.bytes = off;
+  return w;
 }
+}  // namespace
+
+size_t build_tc_workspace_bytes(const BuildParams& p) { return carve_tc(p, nullptr).bytes; }
 
 int build_tc(const BuildParams& p, int /*dtype*/, void* ws, size_t ws_bytes, cudaStream_t st) {
   using namespace tc;
   const Plan pl = make_plan(p);
   const int U = p.b * p.g;
-  if (build_tc_workspace_bytes(p) > ws_bytes) return CTKV_EWORKSPACE;
-  auto a256 = [](size_t x) { return (x + 255) & ~size_t(255); };
-  char* w = static_cast<char*>(ws);
-  __nv_bfloat16* skeys = reinterpret_cast<__nv_bfloat16*>(w);
-  w += a256((size_t)U * pl.ns * p.d * 2);
-  float* sscore = reinterpret_cast<float*>(w);
-  w += a256((size_t)U * p.C * pl.ns * 4);
-  float* thr = reinterpret_cast<float*>(w);
-  w += a256((size_t)U * p.C * 4);
-  int32_t* counts = reinterpret_cast<int32_t*>(w);
-  w += a256((size_t)U * p.C * 4);
-  uint64_t* cand = reinterpret_cast<uint64_t*>(w);
-  w += a256((size_t)U * p.C * pl.cap * 8);
-  int32_t* fail_n = reinterpret_cast<int32_t*>(w);
-  int32_t* fail_rows = fail_n + 4;
+  const TcWs w = carve_tc(p, ws);
+  if (w.bytes > ws_bytes) return CTKV_EWORKSPACE;
   const int katoms = p.d / 64;
   const float scale = (float)(1.0 / std::sqrt((double)p.d));
 
@@ -650,11 +764,11 @@ int build_tc(const BuildParams& p, int /*dtype*/, void* ws, size_t ws_bytes, cud
     const int vpr = p.d * 2 / 16;
     const int64_t total = (int64_t)U * pl.ns * vpr;
     gather_sample_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, st>>>(
-        static_cast<const uint4*>(p.keys), reinterpret_cast<uint4*>(skeys), p.cap, p.off_begin, pl.S,
-        pl.ns, vpr, U);
+        static_cast<const uint4*>(p.keys), reinterpret_cast<uint4*>(w.skeys), p.cap, p.off_begin,
+        pl.S, pl.ns, vpr, U);
   }
   CUtensorMap mapS, mapK, mapC;
-  if (!make_map(&mapS, skeys, (int64_t)U * pl.ns, p.d, kBM) ||
+  if (!make_map(&mapS, w.skeys, (int64_t)U * pl.ns, p.d, kBM) ||
       !make_map(&mapK, p.keys, (int64_t)U * p.cap, p.d, kBM) ||
       !make_map(&mapC, p.cent, (int64_t)p.b * p.h * p.C, p.d, pl.CB))
     return CTKV_ECUDA;
@@ -666,63 +780,41 @@ int build_tc(const BuildParams& p, int /*dtype*/, void* ws, size_t ws_bytes, cud
   gp.h = p.h;
   gp.g = p.g;
   gp.n_cblocks = p.C / pl.CB;
-  gp.items = U * gp.n_cblocks;
   gp.scale = scale;
-  // 2. sample pass (store) + thresholds
+  // 2. sample pass (16-bit score keys) + thresholds
   gp.n = pl.ns;
   gp.key_row0 = 0;
   gp.key_unit_rows = pl.ns;
   gp.mode = kStore;
-  gp.out = sscore;
+  gp.out16 = w.skey16;
   if (int rc = launch_gemm(mapS, mapC, gp, katoms, st)) return rc;
-  const size_t kth_smem = (size_t)pl.ns * 4;
-  if (kth_smem > 200 * 1024) return CTKV_ECONFIG;
-  cudaFuncSetAttribute(kth_value_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kth_smem);
-  kth_value_kernel<<<(unsigned)(U * p.C), 256, kth_smem, st>>>(sscore, pl.ns, pl.ks, thr);
+  const size_t kth_smem = (size_t)pl.ns * 2;
+  if (kth_smem > 48 * 1024)
+    cudaFuncSetAttribute(kth_value_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kth_smem);
+  kth_value_kernel<<<(unsigned)(U * p.C), 256, kth_smem, st>>>(w.skey16, pl.ns, pl.ks, w.thr);
   // 3. filter pass over all keys
+  cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * (size_t)U * p.C, st);
   gp.n = p.n_off;
   gp.key_row0 = p.off_begin;
   gp.key_unit_rows = p.cap;
   gp.mode = kFilter;
-  gp.thresh = thr;
-  gp.counts = counts;
-  gp.cand = cand;
+  gp.thresh = w.thr;
+  gp.counts = w.counts;
+  gp.cand = w.cand;
   gp.cap = pl.cap;
   if (int rc = launch_gemm(mapK, mapC, gp, katoms, st)) return rc;
   // 4. select
-  cudaMemsetAsync(fail_n, 0, sizeof(int32_t), st);
+  cudaMemsetAsync(w.fail_n, 0, sizeof(int32_t), st);
   const size_t sel_smem = (size_t)pl.cap * 12;
   cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
-  select_kernel<<<(unsigned)(U * p.C), kSelT, sel_smem, st>>>(cand, counts, pl.cap, p.rho, p.C,
-                                                            p.lists, (int32_t)p.off_begin, fail_n,
-                                                            fail_rows);
-  // 5. exact fallback for rows outside [rho, cap] (host reads the count once)
-  int32_t nf = 0;
-  cudaMemcpyAsync(&nf, fail_n, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) return CTKV_ECUDA;
-  if (nf > 0) {
-    if (p.flags) {
-      const int32_t bit = kFlagBuildFallback;
-      // OR the info bit in (tiny kernel-free path: read-modify-write on stream order)
-      int32_t cur = 0;
-      cudaMemcpy(&cur, p.flags, 4, cudaMemcpyDeviceToHost);
-      cur |= bit;
-      cudaMemcpy(p.flags, &cur, 4, cudaMemcpyHostToDevice);
-    }
-    // reuse the sample-score buffer as scratch, in chunks of rows
-    const int64_t chunk = std::max<int64_t>(1, ((int64_t)U * p.C * pl.ns) / p.n_off);
-    for (int64_t r0 = 0; r0 < nf; r0 += chunk) {
-      const int64_t nr = std::min<int64_t>(chunk, nf - r0);
-      dim3 grid((unsigned)((p.n_off + 255) / 256), (unsigned)nr);
-      row_scores_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(p.cent),
-                                              static_cast<const __nv_bfloat16*>(p.keys),
-                                              fail_rows + r0, p.C, p.gs, p.h, p.g, p.d, p.cap,
-                                              p.off_begin, p.n_off, scale, sscore);
-      if (int rc = topk_launch(sscore, nr, p.n_off, p.n_off, p.rho, p.lists, p.rho,
-                               (int32_t)p.off_begin, st, -1, 0, fail_rows + r0))
-        return rc;
-    }
-  }
+  select_kernel<<<(unsigned)(U * p.C), kSelT, sel_smem, st>>>(w.cand, w.counts, pl.cap, p.rho, p.C,
+                                                            p.lists, (int32_t)p.off_begin, w.fail_n,
+                                                            w.fail_rows);
+  // 5. exact fallback for rows outside [rho, cap], driven by the device count
+  if (int rc = launch_build_fallback(p.cent, p.keys, w.fail_n, w.fail_rows, p.C, p.gs, p.h, p.g, p.d,
+                                     p.cap, p.off_begin, p.n_off, scale, w.scratch,
+                                     std::max(1, w.scratch_rows), p.rho, p.lists, p.flags, st))
+    return rc;
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
 

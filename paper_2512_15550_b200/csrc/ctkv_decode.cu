@@ -291,7 +291,7 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
   // the rows are in flight; the query may come from the previous kernel and
   // rides its own bulk copy
   pdl_wait();
-  uint64_t* barq = &bars[kMaxGroup - 1];
+  uint64_t* barq = &bars[kMaxGroup];   // after the gs (<= kMaxGroup) head barriers
   if (threadIdx.x == 0) {
     bar_init(barq, 1);
     bar_expect(barq, (uint32_t)(gs * D * sizeof(T)));
@@ -618,7 +618,7 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
 template <typename T, int D>
 __global__ void __launch_bounds__(kScanRowsV2, 4) scan2_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ uint64_t bars[kMaxGroup];
+  __shared__ uint64_t bars[kMaxGroup + 1];
   ktl_mark(p.tl, 0, false);
   s2mark(p, 0);
   const int64_t t0 = p.total ? *p.total : p.id_bound;

@@ -309,28 +309,34 @@ __device__ __forceinline__ void top_merge_shfl(TopEnt (&t)[K], int o) {
 template <int K>
 __device__ void block_top_k(const double* vals, int C, int cp, int32_t* out, double* cval,
                             int* cidx) {
+  constexpr int PT = 16;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   TopEnt t[K];
 #pragma unroll
   for (int r = 0; r < K; ++r) t[r] = TopEnt{0ull, INT32_MAX};
-  constexpr int PT = 16;
-  const int per = (C + (int)blockDim.x - 1) / (int)blockDim.x;   // uniform
-  // PT strided values per thread in flight; C > PT * blockDim takes more
-  // rounds (C <= 4096 at every BASELINE config: one round)
-  for (int x0 = 0; x0 < per; x0 += PT) {
+  if (C <= PT * (int)blockDim.x) {
+    // PT strided values per thread in flight (every BASELINE config: C <= 4096)
     double v[PT];
 #pragma unroll
     for (int x = 0; x < PT; ++x) {
-      const int c = threadIdx.x + (x0 + x) * (int)blockDim.x;
+      const int c = threadIdx.x + x * (int)blockDim.x;
       v[x] = c < C ? __ldcg(vals + c) : 0.0;
     }
+    const int per = (C + (int)blockDim.x - 1) / (int)blockDim.x;   // uniform
 #pragma unroll
     for (int x = 0; x < PT; ++x) {
-      if (x0 + x >= per) break;
-      const int c = threadIdx.x + (x0 + x) * (int)blockDim.x;
+      if (x >= per) break;
+      const int c = threadIdx.x + x * (int)blockDim.x;
       TopEnt e{c < C ? okey64(v[x]) : 0ull, c < C ? c : INT32_MAX};
 #pragma unroll
       for (int r = 0; r < K; ++r) top_cswap(t[r], e);   // insertion: t stays sorted
+    }
+  } else {
+    // larger C: one value at a time
+    for (int c = threadIdx.x; c < C; c += (int)blockDim.x) {
+      TopEnt e{okey64(__ldcg(vals + c)), c};
+#pragma unroll
+      for (int r = 0; r < K; ++r) top_cswap(t[r], e);
     }
   }
 #pragma unroll

@@ -178,6 +178,11 @@ struct BuildParams {
 };
 
 size_t build_workspace_bytes(const BuildParams& p);
+// exact recompute of the tensor-core build's unfinished rows (ctkv_build.cu)
+int launch_build_fallback(const void* cent, const void* keys, const int32_t* fail_n,
+                          const int32_t* fail_rows, int C, int gs, int h, int g, int d, int64_t cap,
+                          int64_t off, int64_t n, float scale, float* scratch, int grid, int rho,
+                          int32_t* lists, int32_t* flags, cudaStream_t st);
 int launch_build(const BuildParams& p, int dtype, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_scores(int dtype, int b, int h, int g, int d, const void* q, int64_t m, const void* k,
                   int64_t n, int64_t k_row_stride, int grouped, float* out, cudaStream_t st);

@@ -34,7 +34,7 @@ import torch
 from . import _native as N
 from .errors import ConfigError
 from .index import QueryCentroidIndex
-from .parallel import ShardPlan
+from .parallel import ShardPlan, gather_lane_outputs
 from .retrieval import DecodeConfig, StepBuffers
 from .store import KvStore
 
@@ -155,17 +155,11 @@ class DecodeEngine:
             N.check(rc, "decode_step")
 
     def _gather(self, k: int, li: int) -> None:
-        """All-gather lane k's layer-li output slice [bl, h_loc, d] and place
-        it into the global [B, H, d] view (rank-major, ShardPlan.assemble)."""
-        import torch.distributed as dist
-        plan, buf = self.plan, self._gbuf[k]
-        local = self.out[li, k * self.bl:(k + 1) * self.bl]
-        dist.all_gather_into_tensor(buf.view((-1,) + tuple(local.shape[1:])), local,
-                                    group=self.group)
-        for r in range(plan.world):
-            b0 = plan.batch_range(r)[0] + k * self.bl
-            h0, h1 = plan.q_range(r)
-            self.gathered[li, b0:b0 + self.bl, h0:h1].copy_(buf[r])
+        """All-gather lane k's layer-li output slice [bl, h_loc, d] into the
+        global [B, H, d] view (parallel.gather_lane_outputs)."""
+        b0 = k * self.bl
+        gather_lane_outputs(self.plan, self.out[li, b0:b0 + self.bl], self._gbuf[k],
+                            self.gathered[li], b0, self.group)
 
     def _enqueue_timed(self, events) -> None:
         """Serial eager step on the current stream with CUDA events around

@@ -103,3 +103,20 @@ def all_gather_outputs(plan: ShardPlan, local: torch.Tensor, group=None,
     dist.all_gather_into_tensor(buf.view((-1,) + tuple(local.shape[1:])), local.contiguous(),
                                 group=group)
     return plan.assemble(buf)
+
+
+def gather_lane_outputs(plan: ShardPlan, local: torch.Tensor, buf: torch.Tensor,
+                        out: torch.Tensor, lane_b0: int, group=None) -> None:
+    """The engine's per-(layer, lane) collective: all-gather one lane's
+    local output slice `local` [bl, h_loc, d] (sequences lane_b0 ..
+    lane_b0+bl of every rank's batch shard) through `buf` [world, bl, h_loc,
+    d] and place each rank's part into the global `out` [B, H, d] view.
+    Every rank issues it with the same (layer, lane) order, so the
+    collectives match."""
+    import torch.distributed as dist
+    bl = local.shape[0]
+    dist.all_gather_into_tensor(buf.view((-1,) + tuple(local.shape[1:])), local, group=group)
+    for r in range(plan.world):
+        b0 = plan.batch_range(r)[0] + lane_b0
+        h0, h1 = plan.q_range(r)
+        out[b0:b0 + bl, h0:h1].copy_(buf[r])

@@ -22,6 +22,11 @@ def pytest_collection_modifyitems(config, items):
     except Exception:  # pragma: no cover
         has_cuda = False
     if has_cuda:
+        # a device-side hang must not stall the whole suite: per-test limit
+        # (pytest-timeout, thread method: dumps stacks and exits the process)
+        for item in items:
+            if "gpu" in item.keywords and item.get_closest_marker("timeout") is None:
+                item.add_marker(pytest.mark.timeout(600, method="thread"))
         return
     skip = pytest.mark.skip(reason="no CUDA device in this container")
     for item in items:

@@ -16,7 +16,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import ctkv_oracle as O
-from paper_2512_15550_b200.parallel import ShardPlan, all_gather_outputs
+from paper_2512_15550_b200.parallel import ShardPlan, all_gather_outputs, gather_lane_outputs
 
 B, H, G, D, S, T = 4, 8, 4, 32, 384, 5
 PARAMS = dict(init_len=8, local_len=40, capacity=24, rho=48)
@@ -111,3 +111,46 @@ def test_assemble_inverts_gather_layout():
         h0, h1 = plan.q_range(r)
         parts.append(full[b0:b1, h0:h1])
     assert torch.equal(plan.assemble(torch.stack(parts)), full)
+
+
+def _lane_worker(rank, world, port, q, lanes):
+    """The engine's collective path (DecodeEngine._gather ->
+    gather_lane_outputs) with gloo: per layer and lane, in the engine's
+    (layer, lane) order, every rank all-gathers its lane slice into the
+    global [L, B, H, d] output."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        Bg, Hg, Gg, Dg, NL = 8, 32, 8, 16, 3
+        plan = ShardPlan(world, rank, Bg, Gg, Hg)
+        full = torch.arange(NL * Bg * Hg * Dg, dtype=torch.float32).view(NL, Bg, Hg, Dg)
+        b0, b1 = plan.batch_range()
+        h0, h1 = plan.q_range()
+        out = full[:, b0:b1, h0:h1].contiguous()           # this rank's engine.out
+        bl = plan.b_loc // lanes
+        gathered = torch.zeros_like(full)
+        bufs = [torch.empty((world, bl, plan.h_loc, Dg)) for _ in range(lanes)]
+        for li in range(NL):
+            for k in range(lanes):
+                gather_lane_outputs(plan, out[li, k * bl:(k + 1) * bl], bufs[k], gathered[li],
+                                    k * bl)
+        if rank == 0:
+            q.put(torch.equal(gathered, full))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,lanes", [(2, 2), (4, 2), (8, 1)])
+def test_engine_lane_gather_reassembles_every_layer(world, lanes):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lane_worker, args=(r, world, port, q, lanes)) for r in range(world)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok
