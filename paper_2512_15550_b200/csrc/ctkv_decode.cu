@@ -478,7 +478,8 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   __shared__ double wmax[kScanRowsV2 / 32][kMaxGroup];   // per-warp head maxima (tensor-core path)
   bool mma_logits = false;
-  if constexpr (sizeof(T) == 2 && D >= 64) {
+  // (the m16n8 tile holds 8 heads: gs = 16 takes the SIMT logits below)
+  if constexpr (sizeof(T) == 2 && D >= 64) if (gs <= 8) {
     // logits on the tensor cores: warp w takes tokens [16w, 16w+16) as the A
     // operand of mma.m16n8k16 (f32 per 16-element k-step, f64 across), the
     // gs heads as B columns; k permuted alike in K and q (as in the chain).
@@ -530,7 +531,8 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
 #pragma unroll
       for (int e = 0; e < 2; ++e)
         if (2 * t4 + e < gs) wmax[warp][2 * t4 + e] = mloc[e];
-  } else {
+  }
+  if (!mma_logits) {
     // logits: pair (t, j), consecutive threads -> consecutive tokens
     for (int pr = threadIdx.x; pr < nt * gs; pr += blockDim.x) {
       const int t = pr % nt, j = pr / nt;
