@@ -10,14 +10,15 @@
 // centroids x gs heads = 64 accumulator columns, read with one batch of
 // tcgen05.ld and a single wait, group max + scale in registers.
 // A work item is (unit, centroid block, key split); small problems split the
-// keys so every SM has work (candidate counters are global, warp-aggregated).
+// keys so every SM has work; each (row, key split) owns a candidate segment
+// whose counter lives in shared memory for the item (no global atomics).
 //
 // Top-rho per row without materialising the 6.4 GB/layer score matrix:
 //   1. sample pass  -- the same GEMM against every S-th key; the epilogue
 //                      stores only the top 16 bits of each score's
 //                      order-preserving key (2 B per sampled score);
-//   2. threshold    -- per row the k_s-th largest sample key (2-pass radix
-//                      select), widened to its 16-bit bin's lower edge, with
+//   2. threshold    -- per row the lower edge of the histogram bin holding
+//                      the k_s-th largest sample key (warp per row), with
 //                      k_s chosen so the full row has ~rho + 6 sigma
 //                      candidates above it with overwhelming probability;
 //   3. filter pass  -- the full GEMM; the epilogue keeps (score, key) pairs
@@ -176,6 +177,25 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// predicated (branch-free) shared-memory slot reservation: old value of
+// *addr, incremented, when `pred`; `otherwise` when not
+__device__ __forceinline__ int atom_inc_if(bool pred, uint32_t addr, int otherwise) {
+  int r = otherwise;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+      "@p atom.shared.add.u32 %0, [%1], 1;\n\t}"
+      : "+r"(r)
+      : "r"(addr), "r"((int)pred)
+      : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_global_if(bool pred, uint64_t* ptr, uint64_t v) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+      "@p st.global.u64 [%0], %1;\n\t}" ::"l"(ptr),
+      "l"(v), "r"((int)pred)
+      : "memory");
+}
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -199,8 +219,8 @@ struct Params {
   uint16_t* out16;         // [U][C][n] top 16 bits of the score keys
   // filter mode
   const float* thresh;     // [U*C]
-  int32_t* counts;         // [U*C] (zeroed before the pass)
-  uint64_t* cand;          // [U*C][cap]
+  int32_t* counts;         // [U*C][ksplit] candidates per (row, key split)
+  uint64_t* cand;          // [U*C][ksplit][cap]
   int cap;
 };
 
@@ -210,8 +230,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                      Params p) {
   constexpr int CB = kBN / GS;     // centroids per item
   constexpr int NC = CB / 4;       // centroids per epilogue warp (64 / GS)
-  constexpr int W = 16 / GS > 0 ? 16 / GS : 1;   // centroids per register chunk (16 values)
-  constexpr int NCH = NC / W;                     // 4 chunks per tile
+  constexpr int WV = 32 / GS < 16 ? 32 / GS : 16;
+  constexpr int W = NC < WV ? NC : WV;            // centroids per register chunk (<= 32 values)
+  constexpr int NCH = NC / W;                     // chunks per tile
   extern __shared__ uint8_t smem_raw[];
   // 1 KB alignment for the 128B swizzle atoms
   const uint32_t raw = smem_u32(smem_raw);
@@ -233,16 +254,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t bempty = bar0 + 8u * (2 * kStages + 5);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 6);
   float* s_thr = reinterpret_cast<float*>(tmem_slot + 4);    // [kEpiWarps][NC]
+  int* s_cnt = reinterpret_cast<int*>(s_thr + kEpiWarps * 64); // [CB] candidates per row (item)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (p.n + kBM - 1) / kBM;
   // item = ((u * ksplit + ks) * n_cblocks + cb): CTAs running side by side
   // share a unit's key range (L2 reuse of the A tiles)
-  auto decode = [&](int it, int& u, int& cb, int64_t& t0, int64_t& t1) {
+  auto decode = [&](int it, int& u, int& cb, int& ks, int64_t& t0, int64_t& t1) {
     cb = it % p.n_cblocks;
     const int r = it / p.n_cblocks;
     u = r / p.ksplit;
-    const int ks = r % p.ksplit;
+    ks = r % p.ksplit;
     t0 = (int64_t)ks * p.tiles_per_split;
     t1 = t0 + p.tiles_per_split < ntiles ? t0 + p.tiles_per_split : ntiles;
   };
@@ -279,9 +301,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0, item_phase = 0;
       for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
-        int u, cb;
+        int u, cb, ks;
         int64_t t0, t1;
-        decode(it, u, cb, t0, t1);
+        decode(it, u, cb, ks, t0, t1);
         const int bi = u / p.g, gi = u % p.g;
         // B: centroid rows (head j, centroids cb*CB ..) of this unit, all K atoms
         mbar_wait(bempty, item_phase ^ 1);
@@ -309,9 +331,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0, item_phase = 0;
       for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
-        int u, cb;
+        int u, cb, ks;
         int64_t t0, t1;
-        decode(it, u, cb, t0, t1);
+        decode(it, u, cb, ks, t0, t1);
         mbar_wait(bfull, item_phase);
         item_phase ^= 1;
         tc_fence_after();
@@ -343,19 +365,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;
     const int quad = warp & 3;
     const int part = ew >> 2;
+    const int etid = threadIdx.x - 64;
+    constexpr int kEpiT = 32 * kEpiWarps;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
-      int u, cb;
+      int u, cb, ks;
       int64_t t0, t1;
-      decode(it, u, cb, t0, t1);
+      decode(it, u, cb, ks, t0, t1);
       const int64_t rowbase = (int64_t)u * p.C + (int64_t)cb * CB + part * NC;
       // this warp's NC row thresholds (its private smem slice: no cross-warp sync)
       float* thr = s_thr + ew * NC;
+      int* cnt = s_cnt + part * NC;
       if (p.mode == kFilter) {
         __syncwarp();
         for (int c = lane; c < NC; c += 32) thr[c] = __ldg(p.thresh + rowbase + c);
-        __syncwarp();
+        for (int i = etid; i < CB; i += kEpiT) s_cnt[i] = 0;
+        named_bar(1, kEpiT);
       }
       for (int64_t t = t0; t < t1; ++t) {
         mbar_wait(tfull(acc), acc_phase);
@@ -363,11 +389,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t key = t * kBM + quad * 32 + lane;
         const bool valid = key < p.n;
         const uint32_t tbase = tmem + ((uint32_t)(quad * 32) << 16) + acc * kBN + part * NC;
-        // four column chunks of W centroids x GS heads (16 live values; the
-        // TMEM read of 4 B per score, 64 B/clk per SM, is this kernel's bound,
-        // so loads stay in flight across the 4 warps per SM sub-partition);
-        // the accumulator goes back to the MMA warp once the last chunk has
-        // landed in registers
+        // column chunks of W centroids x GS heads (<= 64 live values: for
+        // GS >= 4 all of the warp's columns in one batch and one wait); the
+        // accumulator goes back to the MMA warp once the last chunk is in
+        // registers, before the chunk's group max / filter
 #pragma unroll 1
         for (int ch = 0; ch < NCH; ++ch) {
           float v[GS][W];
@@ -394,26 +419,40 @@ __global__ void __launch_bounds__(kThreads, 1)
                 p.out16[(row0 + c) * p.n + key] = (uint16_t)(okey32(v[0][c]) >> 16);
             }
           } else {
+            // hits are rare (~2 % of scores): each lane reserves its own
+            // slots with shared-memory atomics on the row counters (no
+            // ballots, no shuffles; same-row lanes are merged by the atomic unit)
+            unsigned hits = 0u;
 #pragma unroll
-            for (int c = 0; c < W; ++c) {
-              const bool hit = valid && v[0][c] >= thr[ch * W + c];
-              const unsigned bal = __ballot_sync(0xffffffffu, hit);
-              if (bal == 0u) continue;
-              // one counter reservation per (warp, row): the leader adds the popcount
-              const int leader = __ffs(bal) - 1;
-              int base0 = 0;
-              if (lane == leader) base0 = atomicAdd(p.counts + row0 + c, __popc(bal));
-              base0 = __shfl_sync(0xffffffffu, base0, leader);
-              if (hit) {
-                const int pos = base0 + __popc(bal & ((1u << lane) - 1u));
-                if (pos < p.cap)
-                  p.cand[(row0 + c) * p.cap + pos] =
-                      ((uint64_t)(~okey32(v[0][c])) << 32) | (uint32_t)key;
-              }
+            for (int c = 0; c < W; c += 2) {
+              const float2 t = *reinterpret_cast<const float2*>(thr + ch * W + c);
+              hits |= (unsigned)(v[0][c] >= t.x) << c;
+              hits |= (unsigned)(v[0][c + 1] >= t.y) << (c + 1);
+            }
+            if (!valid) hits = 0u;
+            if (__any_sync(0xffffffffu, hits != 0u)) {
+              // all of this lane's reservations first (independent, in
+              // flight together), then the stores
+              uint64_t* dst = p.cand + (row0 * p.ksplit + ks) * p.cap;
+              const int rstride = p.ksplit * p.cap;
+              const uint32_t cnt_s = smem_u32(cnt + ch * W);
+              int pos[W];
+#pragma unroll
+              for (int c = 0; c < W; ++c) pos[c] = atom_inc_if((hits >> c) & 1u, cnt_s + 4 * c, p.cap);
+#pragma unroll
+              for (int c = 0; c < W; ++c)
+                st_global_if(pos[c] < p.cap, dst + (uint32_t)(c * rstride + pos[c]),
+                             ((uint64_t)(~okey32(v[0][c])) << 32) | (uint32_t)key);
             }
           }
         }
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      if (p.mode == kFilter) {
+        named_bar(1, kEpiT);   // every warp's hits of this item are counted
+        const int64_t r0 = (int64_t)u * p.C + (int64_t)cb * CB;
+        for (int i = etid; i < CB; i += kEpiT) p.counts[(r0 + i) * p.ksplit + ks] = s_cnt[i];
+        named_bar(1, kEpiT);   // before the next item resets the counters
       }
     }
   }
@@ -439,53 +478,91 @@ __global__ void gather_sample_kernel(const uint4* __restrict__ keys, uint4* __re
   }
 }
 
-// per row: the k-th largest of n 16-bit sample keys (row resident in smem),
-// as the lower edge of its 16-bit bin: every score whose key is >= it passes
-__global__ void __launch_bounds__(256) kth_value_kernel(const uint16_t* __restrict__ S, int64_t n,
-                                                        int k, float* __restrict__ thr) {
-  extern __shared__ uint16_t keys_s[];
-  __shared__ int hist[2048];
-  __shared__ int s_bin, s_above;
-  const uint16_t* row = S + (int64_t)blockIdx.x * n;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) keys_s[i] = row[i];
-  uint32_t prefix = 0;
-  int above = 0;
-  const int shifts[2] = {5, 0}, widths[2] = {11, 5};
-  for (int pass = 0; pass < 2; ++pass) {
-    const int sh = shifts[pass], nb = 1 << widths[pass], hsh = sh + widths[pass];
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint32_t key = keys_s[i];
-      if (pass == 0 || (key >> hsh) == (prefix >> hsh)) atomicAdd(&hist[(key >> sh) & (nb - 1)], 1);
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      // lane L owns the L-th block of bins from the top (nb >= 32)
-      const int lane = threadIdx.x, per = nb / 32, hi = nb - lane * per, want = k - above;
-      int sum = 0;
-      for (int b = hi - 1; b >= hi - per; --b) sum += hist[b];
-      int incl = sum;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const int excl = incl - sum;
-      const unsigned bal = __ballot_sync(0xffffffffu, incl >= want && excl < want);
-      if (lane == __ffs(bal) - 1) {
-        int run = excl;
-        for (int b = hi - 1; b >= hi - per; --b) {
-          if (run + hist[b] >= want) { s_bin = b; s_above = run; break; }
-          run += hist[b];
-        }
-      }
-    }
-    __syncthreads();
-    prefix |= (uint32_t)s_bin << sh;
-    above += s_above;
+// per row: a threshold with at least k of the row's n 16-bit sample keys at
+// or above it -- the lower edge of the histogram bin holding the k-th
+// largest key.  One warp per row: min/max of the keys, then a 1024-bin
+// histogram over [min, max] (power-of-two bin width, so spread-out bins and
+// little atomic contention), then a top-down prefix over the bins.  Any
+// such threshold is valid (the filter pass keeps every score at or above
+// it); a narrower bin only means fewer surplus candidates.
+constexpr int kKthWarps = 8, kKthBins = 1024;
+__global__ void __launch_bounds__(32 * kKthWarps) kth_value_kernel(const uint16_t* __restrict__ S,
+                                                                  int64_t n, int64_t rows, int k,
+                                                                  float* __restrict__ thr) {
+  __shared__ int hist_all[kKthWarps][kKthBins];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kKthWarps + warp;
+  if (row >= rows) return;
+  int* hist = hist_all[warp];
+  const uint16_t* r = S + row * n;
+  uint32_t mn = 0xffffu, mx = 0u;
+  for (int64_t i = lane; i < n; i += 32) {
+    const uint32_t x = __ldg(r + i);
+    mn = min(mn, x);
+    mx = max(mx, x);
   }
-  if (threadIdx.x == 0) thr[blockIdx.x] = okey32_inv(prefix << 16);
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  int sh = 0;
+  while (((mx - mn) >> sh) >= (uint32_t)kKthBins) ++sh;
+  for (int b = lane; b < kKthBins; b += 32) hist[b] = 0;
+  __syncwarp();
+  for (int64_t i = lane; i < n; i += 32) atomicAdd(&hist[(__ldg(r + i) - mn) >> sh], 1);
+  __syncwarp();
+  // lane L owns bins [kKthBins - 32(L+1), kKthBins - 32L): counts from the top
+  constexpr int per = kKthBins / 32;
+  const int hi = kKthBins - lane * per;
+  int sum = 0;
+  for (int b = hi - 1; b >= hi - per; --b) sum += hist[b];
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int want = min(k, (int)n);
+  unsigned bal = __ballot_sync(0xffffffffu, incl >= want && incl - sum < want);
+  const int owner = __ffs(bal) - 1;
+  int bin = 0, above = 0;
+  if (lane == owner) {
+    int run = incl - sum;
+    bin = hi - per;
+    for (int b = hi - 1; b >= hi - per; --b) {
+      if (run + hist[b] >= want) { bin = b; break; }
+      run += hist[b];
+    }
+    above = run;   // keys in bins above `bin`
+  }
+  bin = __shfl_sync(0xffffffffu, bin, owner);
+  above = __shfl_sync(0xffffffffu, above, owner);
+  uint32_t key = mn + ((uint32_t)bin << sh);
+  if (sh > 0) {
+    // refine inside the bin (2^sh <= 64 distinct keys): exact k-th largest
+    __syncwarp();
+    for (int b = lane; b < 64; b += 32) hist[b] = 0;
+    __syncwarp();
+    const uint32_t lo = key, wid = 1u << sh;
+    for (int64_t i = lane; i < n; i += 32) {
+      const uint32_t x = __ldg(r + i) - lo;
+      if (x < wid) atomicAdd(&hist[x], 1);
+    }
+    __syncwarp();
+    // lane L owns sub-bins 2L, 2L+1 counted from the top (63 - 2L, 62 - 2L)
+    const int b0 = 63 - 2 * lane, b1 = 62 - 2 * lane;
+    const int c0 = b0 < (int)wid ? hist[b0] : 0, c1 = b1 < (int)wid ? hist[b1] : 0;
+    int inc2 = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc2, o);
+      if (lane >= o) inc2 += y;
+    }
+    const int ex2 = above + inc2 - c0 - c1;
+    bal = __ballot_sync(0xffffffffu, ex2 + c0 + c1 >= want && ex2 < want);
+    const int o2 = __ffs(bal) - 1;
+    const int sub = ex2 + c0 >= want ? b0 : b1;
+    key = lo + (uint32_t)__shfl_sync(0xffffffffu, sub, o2);
+  }
+  if (lane == 0) thr[row] = okey32_inv(key << 16);
 }
 
 // per row: exact top-rho of the candidates in (score desc, key asc) order, or
@@ -495,29 +572,37 @@ __global__ void __launch_bounds__(256) kth_value_kernel(const uint16_t* __restri
 // (small) bin; ranks < rho are written straight to the list.
 constexpr int kSelT = 256, kSelBins = 2048;
 __global__ void __launch_bounds__(kSelT) select_kernel(const uint64_t* __restrict__ cand,
-                                                       const int32_t* __restrict__ counts, int cap,
+                                                       const int32_t* __restrict__ counts, int nsplit,
+                                                       int cap,
                                                        int rho, int C, int32_t* __restrict__ lists,
                                                        int32_t add, int32_t* fail_n,
                                                        int32_t* fail_rows) {
   extern __shared__ uint64_t ck[];                            // [cap] candidates
-  int* binned = reinterpret_cast<int*>(ck + cap);             // [cap] indices grouped by bin
-  __shared__ int hist[kSelBins], cur[kSelBins];
+  uint16_t* binned = reinterpret_cast<uint16_t*>(ck + cap);  // [cap] indices grouped by bin
+  // bin counts, then (in place) exclusive starts, then after the scatter
+  // each bin's end: bin b spans [end[b-1], end[b])
+  __shared__ int hist[kSelBins];
   __shared__ uint32_t s_mm[2 * kSelT / 32];
   __shared__ int s_ws[kSelT / 32 + 1];
   const int64_t row = blockIdx.x;
-  const int cnt = counts[row];
+  int cnt = 0;
+  for (int s = 0; s < nsplit; ++s) cnt += __ldg(counts + row * nsplit + s);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (cnt < rho || cnt > cap) {
     if (tid == 0) fail_rows[atomicAdd(fail_n, 1)] = (int32_t)row;
     return;
   }
-  const uint64_t* src = cand + row * cap;
   uint32_t mn = 0xffffffffu, mx = 0u;
-  for (int i = tid; i < cnt; i += kSelT) {
-    const uint64_t k = __ldg(src + i);
-    ck[i] = k;
-    mn = min(mn, (uint32_t)(k >> 32));
-    mx = max(mx, (uint32_t)(k >> 32));
+  for (int s = 0, at = 0; s < nsplit; ++s) {
+    const int n_s = __ldg(counts + row * nsplit + s);
+    const uint64_t* src = cand + (row * nsplit + s) * cap;
+    for (int i = tid; i < n_s; i += kSelT) {
+      const uint64_t k = __ldg(src + i);
+      ck[at + i] = k;
+      mn = min(mn, (uint32_t)(k >> 32));
+      mx = max(mx, (uint32_t)(k >> 32));
+    }
+    at += n_s;
   }
   mn = __reduce_min_sync(0xffffffffu, mn);
   mx = __reduce_max_sync(0xffffffffu, mx);
@@ -552,18 +637,19 @@ __global__ void __launch_bounds__(kSelT) select_kernel(const uint64_t* __restric
     int run = wpre + incl - loc;
 #pragma unroll
     for (int x = 0; x < BPT; ++x) {
-      cur[tid * BPT + x] = run;
-      run += hist[tid * BPT + x];
+      const int c = hist[tid * BPT + x];
+      hist[tid * BPT + x] = run;
+      run += c;
     }
   }
   __syncthreads();
-  for (int i = tid; i < cnt; i += kSelT) binned[atomicAdd(&cur[bin_of(ck[i])], 1)] = i;
+  for (int i = tid; i < cnt; i += kSelT) binned[atomicAdd(&hist[bin_of(ck[i])], 1)] = (uint16_t)i;
   __syncthreads();
   int32_t* dst = lists + row * rho;
   for (int i = tid; i < cnt; i += kSelT) {
     const uint64_t k = ck[i];
     const int b = bin_of(k);
-    const int e = cur[b], s0 = e - hist[b];
+    const int e = hist[b], s0 = b > 0 ? hist[b - 1] : 0;
     if (s0 >= rho) continue;                    // the whole bin ranks below the list
     int r = s0;
     for (int x = s0; x < e; ++x) r += ck[binned[x]] < k;
@@ -607,7 +693,7 @@ static bool make_map(CUtensorMap* map, const void* ptr, int64_t rows, int d, int
 
 static size_t smem_bytes(int katoms) {
   return 1024 + (size_t)kStages * katoms * kAtomBytes + (size_t)katoms * kBN * 128 + 8 * 16 + 16 +
-         sizeof(float) * kEpiWarps * 64;
+         sizeof(float) * kEpiWarps * 64 + sizeof(int) * kBN;
 }
 
 static int num_sms() {
@@ -646,14 +732,19 @@ static int launch_gemm_k(const CUtensorMap& ma, const CUtensorMap& mb, const Par
 
 // work items: (unit, centroid block, key split); split the keys until every
 // SM has ~8 items (load balance at small batch x C), keeping >= 16 tiles each
-static void set_items(Params& gp) {
-  const int64_t ntiles = (gp.n + kBM - 1) / kBM;
-  const int base = gp.U * gp.n_cblocks;
+static int key_splits(int64_t n, int U, int n_cblocks, int64_t* tiles_per_split) {
+  const int64_t ntiles = (n + kBM - 1) / kBM;
+  const int base = U * n_cblocks;
   int ks = (8 * num_sms() + base - 1) / base;
   ks = (int)std::max<int64_t>(1, std::min<int64_t>(ks, ntiles / 16));
-  gp.tiles_per_split = (ntiles + ks - 1) / ks;
-  gp.ksplit = (int)((ntiles + gp.tiles_per_split - 1) / gp.tiles_per_split);
-  gp.items = base * gp.ksplit;
+  const int64_t tps = (ntiles + ks - 1) / ks;
+  if (tiles_per_split) *tiles_per_split = tps;
+  return (int)((ntiles + tps - 1) / tps);
+}
+
+static void set_items(Params& gp) {
+  gp.ksplit = key_splits(gp.n, gp.U, gp.n_cblocks, &gp.tiles_per_split);
+  gp.items = gp.U * gp.n_cblocks * gp.ksplit;
 }
 
 static int launch_gemm(const CUtensorMap& ma, const CUtensorMap& mb, Params p, int katoms,
@@ -668,8 +759,9 @@ struct Plan {
   int S;        // sample stride
   int64_t ns;   // sampled keys per unit
   int ks;       // sample rank giving the threshold
-  int cap;      // candidate slots per row
+  int cap;      // candidate slots per row (and per key split of a row)
   int CB;
+  int fsplit;   // key splits of the filter pass
 };
 
 static Plan make_plan(const BuildParams& p) {
@@ -687,6 +779,7 @@ static Plan make_plan(const BuildParams& p) {
   pl.cap = (int)std::min<int64_t>(((std::max<int64_t>(expect + head, p.rho + 1024) + 255) / 256) * 256,
                                   1 << 14);
   pl.CB = kBN / p.gs;
+  pl.fsplit = key_splits(p.n_off, p.b * p.g, p.C / pl.CB, nullptr);
   return pl;
 }
 
@@ -700,7 +793,6 @@ bool build_tc_supported(const BuildParams& p, int dtype) {
   const int CB = tc::kBN / p.gs;
   if (p.C % CB != 0) return false;
   if (p.n_off < 4096 || p.rho < 1) return false;
-  if (tc::make_plan(p).ns * 2 > 200 * 1024) return false;   // kth row in smem
   return true;
 }
 
@@ -739,8 +831,10 @@ TcWs carve_tc(const BuildParams& p, void* base) {
   w.scratch = reinterpret_cast<float*>(sh);
   w.scratch_rows = (int)std::min<int64_t>(148, (int64_t)(shared / ((size_t)p.n_off * 4)));
   w.thr = reinterpret_cast<float*>(take((size_t)U * p.C * 4));
-  w.counts = reinterpret_cast<int32_t*>(take((size_t)U * p.C * 4));
-  w.cand = reinterpret_cast<uint64_t*>(take((size_t)U * p.C * pl.cap * 8));
+  // each (row, key split) owns a whole cap-slot segment: a split never
+  // overflows before the row does (top scores may cluster in one split)
+  w.counts = reinterpret_cast<int32_t*>(take((size_t)U * p.C * pl.fsplit * 4));
+  w.cand = reinterpret_cast<uint64_t*>(take((size_t)U * p.C * pl.fsplit * pl.cap * 8));
   w.fail_n = reinterpret_cast<int32_t*>(take((size_t)U * p.C * 4 + 16));
   w.fail_rows = w.fail_n ? w.fail_n + 4 : nullptr;
   w.bytes = off;
@@ -788,12 +882,10 @@ int build_tc(const BuildParams& p, int /*dtype*/, void* ws, size_t ws_bytes, cud
   gp.mode = kStore;
   gp.out16 = w.skey16;
   if (int rc = launch_gemm(mapS, mapC, gp, katoms, st)) return rc;
-  const size_t kth_smem = (size_t)pl.ns * 2;
-  if (kth_smem > 48 * 1024)
-    cudaFuncSetAttribute(kth_value_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kth_smem);
-  kth_value_kernel<<<(unsigned)(U * p.C), 256, kth_smem, st>>>(w.skey16, pl.ns, pl.ks, w.thr);
-  // 3. filter pass over all keys
-  cudaMemsetAsync(w.counts, 0, sizeof(int32_t) * (size_t)U * p.C, st);
+  const int64_t nrows = (int64_t)U * p.C;
+  kth_value_kernel<<<(unsigned)((nrows + kKthWarps - 1) / kKthWarps), 32 * kKthWarps, 0, st>>>(
+      w.skey16, pl.ns, nrows, pl.ks, w.thr);
+  // 3. filter pass over all keys (every (row, split) count is written by its item)
   gp.n = p.n_off;
   gp.key_row0 = p.off_begin;
   gp.key_unit_rows = p.cap;
@@ -805,9 +897,9 @@ int build_tc(const BuildParams& p, int /*dtype*/, void* ws, size_t ws_bytes, cud
   if (int rc = launch_gemm(mapK, mapC, gp, katoms, st)) return rc;
   // 4. select
   cudaMemsetAsync(w.fail_n, 0, sizeof(int32_t), st);
-  const size_t sel_smem = (size_t)pl.cap * 12;
+  const size_t sel_smem = (size_t)pl.cap * 10;
   cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
-  select_kernel<<<(unsigned)(U * p.C), kSelT, sel_smem, st>>>(w.cand, w.counts, pl.cap, p.rho, p.C,
+  select_kernel<<<(unsigned)(U * p.C), kSelT, sel_smem, st>>>(w.cand, w.counts, pl.fsplit, pl.cap, p.rho, p.C,
                                                             p.lists, (int32_t)p.off_begin, w.fail_n,
                                                             w.fail_rows);
   // 5. exact fallback for rows outside [rho, cap], driven by the device count
