@@ -216,7 +216,7 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   if (phase < 1) return CTKV_ECONFIG;
   if (int rc = check_layout(L)) return rc;
   if (!A || !A->query || !A->out || !S.keys || !S.values || !S.total) return CTKV_ECONFIG;
-  if (I.capacity < 1) return CTKV_ECONFIG;                            // "recall: empty index"
+  if (I.capacity < 1 || I.capacity > (1 << 20)) return CTKV_ECONFIG;   // slot keys: 20 bits                            // "recall: empty index"
   if (A->c_prime < 1 || A->c_prime > I.capacity) return CTKV_ECONFIG;  // ck/retrieval.py:138
   if (A->rho_prime < 1) return CTKV_ECONFIG;
   if (I.rho < 0 || I.rho > 8 * 512) return CTKV_ECONFIG;
@@ -307,7 +307,7 @@ int ctkv_recall(const ctkv_layout* L, ctkv_index I, int64_t id_bound, const void
                 int32_t c_prime, int32_t* selected, int32_t* recalled, int32_t* recall_len,
                 int32_t* flags, void* workspace, size_t workspace_bytes, void* stream) {
   if (int rc = check_layout(L)) return rc;
-  if (I.capacity < 1) return CTKV_ECONFIG;
+  if (I.capacity < 1 || I.capacity > (1 << 20)) return CTKV_ECONFIG;   // slot keys: 20 bits
   if (c_prime < 1 || c_prime > I.capacity) return CTKV_ECONFIG;
   if (I.rho < 0 || I.rho > 8 * 512) return CTKV_ECONFIG;
   const int lmax = c_prime * I.rho;

@@ -99,7 +99,6 @@ constexpr int kCW = kCT / 32;
 constexpr int kCB = 128;         // selected rows per attention batch
 constexpr int kCMaxLists = 8;    // c' <= 8
 constexpr int kCMaxPer = 32;     // list entries per thread (keep mask bits)
-constexpr int kKUn = 8;          // K-row passes in flight per warp (4 rows each)
 constexpr int kVUn = 8;          // V-row passes in flight per warp (2 rows each)
 constexpr int kCBins = 1024;     // top-rho' selection: histogram bins
 constexpr int kCBnd = 256;       // ... and keys ranked exactly in the boundary bin

@@ -367,7 +367,7 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
     __syncthreads();
     s2mark(p, 6);
     block_top_slots(p.gcos + (int64_t)u * p.C, p.C, p.c_prime, p.selg + (int64_t)u * p.c_prime,
-                    cosv, reinterpret_cast<int*>(cosv + 64));
+                    reinterpret_cast<uint64_t*>(cosv));
     s2mark(p, 7);
     return;
   }

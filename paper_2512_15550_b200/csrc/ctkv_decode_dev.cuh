@@ -267,105 +267,111 @@ static __device__ void warp_top_slots(const DecodeParams& p, int u, int32_t* sel
 
 // Top-C' slots of vals[0..C) (value desc, slot asc; ck/tensor_ops.py:121-141
 // on the group-max cosines of ck/retrieval.py:145-154) with the whole block,
-// by sorting networks (no serial arg-max rounds, no lane-divergent code
-// around the shuffles; scripts/micro/topc_bench):
+// by sorting networks over one 64-bit key per entry (no serial arg-max
+// rounds, no lane-divergent code around the shuffles):
 //   1. each thread keeps a sorted top-K of its strided values (branch-free
 //      insertion);
 //   2. warps merge lane lists pairwise by butterflies: the top-K of two
-//      sorted K-lists is bitonic after one compare per position, then a
-//      log K half-cleaner sorts it;
+//      sorted K-lists is bitonic after one max per position, then a log K
+//      half-cleaner sorts it;
 //   3. warp 0 merges the warps' lists the same way.
-// K = 4 or 8 >= c'; C <= 16 values per thread.  cval/cidx: shared scratch of
-// (blockDim/32) * K entries.
-struct TopEnt {
-  uint64_t k;
-  int i;
-};
-__device__ __forceinline__ bool top_better(const TopEnt& a, const TopEnt& b) {
-  return (a.k > b.k) | ((a.k == b.k) & (a.i < b.i));
+// The key is the value's order key with its low kSlotBits bits replaced by
+// (mask - slot): one unsigned compare orders by (value desc, slot asc).
+// Values closer than 2^-32 relative compare by slot alone -- far inside the
+// north_star's 1e-6 tie window (the cosines themselves carry f32-chunk
+// rounding).
+constexpr int kSlotBits = 20;                       // C <= 2^20
+constexpr uint64_t kSlotMask = (1ull << kSlotBits) - 1;
+__device__ __forceinline__ uint64_t slot_key(double v, int slot) {
+  return (okey64(v) & ~kSlotMask) | (kSlotMask - (uint64_t)slot);
 }
-__device__ __forceinline__ void top_cswap(TopEnt& a, TopEnt& b) {   // a := better
-  const bool sw = top_better(b, a);
-  const TopEnt t = a;
-  a = sw ? b : a;
-  b = sw ? t : b;
-}
+__device__ __forceinline__ int key_slot(uint64_t k) { return (int)(kSlotMask - (k & kSlotMask)); }
+
 template <int K>
-__device__ __forceinline__ void top_merge_shfl(TopEnt (&t)[K], int o) {
-  TopEnt pt[K];
+__device__ __forceinline__ void topk_insert(uint64_t (&t)[K], uint64_t e) {
 #pragma unroll
   for (int r = 0; r < K; ++r) {
-    pt[r].k = __shfl_xor_sync(0xffffffffu, t[r].k, o);
-    pt[r].i = __shfl_xor_sync(0xffffffffu, t[r].i, o);
+    const uint64_t hi = t[r] > e ? t[r] : e;
+    e = t[r] > e ? e : t[r];
+    t[r] = hi;
   }
+}
+// merge with the list of lane (lane ^ o): both sorted descending
+template <int K>
+__device__ __forceinline__ void topk_merge_shfl(uint64_t (&t)[K], int o) {
+  uint64_t pt[K];
 #pragma unroll
-  for (int r = 0; r < K; ++r) t[r] = top_better(t[r], pt[K - 1 - r]) ? t[r] : pt[K - 1 - r];
+  for (int r = 0; r < K; ++r) pt[r] = __shfl_xor_sync(0xffffffffu, t[r], o);
+#pragma unroll
+  for (int r = 0; r < K; ++r) t[r] = t[r] > pt[K - 1 - r] ? t[r] : pt[K - 1 - r];
 #pragma unroll
   for (int st = K / 2; st > 0; st >>= 1)
 #pragma unroll
     for (int r = 0; r < K; ++r)
-      if ((r & st) == 0) top_cswap(t[r], t[r + st]);
+      if ((r & st) == 0) {
+        const uint64_t x = t[r], y = t[r + st];
+        t[r] = x > y ? x : y;
+        t[r + st] = x > y ? y : x;
+      }
 }
-template <int K>
-__device__ void block_top_k(const double* vals, int C, int cp, int32_t* out, double* cval,
-                            int* cidx) {
-  constexpr int PT = 16;
+
+// top-K keys of vals[lo, hi) (slots are absolute indices); the sorted list
+// ends in the registers of lane 0 of warp 0 (lanes < blockDim/32 of warp 0
+// hold it too).  scratch: (blockDim/32)*K.
+template <int K, int PT = 16>
+__device__ void block_top_core(const double* vals, int lo, int hi, uint64_t (&t)[K],
+                               uint64_t* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  TopEnt t[K];
+  const int n = hi - lo;
 #pragma unroll
-  for (int r = 0; r < K; ++r) t[r] = TopEnt{0ull, INT32_MAX};
-  if (C <= PT * (int)blockDim.x) {
-    // PT strided values per thread in flight (every BASELINE config: C <= 4096)
+  for (int r = 0; r < K; ++r) t[r] = 0ull;
+  if (n <= PT * (int)blockDim.x) {
+    // PT strided values per thread in flight
     double v[PT];
 #pragma unroll
     for (int x = 0; x < PT; ++x) {
       const int c = threadIdx.x + x * (int)blockDim.x;
-      v[x] = c < C ? __ldcg(vals + c) : 0.0;
+      v[x] = c < n ? __ldcg(vals + lo + c) : 0.0;
     }
-    const int per = (C + (int)blockDim.x - 1) / (int)blockDim.x;   // uniform
+    const int per = (n + (int)blockDim.x - 1) / (int)blockDim.x;   // uniform
 #pragma unroll
     for (int x = 0; x < PT; ++x) {
       if (x >= per) break;
       const int c = threadIdx.x + x * (int)blockDim.x;
-      TopEnt e{c < C ? okey64(v[x]) : 0ull, c < C ? c : INT32_MAX};
-#pragma unroll
-      for (int r = 0; r < K; ++r) top_cswap(t[r], e);   // insertion: t stays sorted
+      topk_insert<K>(t, c < n ? slot_key(v[x], lo + c) : 0ull);
     }
   } else {
-    // larger C: one value at a time
-    for (int c = threadIdx.x; c < C; c += (int)blockDim.x) {
-      TopEnt e{okey64(__ldcg(vals + c)), c};
-#pragma unroll
-      for (int r = 0; r < K; ++r) top_cswap(t[r], e);
-    }
+    for (int c = threadIdx.x; c < n; c += (int)blockDim.x)
+      topk_insert<K>(t, slot_key(__ldcg(vals + lo + c), lo + c));
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) top_merge_shfl<K>(t, o);
+  for (int o = 16; o > 0; o >>= 1) topk_merge_shfl<K>(t, o);
   if (lane == 0)
 #pragma unroll
-    for (int r = 0; r < K; ++r) {
-      cval[warp * K + r] = __longlong_as_double((long long)t[r].k);
-      cidx[warp * K + r] = t[r].i;
-    }
+    for (int r = 0; r < K; ++r) scratch[warp * K + r] = t[r];
   __syncthreads();
   if (warp == 0) {
 #pragma unroll
-    for (int r = 0; r < K; ++r)
-      t[r] = lane < nw ? TopEnt{(uint64_t)__double_as_longlong(cval[lane * K + r]), cidx[lane * K + r]}
-                       : TopEnt{0ull, INT32_MAX};
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) top_merge_shfl<K>(t, o);
-    if (lane == 0)
-#pragma unroll
-      for (int r = 0; r < K; ++r)
-        if (r < cp) out[r] = t[r].i;                 // compile-time index: t stays in registers
+    for (int r = 0; r < K; ++r) t[r] = lane < nw ? scratch[lane * K + r] : 0ull;
+    for (int o = 16; o > 0; o >>= 1)
+      if (o < nw) topk_merge_shfl<K>(t, o);   // (uniform: lanes >= nw hold nothing)
   }
 }
 
+template <int K>
+__device__ void block_top_k(const double* vals, int C, int cp, int32_t* out, uint64_t* scratch) {
+  uint64_t t[K];
+  block_top_core<K>(vals, 0, C, t, scratch);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+      if (r < cp) out[r] = key_slot(t[r]);          // compile-time index: t stays in registers
+}
+
 static __device__ __noinline__ void block_top_slots(const double* vals, int C, int cp, int32_t* out,
-                                                    double* cval, int* cidx) {
-  if (cp <= 4) block_top_k<4>(vals, C, cp, out, cval, cidx);
-  else block_top_k<8>(vals, C, cp, out, cval, cidx);
+                                                    uint64_t* scratch) {
+  if (cp <= 4) block_top_k<4>(vals, C, cp, out, scratch);
+  else block_top_k<8>(vals, C, cp, out, scratch);
 }
 
 }  // namespace ctkv
