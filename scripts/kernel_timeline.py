@@ -18,6 +18,7 @@ from paper_2512_15550_b200.store import KvStore  # noqa: E402
 
 NL = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 lanes = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+stagger = bool(int(sys.argv[3])) if len(sys.argv) > 3 else False
 b, h, g, d, s, C, T = 8, 32, 8, 128, 98304, 2048, 16
 built, tails = [], []
 for li in range(NL):
@@ -35,7 +36,7 @@ for li in range(NL):
 lib = N.lib()
 lib.ctkv_debug_kernel_timeline(1)
 lib.ctkv_debug_phase_timing(1, None, 0)   # chain phase marks (a launch parameter: on before capture)
-eng = DecodeEngine(built, P.DecodeConfig(4, 512), lanes=lanes)
+eng = DecodeEngine(built, P.DecodeConfig(4, 512), lanes=lanes, stagger=stagger)
 
 
 def load(t):
@@ -78,7 +79,7 @@ for t in range(6):
         for kind, nm in enumerate(["scan", "chain", "tail"]):
             a = np.array(span[kind])
             print(f"  {nm:6s} span per launch: median {np.median(a):6.1f}  p90 {np.percentile(a, 90):6.1f} us")
-        for k_ in (0, lanes - 1):
+        for k_ in range(lanes):
             line = []
             for li in range(NL):
                 v = rows[k_ * NL + li][2]

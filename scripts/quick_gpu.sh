@@ -8,4 +8,4 @@ if [ "$T" = "full" ]; then
 fi
 timeout 300 python scripts/chain_phases.py 8 > gpurun_out/q_cp8.txt 2>&1
 timeout 300 python scripts/kernel_timeline.py 8 8 > gpurun_out/q_kt.txt 2>&1
-timeout 600 python bench.py --no-cpu --steps 20 --warmup 5 > gpurun_out/q_bench.txt 2>&1
+timeout 600 python bench.py --parity-steps 0 --steps 20 --warmup 5 > gpurun_out/q_bench.txt 2>&1
