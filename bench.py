@@ -99,8 +99,6 @@ def parse():
                     help="steps replayed on the CPU per sampled unit (0: no parity leg)")
     ap.add_argument("--parity-units", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--stagger", type=int, default=0,
-                    help="rank the lanes' scans (DecodeEngine stagger): 1 on, 0 off")
     a = ap.parse_args()
     pre = PRESETS[a.config]
     for k, v in pre.items():
@@ -412,7 +410,7 @@ def main():
     unit_ms = statistics.mean(e[1].elapsed_time(e[2]) for run_ in evs for e in run_)
     del tengine
     engine = DecodeEngine(layers, cfg, plan=plan if world > 1 else None, group=group,
-                          lanes=a.lanes, stagger=bool(a.stagger))
+                          lanes=a.lanes)
     # ---- warm-up (eager), capture, more warm-up ----
     for _ in range(max(1, a.warmup // 2)):
         load_inputs(engine)

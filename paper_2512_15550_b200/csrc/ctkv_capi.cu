@@ -210,9 +210,8 @@ int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctk
 int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
                            const ctkv_step_args* A, int32_t phase, void* workspace,
                            size_t workspace_bytes, void* stream) {
-  if (phase < 1 || phase > 255) return CTKV_ECONFIG;
+  if (phase < 1 || phase > 31) return CTKV_ECONFIG;
   const PdlScope pdl_scope((phase & 16) != 0);   // 16: the caller allows programmatic dependent launch
-  const ScanRankScope rank_scope((phase >> 5) & 7);   // bits 5-7: the scan's dispatch rank
   phase &= 15;
   if (phase < 1) return CTKV_ECONFIG;
   if (int rc = check_layout(L)) return rc;

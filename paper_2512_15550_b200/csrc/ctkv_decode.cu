@@ -1739,16 +1739,11 @@ int kernel_timeline(int on) {   // host switch; on < 0 queries
 // Launch priorities: the latency-bound chain kernels are dispatched first,
 // the bandwidth-bound scans and the deferred tails after them (a ready chain
 // otherwise waits ~16 us behind queued scan CTAs).
-thread_local int t_scan_rank = 0;
 int launch_priority(LaunchPrio pr) {
   static int lo = 1, hi = 0, init = 0;
   if (!init) {
     if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) { lo = 0; hi = 0; }
     init = 1;
-  }
-  if (pr == kPrioLow && t_scan_rank > 0) {   // ranked scan: hi + rank, above the tails
-    const int v = hi + t_scan_rank;
-    return v < lo ? v : (lo > hi ? lo - 1 : lo);
   }
   return pr == kPrioHigh ? hi : lo;   // numerically lower = higher priority
 }

@@ -133,15 +133,7 @@ struct PdlScope {
 };
 // Launch priorities (CTA dispatch order when several kernels wait for SMs):
 // the latency-critical chain kernels go first, the bandwidth-bound scans
-// last.  A caller running several micro-batch lanes may rank its scans
-// (phase bits 5-7, rank r >= 1): scans of rank r sit r levels below the
-// chains, so concurrent lanes' scans are served one after another (each at
-// the full bandwidth) instead of all at once; deferred tails stay lowest.
-extern thread_local int t_scan_rank;
-struct ScanRankScope {
-  explicit ScanRankScope(int r) { t_scan_rank = r; }
-  ~ScanRankScope() { t_scan_rank = 0; }
-};
+// last.
 enum LaunchPrio { kPrioLow = 0, kPrioMid = 1, kPrioHigh = 2 };
 int launch_priority(LaunchPrio pr);
 template <typename... KArgs, typename... Args>

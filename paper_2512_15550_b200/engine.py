@@ -52,8 +52,7 @@ class Layer:
 
 class DecodeEngine:
     def __init__(self, layers: list[tuple[KvStore, QueryCentroidIndex]], cfg: DecodeConfig, *,
-                 plan: ShardPlan | None = None, group=None, lanes: int = 1,
-                 stagger: bool = False):
+                 plan: ShardPlan | None = None, group=None, lanes: int = 1):
         if not layers:
             raise ValueError("DecodeEngine needs at least one layer")
         self.cfg = cfg
@@ -67,12 +66,6 @@ class DecodeEngine:
             raise ValueError(f"lanes={lanes} must divide the batch {self.b}")
         self.nlanes = lanes
         self.bl = self.b // lanes
-        # stagger: lane k's scans get dispatch rank k+1 (phase bits 5-7), so
-        # concurrent lanes' scans are served in lane order, each at the full
-        # bandwidth, and the lanes fall into a pipeline (scan of one lane
-        # while the others run their chains) instead of scanning in lockstep
-        self._scan_bits = [((min(k, 6) + 1) << 5) if (stagger and lanes > 1) else 0
-                           for k in range(lanes)]
         self.dtype = st0.dtype
         dev = st0.keys.device
         nl = len(layers)
@@ -228,7 +221,7 @@ class DecodeEngine:
                 # previous layer's chain, before a chain this layer's scan).
                 # The previous layer's tail is released once this layer's scan
                 # is done, so it shares the GPU with this chain, not this scan.
-                self._launch(L, 1 | 16 | self._scan_bits[k], ls)
+                self._launch(L, 1 | 16, ls)
                 if li > 0:
                     es = self._evs[k][li]
                     es.record(ls)

@@ -18,7 +18,6 @@ from paper_2512_15550_b200.store import KvStore  # noqa: E402
 
 NL = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 lanes = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-stagger = bool(int(sys.argv[3])) if len(sys.argv) > 3 else False
 b, h, g, d, s, C, T = 8, 32, 8, 128, 98304, 2048, 16
 built, tails = [], []
 for li in range(NL):
@@ -36,7 +35,7 @@ for li in range(NL):
 lib = N.lib()
 lib.ctkv_debug_kernel_timeline(1)
 lib.ctkv_debug_phase_timing(1, None, 0)   # chain phase marks (a launch parameter: on before capture)
-eng = DecodeEngine(built, P.DecodeConfig(4, 512), lanes=lanes, stagger=stagger)
+eng = DecodeEngine(built, P.DecodeConfig(4, 512), lanes=lanes)
 
 
 def load(t):
