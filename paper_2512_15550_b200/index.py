@@ -110,7 +110,7 @@ class QueryCentroidIndex:
 
     @classmethod
     def build(cls, queries, store: KvStore, capacity: int, rho: int, *,
-              mode: int | None = None) -> "QueryCentroidIndex":
+              mode: int | None = None, workspace: torch.Tensor | None = None) -> "QueryCentroidIndex":
         if queries.ndim != 4:
             raise ShapeError(f"build: queries must be 4-D, got {tuple(queries.shape)}")
         b, h, s, d = queries.shape
@@ -135,7 +135,10 @@ class QueryCentroidIndex:
             lay = store.ctkv_layout()
             lib = N.lib()
             ws_bytes = lib.ctkv_build_workspace_bytes(lay, capacity, rho, off.size, mode)
-            ws = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=cent.device)
+            if workspace is not None and workspace.is_cuda and workspace.numel() >= ws_bytes:
+                ws = workspace   # caller-owned scratch, reused across layers
+            else:
+                ws = torch.empty(max(int(ws_bytes), 1), dtype=torch.uint8, device=cent.device)
             flags = torch.zeros(1, dtype=torch.int32, device=cent.device)
             N.check(lib.ctkv_build_lists(lay, N.ptr(cent), N.ptr(store.keys), int(off[0]),
                                          off.size, capacity, rho, mode, N.ptr(lists), N.ptr(flags),
