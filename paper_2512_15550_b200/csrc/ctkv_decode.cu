@@ -623,16 +623,19 @@ __global__ void __launch_bounds__(kScanRowsV2, 4) scan2_kernel(DecodeParams p) {
   __shared__ uint64_t bars[kMaxGroup + 1];
   ktl_mark(p.tl, 0, false);
   s2mark(p, 0);
-  const int64_t t0 = p.total ? *p.total : p.id_bound;
   const bool appending = p.k_new != nullptr;
-  const int64_t total = t0 + (appending ? 1 : 0);
   const int ncos = p.do_cos ? p.U * p.cos_blocks_per_unit : 0;
-  if ((int)blockIdx.x < ncos)
+  // the token counter is read only where it is used (static tasks, the
+  // append): a cosine CTA issues its centroid copies without that round trip
+  if ((int)blockIdx.x < ncos) {
     cos_task<T, D>(p, blockIdx.x, smem, bars);
-  else
-    static_task<T, D>(p, blockIdx.x - ncos, t0, total, smem, bars);
+  } else {
+    const int64_t t0 = p.total ? *p.total : p.id_bound;
+    static_task<T, D>(p, blockIdx.x - ncos, t0, t0 + (appending ? 1 : 0), smem, bars);
+  }
   s2mark(p, 2);
   if (appending && blockIdx.x == 0) {
+    const int64_t t0 = p.total ? *p.total : p.id_bound;
     T* keys = static_cast<T*>(const_cast<void*>(p.keys));
     T* vals = static_cast<T*>(const_cast<void*>(p.values));
     const T* kn = static_cast<const T*>(p.k_new);
