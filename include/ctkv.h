@@ -153,6 +153,13 @@ int ctkv_build_lists(const ctkv_layout* L, const void* centroids, const void* ke
 int ctkv_centroid_norms(const ctkv_layout* L, const void* centroids, int32_t capacity,
                         float* cnorm, void* stream);
 
+/* Copy `bytes` (a multiple of 16, 16-byte aligned pointers) by a kernel
+ * rather than a DMA: either side may be pinned (page-locked) host memory,
+ * addressed through unified virtual addressing.  The engine's host-I/O step
+ * graph stages its inputs and outputs with it (kernel nodes instead of host
+ * memcpy nodes, which make every graph launch hundreds of us slower). */
+int ctkv_stage_copy(void* dst, const void* src, size_t bytes, void* stream);
+
 /* ---- decode (ck/retrieval.py) --------------------------------------------- */
 
 /* The decode workspace must be zero-filled before its first use; the

@@ -96,6 +96,7 @@ SIGNATURES = {
     "ctkv_debug_kernel_timeline": (c_i32, [c_i32]),
     "ctkv_debug_timeline_rw": (c_i32, [ctypes.POINTER(Layout), c_i32, c_i32, c_i32, c_vp, c_vp, c_i32]),
     "ctkv_centroid_norms": (c_i32, [ctypes.POINTER(Layout), c_vp, c_i32, c_vp, c_vp]),
+    "ctkv_stage_copy": (c_i32, [c_vp, c_vp, c_size, c_vp]),
 }
 
 _lib = None

@@ -486,6 +486,14 @@ int ctkv_centroid_norms(const ctkv_layout* L, const void* centroids, int32_t cap
                                static_cast<cudaStream_t>(stream));
 }
 
+int ctkv_stage_copy(void* dst, const void* src, size_t bytes, void* stream) {
+  if ((bytes & 15) || ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15))
+    return CTKV_ECONFIG;
+  if (bytes == 0) return CTKV_OK;
+  if (!dst || !src) return CTKV_ECONFIG;
+  return launch_stage_copy(dst, src, bytes, static_cast<cudaStream_t>(stream));
+}
+
 int ctkv_debug_kernel_timeline(int32_t on) {
 #ifndef CTKV_PROFILE
   return CTKV_ECONFIG;   // profiling builds only (make -C csrc profile)

@@ -1758,6 +1758,32 @@ int launch_priority(LaunchPrio pr) {
 // centroid TMA loads start before its griddepcontrol wait).
 thread_local int t_pdl_ok = 0;
 
+// 16-byte copy by a kernel (either side may be mapped pinned host memory):
+// every load of a thread issued before its stores, so a PCIe read stream has
+// many requests in flight
+__global__ void __launch_bounds__(256) stage_copy_kernel(uint4* __restrict__ dst,
+                                                         const uint4* __restrict__ src, int64_t n) {
+  constexpr int U = 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    uint4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < n) r[u] = src[i0 + u * stride];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i0 + u * stride < n) dst[i0 + u * stride] = r[u];
+  }
+}
+
+int launch_stage_copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  const int64_t n = (int64_t)(bytes / 16);
+  const int64_t blocks = std::min<int64_t>((n + 1023) / 1024, 4 * 148);
+  stage_copy_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(
+      static_cast<uint4*>(dst), static_cast<const uint4*>(src), n);
+  return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
+}
+
 // |row| for rows of D elements: one warp per row, f64 squares (exact for
 // bf16 and f32 inputs), rounded to f32
 template <typename T, int D>

@@ -190,4 +190,6 @@ size_t topk_workspace_bytes(int64_t rows, int64_t n, int k);
 int launch_topk_rows(const float* v, int64_t rows, int64_t n, int k, int32_t* idx, void* ws,
                      size_t ws_bytes, cudaStream_t st);
 
+int launch_stage_copy(void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 }  // namespace ctkv

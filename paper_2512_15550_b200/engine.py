@@ -154,6 +154,16 @@ class DecodeEngine:
         if rc:
             N.check(rc, "decode_step")
 
+    @staticmethod
+    def _stage(dst: torch.Tensor, src: torch.Tensor, stream) -> None:
+        """Host<->device staging copy by a kernel (ctkv_stage_copy): one side
+        is pinned host memory, reached through unified addressing, so the
+        step graph holds kernel nodes instead of host memcpy nodes (those make
+        every launch of the graph hundreds of microseconds slower)."""
+        assert dst.is_contiguous() and src.is_contiguous() and dst.nbytes == src.nbytes
+        N.check(N.lib().ctkv_stage_copy(dst.data_ptr(), src.data_ptr(), src.nbytes,
+                                        stream.cuda_stream), "stage copy")
+
     def _gather(self, k: int, li: int) -> None:
         """All-gather lane k's layer-li output slice [bl, h_loc, d] into the
         global [B, H, d] view (parallel.gather_lane_outputs)."""
@@ -196,15 +206,14 @@ class DecodeEngine:
             # host inputs: every (layer, lane) slice copied in issue order on
             # one stream, so the copies run ahead of the layers that use them
             hq, hk, hv, _ = hio
-            with torch.cuda.stream(self._cin):
-                for c0 in range(0, self.nl, self._cin_chunk):
-                    c1 = min(self.nl, c0 + self._cin_chunk)
-                    self.q[c0:c1].copy_(hq[c0:c1], non_blocking=True)
-                    self.k[c0:c1].copy_(hk[c0:c1], non_blocking=True)
-                    self.v[c0:c1].copy_(hv[c0:c1], non_blocking=True)
-                    for li in range(c0, c1):
-                        for k in range(self.nlanes):
-                            self._cin_ev[k][li].record(self._cin)
+            for c0 in range(0, self.nl, self._cin_chunk):
+                c1 = min(self.nl, c0 + self._cin_chunk)
+                self._stage(self.q[c0:c1], hq[c0:c1], self._cin)
+                self._stage(self.k[c0:c1], hk[c0:c1], self._cin)
+                self._stage(self.v[c0:c1], hv[c0:c1], self._cin)
+                for li in range(c0, c1):
+                    for k in range(self.nlanes):
+                        self._cin_ev[k][li].record(self._cin)
         for li in range(self.nl):
             for k in range(self.nlanes):
                 L = self.lane_layers[k][li]
@@ -245,12 +254,10 @@ class DecodeEngine:
                     # a finished (layer, lane) output leaves while later layers run
                     self._cout.wait_event(ev)
                     b0, b1 = k * self.bl, (k + 1) * self.bl
-                    with torch.cuda.stream(self._cout):
-                        hio[3][li, b0:b1].copy_(self.out[li, b0:b1], non_blocking=True)
+                    self._stage(hio[3][li, b0:b1], self.out[li, b0:b1], self._cout)
             if hio is not None and self._comm is not None:
                 self._cout.wait_event(self._gev[self.nlanes - 1][li])   # all lanes gathered
-                with torch.cuda.stream(self._cout):
-                    hio[3][li].copy_(self.gathered[li], non_blocking=True)
+                self._stage(hio[3][li], self.gathered[li], self._cout)
         for s in streams:
             main.wait_stream(s)
 
