@@ -206,8 +206,11 @@ class DecodeEngine:
             # host inputs: every (layer, lane) slice copied in issue order on
             # one stream, so the copies run ahead of the layers that use them
             hq, hk, hv, _ = hio
-            for c0 in range(0, self.nl, self._cin_chunk):
-                c1 = min(self.nl, c0 + self._cin_chunk)
+            # layer 0 alone first (the step starts as soon as it is in), then
+            # chunks of _cin_chunk layers running ahead of their use
+            bounds = [0, 1] + list(range(1 + self._cin_chunk, self.nl, self._cin_chunk)) + [self.nl]
+            bounds = sorted(set(min(x, self.nl) for x in bounds))
+            for c0, c1 in zip(bounds[:-1], bounds[1:]):
                 self._stage(self.q[c0:c1], hq[c0:c1], self._cin)
                 self._stage(self.k[c0:c1], hk[c0:c1], self._cin)
                 self._stage(self.v[c0:c1], hv[c0:c1], self._cin)
