@@ -279,7 +279,7 @@ int launch_build_fallback(const void* cent, const void* keys, const int32_t* fai
                           int32_t* lists, int32_t* flags, cudaStream_t st) {
   const size_t sm = sizeof(int) * kTBins + sizeof(uint64_t) * next_pow2(rho);
   if (sm > 200 * 1024 || gs * d > 16 * 256) return CTKV_ECONFIG;
-  cudaFuncSetAttribute(build_fallback_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (int rc = set_max_smem_k(build_fallback_kernel, sm)) return rc;
   build_fallback_kernel<<<grid, kTThreads, sm, st>>>(
       static_cast<const __nv_bfloat16*>(cent), static_cast<const __nv_bfloat16*>(keys), fail_n,
       fail_rows, C, gs, h, g, d, cap, off, n, scale, scratch, rho, lists, flags);
@@ -307,12 +307,12 @@ int topk_launch(const float* v, int64_t rows, int64_t n, int64_t ld, int k, int3
   const size_t sm = topk_smem(n, k, smem_row);
   if (sm > 220 * 1024) return CTKV_ECONFIG;
   if (smem_row) {
-    cudaFuncSetAttribute(topk_rows_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (int rc = set_max_smem_k(topk_rows_kernel<true>, sm)) return rc;
     topk_rows_kernel<true><<<(unsigned)rows, kTThreads, sm, st>>>(v, n, ld, k, out, out_ld, add,
                                                                   rows_per_group, group_stride,
                                                                   row_map);
   } else {
-    cudaFuncSetAttribute(topk_rows_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (int rc = set_max_smem_k(topk_rows_kernel<false>, sm)) return rc;
     topk_rows_kernel<false><<<(unsigned)rows, kTThreads, sm, st>>>(v, n, ld, k, out, out_ld, add,
                                                                   rows_per_group, group_stride,
                                                                   row_map);

@@ -712,7 +712,7 @@ static int launch_gemm_t(const CUtensorMap& ma, const CUtensorMap& mb, const Par
   const size_t sm = smem_bytes(KATOMS);
   const int grid = std::min(p.items, num_sms());
   auto k = scores_tc_kernel<KATOMS, GS>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (int rc = set_max_smem_k(k, sm)) return rc;
   k<<<grid, kThreads, sm, st>>>(ma, mb, p);
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
@@ -898,7 +898,7 @@ int build_tc(const BuildParams& p, int /*dtype*/, void* ws, size_t ws_bytes, cud
   // 4. select
   cudaMemsetAsync(w.fail_n, 0, sizeof(int32_t), st);
   const size_t sel_smem = (size_t)pl.cap * 10;
-  cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem);
+  if (int rc = set_max_smem_k(select_kernel, sel_smem)) return rc;
   select_kernel<<<(unsigned)(U * p.C), kSelT, sel_smem, st>>>(w.cand, w.counts, pl.fsplit, pl.cap, p.rho, p.C,
                                                             p.lists, (int32_t)p.off_begin, w.fail_n,
                                                             w.fail_rows);

@@ -4,6 +4,8 @@
 // (ConfigError, e.g. ck/retrieval.py:136-139), CUDA failures -> CTKV_ECUDA.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 #include "ctkv.h"
 #include "ctkv_internal.h"
@@ -111,6 +113,22 @@ void fill_layout(DecodeParams& p, const ctkv_layout* L) {
 
 
 }  // namespace
+
+namespace ctkv {
+int set_max_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> given;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return CTKV_ECUDA;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = given[{dev, kernel}];
+  if (bytes <= have) return CTKV_OK;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return CTKV_ECUDA;
+  have = bytes;
+  return CTKV_OK;
+}
+}  // namespace ctkv
 
 extern "C" {
 

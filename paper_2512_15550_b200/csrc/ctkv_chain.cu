@@ -809,12 +809,7 @@ static int launch_chain_t(const DecodeParams& p0, cudaStream_t st) {
   p.dbg = g_host_dbg;
   const size_t sm = chain_layout(p, D, CL, nullptr, nullptr);
   auto k = chain_kernel<T, D, CL, GS>;
-  static size_t configured = 0;
-  if (sm > configured) {
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))
-      return CTKV_ECUDA;
-    configured = sm;
-  }
+  if (int rc = set_max_smem_k(k, sm)) return rc;
   launch_k(k, dim3(p.U * CL), dim3(kCT), sm, st, kPrioHigh, p);
   return cudaGetLastError() == cudaSuccess ? CTKV_OK : CTKV_ECUDA;
 }

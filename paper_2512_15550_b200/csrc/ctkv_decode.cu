@@ -1642,11 +1642,7 @@ static int launch_scan_t(const DecodeParams& p0, int nblocks, cudaStream_t st) {
   p.dbg = g_host_dbg;
   const size_t sm = scan2_smem<T, D>(p.gs);
   auto k = scan2_kernel<T, D>;
-  static size_t configured = 0;
-  if (sm > 48 * 1024 && sm > configured) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    configured = sm;
-  }
+  if (int rc = set_max_smem_k(k, sm)) return rc;
   if (nblocks > 0) launch_k(k, dim3(nblocks), dim3(kScanRowsV2), sm, st, kPrioLow, p);
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
@@ -1656,11 +1652,7 @@ static int launch_unit2_t(const DecodeParams& p, cudaStream_t st) {
   const size_t sm = unit2_smem_bytes(p, D);
   if (sm > 200 * 1024) return CTKV_ECONFIG;
   auto k = unit2_kernel<T, D>;
-  static size_t configured = 0;
-  if (sm > configured) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    configured = sm;
-  }
+  if (int rc = set_max_smem_k(k, sm)) return rc;
   k<<<2 * p.U, kU2Threads, sm, st>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
@@ -1670,7 +1662,7 @@ static int launch_unit_t(const DecodeParams& p, cudaStream_t st) {
   const size_t sm = unit_smem_bytes(p, D);
   if (sm > 220 * 1024) return CTKV_ECONFIG;
   auto k = unit_kernel<T, D>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (int rc = set_max_smem_k(k, sm)) return rc;
   k<<<p.U, kUnitThreads, sm, st>>>(p);
   return cudaGetLastError() == cudaSuccess ? 0 : CTKV_ECUDA;
 }
@@ -1679,7 +1671,7 @@ template <typename T, int D>
 static int launch_attn_t(const DecodeParams& p, cudaStream_t st) {
   const size_t sm = scan_smem_bytes(p, D);
   auto k = attn_split_kernel<T, D>;
-  if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (int rc = set_max_smem_k(k, sm)) return rc;
   k<<<p.U * p.ns, kScanThreads, sm, st>>>(p);
   const int64_t n = (int64_t)p.U * p.gs * D;
   attn_merge_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, D);

@@ -192,4 +192,13 @@ int launch_topk_rows(const float* v, int64_t rows, int64_t n, int k, int32_t* id
 
 int launch_stage_copy(void* dst, const void* src, size_t bytes, cudaStream_t st);
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
+// more than it was last given on this device (the per-call API otherwise
+// pays the attribute call on every launch)
+int set_max_smem(const void* kernel, size_t bytes);
+template <typename K>
+inline int set_max_smem_k(K* kernel, size_t bytes) {
+  return set_max_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 }  // namespace ctkv

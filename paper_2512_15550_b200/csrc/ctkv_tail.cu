@@ -159,8 +159,7 @@ static int launch_tail_t(const DecodeParams& p, cudaStream_t st) {
   if (!any) return CTKV_OK;
   auto kt = tail_kernel<T, D>;
   const size_t sm = tail_smem(p);
-  if (cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm))
-    return CTKV_ECUDA;
+  if (int rc = set_max_smem_k(kt, sm)) return rc;
   launch_k(kt, dim3(p.U), dim3(kTailT), sm, st, kPrioMid, p);
   return cudaGetLastError() == cudaSuccess ? CTKV_OK : CTKV_ECUDA;
 }

@@ -11,6 +11,7 @@ return the reference's host types (numpy, PerHead nested lists).
 from __future__ import annotations
 
 import hashlib
+import dataclasses
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -107,6 +108,9 @@ class DecodeState:
     oracle: object | None = None
     step: int = 0
     trace: list = field(default_factory=list)
+    # device step buffers and pinned host mirrors, reused across decode_step
+    # calls (rebuilt when the workspace size or the config changes)
+    _cache: tuple | None = field(default=None, repr=False, compare=False)
 
 
 # ---------------------------------------------------------------------------
@@ -323,6 +327,21 @@ def digest(ids_bg) -> str:
     return hsh.hexdigest()[:16]
 
 
+def digest_padded(pad: np.ndarray, lens: np.ndarray) -> str:
+    """digest() of the per-(b, g) prefixes pad[b, g, :lens[b, g]] without
+    building the per-head lists: one int64 conversion and one sha256 call
+    over the same byte stream (sha256 releases the GIL, so run_decode hashes
+    its steps on a thread pool)."""
+    p64 = pad.astype(np.int64, copy=False)
+    b, g = lens.shape
+    parts = []
+    for bi in range(b):
+        for gi in range(g):
+            parts.append(p64[bi, gi, :lens[bi, gi]].tobytes())
+            parts.append(b"|")
+    return hashlib.sha256(b"".join(parts)).hexdigest()[:16]
+
+
 # ---------------------------------------------------------------------------
 # fused step
 # ---------------------------------------------------------------------------
@@ -385,16 +404,15 @@ def trace_row(step: int, cfg: DecodeConfig, store: KvStore, index: QueryCentroid
     alpha = float((recall_len / denom).mean()) if denom else 0.0
     row = TraceRow(step=step, recall_len=total, alpha=alpha, rerank_len=0, sparse_digest="")
     if total > 0:
-        sp = _split_per_head(sparse_ids, sparse_len)
         n_sparse = int(sparse_len.sum())
         row.rerank_len = n_sparse
         if cfg.use_rerank:
             row.macs_rerank_qk = lay.group_size * lay.head_dim * total
         row.macs_sparse_qk = lay.group_size * lay.head_dim * n_sparse
         row.macs_sparse_wv = lay.group_size * lay.head_dim * n_sparse
-        row.sparse_digest = digest(sp)
+        row.sparse_digest = digest_padded(sparse_ids, sparse_len)
         if cfg.keep_sets:
-            row.sparse = sp
+            row.sparse = _split_per_head(sparse_ids, sparse_len)
     return row
 
 
@@ -403,11 +421,24 @@ def decode_step(state: DecodeState, query):
     store, index, cfg = state.store, state.index, state.config
     lay = store.layout
     q = _as_query(query, lay.batch, lay.query_heads, lay.head_dim, store.dtype)
-    bufs = StepBuffers.allocate(store, index, cfg)
+    ws_bytes = N.lib().ctkv_decode_workspace_bytes(store.ctkv_layout(), index.capacity, index.rho,
+                                                  cfg.c_prime, cfg.rho_prime)
+    key = (ws_bytes, dataclasses.astuple(cfg), index.capacity, index.rho, store.keys.device)
+    if state._cache is None or state._cache[0] != key:
+        bufs = StepBuffers.allocate(store, index, cfg)
+        host = tuple(torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                     for t in (bufs.flags, bufs.recall_len, bufs.sparse_ids, bufs.sparse_len))
+        state._cache = (key, bufs, host)
+    _, bufs, host = state._cache
+    bufs.flags.zero_()
     launch_step(store, index, cfg, q, bufs)
-    _flags_check(bufs.flags, "decode_step")
-    row = trace_row(state.step, cfg, store, index, bufs.recall_len.cpu().numpy().astype(np.int64),
-                    bufs.sparse_ids.cpu().numpy(), bufs.sparse_len.cpu().numpy())
+    # one device->host round trip for everything the trace row needs
+    for h_, d_ in zip(host, (bufs.flags, bufs.recall_len, bufs.sparse_ids, bufs.sparse_len)):
+        h_.copy_(d_, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    N.raise_flags(int(host[0].item()), "decode_step")
+    row = trace_row(state.step, cfg, store, index, host[1].numpy().astype(np.int64),
+                    host[2].numpy().copy(), host[3].numpy().copy())
     if state.oracle is not None and row.recall_len > 0:
         row.recall_at_k = state.oracle.recall_at_k(q, bufs.sparse_ids, bufs.sparse_len,
                                                    min(cfg.rho_prime, store.offloaded_ids().size))

@@ -75,3 +75,15 @@ def test_device_entry_points_fail_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         N.load_library(require_device=True)
+
+
+def test_padded_digest_equals_reference_digest():
+    """retrieval.digest_padded (one sha256 over the padded id array) equals
+    the per-head digest of ck/retrieval.py:295-301 that trace rows carry."""
+    import numpy as np
+    from paper_2512_15550_b200.retrieval import _split_per_head, digest, digest_padded
+    rng = np.random.default_rng(5)
+    pad = rng.integers(0, 1 << 20, size=(3, 4, 64), dtype=np.int32)
+    lens = rng.integers(0, 65, size=(3, 4)).astype(np.int32)
+    lens[0, 0] = 0
+    assert digest_padded(pad, lens) == digest(_split_per_head(pad, lens))
