@@ -486,6 +486,24 @@ __global__ void gather_sample_kernel(const uint4* __restrict__ keys, uint4* __re
 // such threshold is valid (the filter pass keeps every score at or above
 // it); a narrower bin only means fewer surplus candidates.
 constexpr int kKthWarps = 8, kKthBins = 1024;
+
+// f(key) for every 16-bit key of a row, the aligned middle with 16-byte
+// loads (8 keys each, several in flight per lane), head and tail scalar
+template <typename F>
+__device__ __forceinline__ void row_keys16(const uint16_t* r, int64_t n, int lane, F&& f) {
+  int64_t head = (int64_t)(((16u - (reinterpret_cast<uintptr_t>(r) & 15u)) & 15u) >> 1);
+  if (head > n) head = n;
+  if (lane < head) f((uint32_t)__ldg(r + lane));
+  const uint4* v = reinterpret_cast<const uint4*>(r + head);
+  const int64_t nv = (n - head) >> 3;
+#pragma unroll 2
+  for (int64_t i = lane; i < nv; i += 32) {
+    const uint4 w = __ldg(v + i);
+    f(w.x & 0xffffu); f(w.x >> 16); f(w.y & 0xffffu); f(w.y >> 16);
+    f(w.z & 0xffffu); f(w.z >> 16); f(w.w & 0xffffu); f(w.w >> 16);
+  }
+  for (int64_t i = head + nv * 8 + lane; i < n; i += 32) f((uint32_t)__ldg(r + i));
+}
 __global__ void __launch_bounds__(32 * kKthWarps) kth_value_kernel(const uint16_t* __restrict__ S,
                                                                   int64_t n, int64_t rows, int k,
                                                                   float* __restrict__ thr) {
@@ -496,18 +514,17 @@ __global__ void __launch_bounds__(32 * kKthWarps) kth_value_kernel(const uint16_
   int* hist = hist_all[warp];
   const uint16_t* r = S + row * n;
   uint32_t mn = 0xffffu, mx = 0u;
-  for (int64_t i = lane; i < n; i += 32) {
-    const uint32_t x = __ldg(r + i);
+  row_keys16(r, n, lane, [&](uint32_t x) {
     mn = min(mn, x);
     mx = max(mx, x);
-  }
+  });
   mn = __reduce_min_sync(0xffffffffu, mn);
   mx = __reduce_max_sync(0xffffffffu, mx);
   int sh = 0;
   while (((mx - mn) >> sh) >= (uint32_t)kKthBins) ++sh;
   for (int b = lane; b < kKthBins; b += 32) hist[b] = 0;
   __syncwarp();
-  for (int64_t i = lane; i < n; i += 32) atomicAdd(&hist[(__ldg(r + i) - mn) >> sh], 1);
+  row_keys16(r, n, lane, [&](uint32_t x) { atomicAdd(&hist[(x - mn) >> sh], 1); });
   __syncwarp();
   // lane L owns bins [kKthBins - 32(L+1), kKthBins - 32L): counts from the top
   constexpr int per = kKthBins / 32;
@@ -542,10 +559,10 @@ __global__ void __launch_bounds__(32 * kKthWarps) kth_value_kernel(const uint16_
     for (int b = lane; b < 64; b += 32) hist[b] = 0;
     __syncwarp();
     const uint32_t lo = key, wid = 1u << sh;
-    for (int64_t i = lane; i < n; i += 32) {
-      const uint32_t x = __ldg(r + i) - lo;
+    row_keys16(r, n, lane, [&](uint32_t x) {
+      x -= lo;
       if (x < wid) atomicAdd(&hist[x], 1);
-    }
+    });
     __syncwarp();
     // lane L owns sub-bins 2L, 2L+1 counted from the top (63 - 2L, 62 - 2L)
     const int b0 = 63 - 2 * lane, b1 = 62 - 2 * lane;
@@ -595,12 +612,20 @@ __global__ void __launch_bounds__(kSelT) select_kernel(const uint64_t* __restric
   uint32_t mn = 0xffffffffu, mx = 0u;
   for (int s = 0, at = 0; s < nsplit; ++s) {
     const int n_s = __ldg(counts + row * nsplit + s);
-    const uint64_t* src = cand + (row * nsplit + s) * cap;
-    for (int i = tid; i < n_s; i += kSelT) {
-      const uint64_t k = __ldg(src + i);
-      ck[at + i] = k;
-      mn = min(mn, (uint32_t)(k >> 32));
-      mx = max(mx, (uint32_t)(k >> 32));
+    // 16-byte loads (two candidates each, segments are 16-byte aligned),
+    // several in flight per thread
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(cand + (row * nsplit + s) * cap);
+#pragma unroll 4
+    for (int i = tid; 2 * i < n_s; i += kSelT) {
+      const ulonglong2 w = __ldg(src + i);
+      ck[at + 2 * i] = w.x;
+      mn = min(mn, (uint32_t)(w.x >> 32));
+      mx = max(mx, (uint32_t)(w.x >> 32));
+      if (2 * i + 1 < n_s) {
+        ck[at + 2 * i + 1] = w.y;
+        mn = min(mn, (uint32_t)(w.y >> 32));
+        mx = max(mx, (uint32_t)(w.y >> 32));
+      }
     }
     at += n_s;
   }
