@@ -102,11 +102,17 @@ lib.ctkv_debug_phase_timing(0, pb, n)
 a = np.frombuffer(pb, dtype=np.uint64).reshape(512, 16).astype(np.int64)[:eng.bl * g * 4]
 names = ["start", "q + slots", "lists+survivors", "sync2", "pull ids", "logits", "sync3",
          "pull keys", "threshold", "compaction", "attention", "sync4+merge"]
-print("  chain phases under load (last writer per CTA slot), median us:")
+print("  chain phases under load (last writer per CTA slot): median / p90 / max us")
 for kk in range(1, 12):
     rows = a[:, kk] > 0
     dd = (a[rows, kk] - a[rows, kk - 1]) / 1e3
     if kk == 11:
         dd = (a[0::4, 11] - a[0::4, 10]) / 1e3
-    print(f"    {names[kk]:18s} {np.median(dd):7.2f}")
+    print(f"    {names[kk]:18s} {np.median(dd):7.2f} {np.percentile(dd, 90):7.2f} {dd.max():7.2f}")
+tot = (a[0::4, 11] - a[0::4, 0]) / 1e3
+print(f"  chain CTA-0 start->merge end: median {np.median(tot):.2f} p90 {np.percentile(tot, 90):.2f} max {tot.max():.2f} us")
+# per cluster: the slowest rank's attention end vs the fastest's
+cl = a.reshape(-1, 4, 16)
+lag = (cl[:, :, 10].max(axis=1) - cl[:, :, 10].min(axis=1)) / 1e3
+print(f"  cluster imbalance at attention end (max - min rank): median {np.median(lag):.2f} p90 {np.percentile(lag, 90):.2f} us")
 lib.ctkv_debug_kernel_timeline(0)
