@@ -513,3 +513,65 @@ def test_bf16_capacity_above_4096_selects_every_slot():
     for t in range(T):
         assert trace[t].sparse_digest == recs[t].digest
         assert nrel(outs[:, :, t], ref_out[:, :, t]) < 1e-3
+
+
+# ---------------------------------------------------------------------------
+# GPU FlatOracle (the recall@k ground truth) vs ck/oracle.py:37-60
+# ---------------------------------------------------------------------------
+
+def _np_flat_topk(keys, q, lo, k, gs, d):
+    """ck/oracle.py:37-60 restated: per (b, g) the f64 GQA group max of the
+    scaled logits over keys[lo:], rounded to f32, top-k (score desc, id asc)."""
+    b, g = keys.shape[:2]
+    ids = np.arange(lo, keys.shape[2], dtype=np.int64)
+    out = np.empty((b, g, k), dtype=np.int64)
+    for bi in range(b):
+        for gi in range(g):
+            kk = keys[bi, gi, lo:].astype(np.float64)
+            qh = q[bi, gi * gs:(gi + 1) * gs].astype(np.float64)
+            grouped = ((qh @ kk.T) * (1.0 / np.sqrt(d))).max(axis=0).astype(np.float32)
+            out[bi, gi] = ids[np.lexsort((ids, -grouped.astype(np.float64)))[:k]]
+    return out
+
+
+@pytest.mark.parametrize("dtype,s", [(torch.float32, 8192), (torch.bfloat16, 8192),
+                                     (torch.bfloat16, 98304)])
+def test_flat_oracle_topk_and_recall_at_k_match_reference(dtype, s):
+    b, h, g, d, T, k = 1, 32, 8, 128, 4, 512
+    gs = h // g
+    lay = P.HeadLayout(b, h, g, s + T, d)
+    q, kk, vv, _ = P.generate(P.DriftConfig(seed=31, s=s, decode_steps=T), lay, dtype=dtype,
+                              q_rows=(s - 512, s + T))
+    store, index = P.prefill(q[:, :, :512].contiguous(), kk[:, :, :s].contiguous(),
+                             vv[:, :, :s].contiguous(), P.PrefillParams(128, 1024, 512, 1280),
+                             reserve=T, build_mode=0 if dtype == torch.float32 else 1)
+    fo = P.FlatOracle(store)
+    keys = store.keys[:, :, :s].float().cpu().numpy()
+    qt = q[:, :, 512].float().cpu().numpy()
+    off = store.offloaded_ids()
+    for scope, lo in (("all", 0), ("offloaded", int(off[0]))):
+        got = np.asarray(fo.topk(q[:, :, 512], k, scope)).reshape(b, g, k)
+        kv = keys[:, :, :int(off[-1]) + 1] if scope == "offloaded" else keys
+        ref = _np_flat_topk(kv, qt, lo, k, gs, d)
+        for gi in range(g):   # order equal; any difference must be an f64-summation-order tie
+            if np.array_equal(got[0, gi], ref[0, gi]):
+                continue
+            kk64 = kv[0, gi].astype(np.float64)
+            sc = ((qt[0, gi * gs:(gi + 1) * gs].astype(np.float64) @ kk64.T) / np.sqrt(d)).max(0)
+            kth = sc[ref[0, gi, -1]]
+            bad = [i for i in range(k) if got[0, gi, i] != ref[0, gi, i]]
+            assert all(abs(sc[got[0, gi, i]] - sc[ref[0, gi, i]]) <= TIE_REL * abs(kth) for i in bad), \
+                f"{scope}: FlatOracle.topk differs from ck/oracle.py beyond the tie window"
+    # recall@k in the trace = |sparse ∩ flat top-k over the offloaded keys| / k (ck/retrieval.py:360-370)
+    cfg = P.DecodeConfig(4, k, keep_sets=True)
+    outs, trace = P.run_decode(store, index, cfg, q[:, :, 512:512 + T], kk[:, :, s:s + T],
+                               vv[:, :, s:s + T], with_oracle=True)
+    for t, row in enumerate(trace):
+        keys_t = store.keys[:, :, :s + t + 1].float().cpu().numpy()
+        off_t = np.arange(128, s + t + 1 - 1024)
+        truth = _np_flat_topk(keys_t[:, :, :off_t[-1] + 1], q[:, :, 512 + t].float().cpu().numpy(),
+                              int(off_t[0]), k, gs, d)
+        hits = sum(np.intersect1d(row.sparse[bi][gi], truth[bi, gi]).size
+                   for bi in range(b) for gi in range(g))
+        assert row.recall_at_k == pytest.approx(hits / (b * g * k), abs=1e-12)
+        assert row.recall_at_k > 0.9, row.recall_at_k
