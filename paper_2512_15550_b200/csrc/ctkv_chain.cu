@@ -268,12 +268,23 @@ __device__ void chain_select(const uint32_t* key, int L, int R, int* hist, uint6
     uint32_t vb;
     int need;
     chain_boundary(key, L, R, hist, st, &vb, &need);
-    // the need-th equal key in position order
-    if (tid == 0) {
-      int c = 0, vp = -1;
-      for (int i = 0; i < L; ++i)
-        if (key[i] == vb && ++c == need) { vp = i; break; }
-      st[3] = vp;
+    // the need-th key equal to vb in position order: per-thread counts over
+    // contiguous chunks, an exclusive scan, then the owning thread walks its
+    // chunk (a single-thread walk over L cost up to ~25 us at large L)
+    const int pt = (L + (int)blockDim.x - 1) / (int)blockDim.x;
+    int c = 0;
+    for (int e = 0; e < pt; ++e) {
+      const int i = tid * pt + e;
+      c += (i < L && key[i] == vb) ? 1 : 0;
+    }
+    int tot;
+    const int before = block_exclusive_scan(c, &tot, reinterpret_cast<double*>(red));
+    if (before < need && before + c >= need) {
+      int cc = before;
+      for (int e = 0; e < pt; ++e) {
+        const int i = tid * pt + e;
+        if (i < L && key[i] == vb && ++cc == need) { st[3] = i; break; }
+      }
     }
     __syncthreads();
     *vk_out = vb;
