@@ -37,7 +37,7 @@ for li in range(NL):
     del q, k, v
 lib = N.lib()
 eng = DecodeEngine(built, P.DecodeConfig(4, 512), lanes=LANES)
-iid = len(sys.argv) > 3 and sys.argv[3] == "iid"   # iid Gaussian inputs (alpha ~0.75) instead of drift
+iid = "iid" in sys.argv[3:]   # iid Gaussian inputs (alpha ~0.75) instead of drift
 
 
 def load(t):
@@ -65,11 +65,25 @@ def hooked(layer, phase, stream=None):
         lib.ctkv_debug_phase_timing(0, None, 0)
 
 
-for t in range(3):
-    load(t)
-    eng._launch = hooked if t == 2 else orig
-    eng.step()
+graph = "graph" in sys.argv[3:]
+if graph:   # the debug bit is a kernel parameter: capture with it on for the target launch only
+    for t in range(2):
+        load(t)
+        eng.step()
     torch.cuda.synchronize()
+    eng._launch = hooked
+    eng.capture()
+    eng._launch = orig
+    for t in range(2, 6):
+        load(t)
+        eng.replay()
+        torch.cuda.synchronize()
+else:
+    for t in range(3):
+        load(t)
+        eng._launch = hooked if t == 2 else orig
+        eng.step()
+        torch.cuda.synchronize()
 n = 512 * 16
 buf = (ctypes.c_uint64 * n)()
 lib.ctkv_debug_phase_timing(-1, buf, n)
@@ -77,7 +91,7 @@ a = np.frombuffer(buf, dtype=np.uint64).reshape(512, 16).astype(np.int64)[:eng.b
 names = ["start", "q + slots", "lists+survivors", "sync2", "pull ids", "logits", "sync3",
          "pull keys", "threshold", "compaction", "attention", "sync4+merge"]
 t0 = a[:, 0].min()
-print(f"chain (lane {want_lane}, layer {want_layer}{', iid inputs' if iid else ''}) under load: {a.shape[0]} CTAs, "
+print(f"chain (lane {want_lane}, layer {want_layer}{', iid inputs' if iid else ''}{', graph replay' if graph else ', eager'}) under load: {a.shape[0]} CTAs, "
       f"start spread {(a[:, 0].max() - t0) / 1e3:.2f} us, span {(a[0::4, 11].max() - t0) / 1e3:.2f} us")
 for kk in range(1, 12):
     dd = (a[:, kk] - a[:, kk - 1]) / 1e3 if kk < 11 else (a[0::4, 11] - a[0::4, 10]) / 1e3
