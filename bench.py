@@ -61,7 +61,7 @@ PRESETS = {
                  workload="cfg2: Llama-3-8B geometry 32q/8kv d=128, 32 layers, 96K ctx, batch 8 "
                           "per GPU, bf16 (BASELINE configs[1])", model="llama3-8b-geometry"),
     "cfg3": dict(layers=48, batch=16, seq=98304, query_heads=32, kv_heads=4, capacity=2048,
-                 dtype="bf16", build_mode=1, lanes=4, phys_layers=36,
+                 dtype="bf16", build_mode=1, lanes=2, phys_layers=36,
                  workload="cfg3: Yi-9B geometry 32q/4kv d=128, 48 layers, 96K ctx, batch 16 per "
                           "GPU, bf16 (BASELINE configs[2]); 48 logical layers over 36 physical "
                           "layer buffers (capacity plan)", model="yi-9b-geometry"),

@@ -18,7 +18,9 @@ from paper_2512_15550_b200.store import KvStore  # noqa: E402
 
 NL = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 lanes = int(sys.argv[2]) if len(sys.argv) > 2 else 8
-b, h, g, d, s, C, T = 8, 32, 8, 128, 98304, 2048, 16
+b = int(sys.argv[3]) if len(sys.argv) > 3 else 8     # cfg3 geometry: 16 4
+g = int(sys.argv[4]) if len(sys.argv) > 4 else 8
+h, d, s, C, T = 32, 128, 98304, 2048, 16
 built, tails = [], []
 for li in range(NL):
     lay = P.HeadLayout(b, h, g, s + T, d)
@@ -99,7 +101,7 @@ for t in range(6):
 n = 512 * 16
 pb = (ctypes.c_uint64 * n)()
 lib.ctkv_debug_phase_timing(0, pb, n)
-a = np.frombuffer(pb, dtype=np.uint64).reshape(512, 16).astype(np.int64)[:eng.bl * g * 4]
+a = np.frombuffer(pb, dtype=np.uint64).reshape(512, 16).astype(np.int64)[:min(512, eng.bl * g * 4)]
 names = ["start", "q + slots", "lists+survivors", "sync2", "pull ids", "logits", "sync3",
          "pull keys", "threshold", "compaction", "attention", "sync4+merge"]
 print("  chain phases under load (last writer per CTA slot): median / p90 / max us")

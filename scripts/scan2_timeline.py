@@ -15,7 +15,11 @@ from paper_2512_15550_b200.engine import DecodeEngine  # noqa: E402
 from paper_2512_15550_b200.index import QueryCentroidIndex  # noqa: E402
 from paper_2512_15550_b200.store import KvStore  # noqa: E402
 
-b, h, g, d, s, C, T = 8, 32, 8, 128, 98304, 2048, 16
+b = int(sys.argv[1]) if len(sys.argv) > 1 else 8     # cfg3 geometry: 16 4
+g = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+h, d, s, C, T = 32, 128, 98304, 2048, 16
+CPU = C // (256 // (h // g))   # cosine chunks per unit
+NS = 9                         # static splits per unit (1152 tokens / 128)
 lay = P.HeadLayout(b, h, g, s + T, d)
 q, k, v, _ = P.generate(P.DriftConfig(seed=42, s=s, decode_steps=T), lay, dtype=torch.bfloat16,
                         q_rows=(s - C, s + T))
@@ -25,7 +29,7 @@ st.values[:, :, :s].copy_(v[:, :, :s])
 st._set_total(s)
 ix = QueryCentroidIndex.build(q[:, :, :C].contiguous(), st, C, 1280)
 lib = N.lib()
-for lanes in (8, 1):
+for lanes in (4, 1):
     eng = DecodeEngine([(st, ix)], P.DecodeConfig(4, 512), lanes=lanes)
     for t in range(3):
         eng.q[0].copy_(q[:, :, C + t])
@@ -39,7 +43,7 @@ for lanes in (8, 1):
             n = 4096 * 8
             buf = (ctypes.c_uint64 * n)()
             lib.ctkv_debug_scan_timeline(0, buf, n)
-            nct = eng.bl * g * (32 + 9)
+            nct = eng.bl * g * (CPU + NS)
             a = np.frombuffer(buf, dtype=np.uint64).reshape(4096, 8).astype(np.int64)[:nct]
             t0 = a[:, 0].min()
             r = (a - t0) / 1e3
@@ -47,7 +51,7 @@ for lanes in (8, 1):
             for nm, col in (("start", 0), ("rows landed", 1), ("compute done", 2), ("end", 3)):
                 x = r[:, col][a[:, col] > 0]
                 print(f"  {nm:13s} min {x.min():6.1f} median {np.median(x):6.1f} p90 {np.percentile(x, 90):6.1f} max {x.max():6.1f}")
-            ncos = eng.bl * g * 32
+            ncos = eng.bl * g * CPU
             lat = (a[:ncos, 1] - a[:ncos, 0]) / 1e3
             print(f"  cos CTA: start->rows median {np.median(lat):.1f} us; rows->done median {np.median((a[:ncos,2]-a[:ncos,1])/1e3):.1f}; done->end median {np.median((a[:ncos,3]-a[:ncos,2])/1e3):.1f}")
             stl = (a[ncos:, 2] - a[ncos:, 0]) / 1e3
@@ -61,7 +65,7 @@ for lanes in (8, 1):
                 print(f"    last cos CTA {i}: rows {r[i,1]:.1f} dots+gcos {r[i,4]:.1f} atomic {r[i,5]:.1f} fence {r[i,6]:.1f} select done {r[i,7]:.1f}")
             order = np.argsort(-a[:, 3])[:10]
             for i in order:
-                kind = f"cos u{i // 32} c{i % 32}" if i < ncos else f"static u{(i - ncos) // 9} s{(i - ncos) % 9}"
+                kind = f"cos u{i // CPU} c{i % CPU}" if i < ncos else f"static u{(i - ncos) // NS} s{(i - ncos) % NS}"
                 print(f"    slow CTA {i:4d} {kind:16s} start {r[i,0]:5.1f} rows {r[i,1]:5.1f} done {r[i,2]:5.1f} end {r[i,3]:5.1f}")
         else:
             eng.step()
