@@ -94,7 +94,7 @@ def parse():
     ap.add_argument("--local-len", type=int, default=1024)
     ap.add_argument("--no-rerank", action="store_true",
                     help="attend the whole recall set (ck/retrieval.py:334-337; Fig. 11 ablation)")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=30)
     ap.add_argument("--parity-steps", type=int, default=10,
                     help="steps replayed on the CPU per sampled unit (0: no parity leg)")
     ap.add_argument("--parity-units", type=int, default=3)
