@@ -198,7 +198,13 @@ int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctk
  * the kernel before a scan is the previous layer's chain (another layer's
  * state) and the kernel before a chain is the same layer's scan, which does
  * not write *total; k_new/v_new arrive from a copy stream through an event
- * (a full dependency). */
+ * (a full dependency).
+ * 32 (with any of the above): the caller chooses the chain kernel's cluster
+ * size -- 8 CTAs per (b, kv head) unit when 64 is also set, else 4.  Without
+ * 32 the library uses 8 when the call covers at most 16 units, else 4.  The
+ * cluster size changes the f32 summation grouping of the sparse attention
+ * (results agree to ~1e-8), so a caller that splits one batch over several
+ * calls (the lanes engine) passes the choice for the whole batch. */
 int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
                            const ctkv_step_args* A, int32_t phase, void* workspace,
                            size_t workspace_bytes, void* stream);

@@ -228,8 +228,12 @@ int ctkv_decode_step(const ctkv_layout* L, ctkv_store S, ctkv_index I, const ctk
 int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
                            const ctkv_step_args* A, int32_t phase, void* workspace,
                            size_t workspace_bytes, void* stream) {
-  if (phase < 1 || phase > 31) return CTKV_ECONFIG;
+  if (phase < 1 || phase > 127) return CTKV_ECONFIG;
   const PdlScope pdl_scope((phase & 16) != 0);   // 16: the caller allows programmatic dependent launch
+  // 32: the caller picks the chain's cluster size -- 8 CTAs per unit if 64
+  // is set, else 4 (a lanes engine decides from its whole batch, so a step's
+  // result does not depend on how the batch is split into lanes)
+  const int chain_cl = (phase & 32) ? ((phase & 64) ? 8 : 4) : 0;
   phase &= 15;
   if (phase < 1) return CTKV_ECONFIG;
   if (int rc = check_layout(L)) return rc;
@@ -289,6 +293,7 @@ int ctkv_decode_step_phase(const ctkv_layout* L, ctkv_store S, ctkv_index I,
   p.sparse_ids = A->sparse_ids;
   p.sparse_len = A->sparse_len;
   p.sparse_cap = A->sparse_ids ? A->sparse_cap : 0;
+  p.chain_cl = chain_cl;
   p.flags = A->flags;
   // bf16: 2-CTA cluster unit kernel (f32-chunked logits); f32: exact f64 unit kernel
   const bool v2 = L->dtype == CTKV_BF16 && L->head_dim >= 64 && p.gs <= 8 && I.rho <= 4096 &&

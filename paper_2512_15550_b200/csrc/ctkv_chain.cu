@@ -812,7 +812,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
 // launcher
 // ------------------------------------------------------------------------
 
-constexpr int kChainCL = 4;   // CTAs per unit (cluster size)
+// CTAs per unit (cluster size).  A step of few units (<= 16: small
+// batches, e.g. one GPU's slice of cfg5 at B <= 16) is latency-bound and
+// splits each unit's gathers and selection over 8 CTAs (+4-6 % at cfg5
+// B = 1..16); larger steps share the GPU between lanes and keep 4 (8 lost at
+// cfg5 B = 32 and at cfg2).  The lanes engine passes its whole-batch choice
+// (phase bits 32/64) so every lane of a step uses the same size.
+constexpr int kChainCL = 4, kChainCLSmall = 8, kChainSmallUnits = 16;
+static int chain_cl(const DecodeParams& p) {
+  if (p.chain_cl) return p.chain_cl;
+  return p.U <= kChainSmallUnits ? kChainCLSmall : kChainCL;
+}
 
 template <typename T, int D, int CL, int GS>
 static int launch_chain_t(const DecodeParams& p0, cudaStream_t st) {
@@ -838,9 +848,8 @@ int chain_phase_timing(int on, unsigned long long* out, int n) {
 bool chain_supported(const DecodeParams& p, int dtype, int D) {
   if (dtype != CTKV_BF16 || (D != 64 && D != 128)) return false;
   if ((p.gs != 1 && p.gs != 2 && p.gs != 4 && p.gs != 8) || p.c_prime > kCMaxLists) return false;
-  const int CL = kChainCL;
   if ((p.rho + kCT - 1) / kCT > kCMaxPer) return false;
-  return chain_layout(p, D, CL, nullptr, nullptr) <= 200 * 1024;
+  return chain_layout(p, D, chain_cl(p), nullptr, nullptr) <= 200 * 1024;
 }
 
 template <int D, int CL>
@@ -856,8 +865,9 @@ static int launch_chain_g(const DecodeParams& p, cudaStream_t st) {
 
 int launch_chain(const DecodeParams& p, int dtype, int D, cudaStream_t st) {
   if (dtype != CTKV_BF16) return CTKV_ECONFIG;
-  if (D == 128) return launch_chain_g<128, kChainCL>(p, st);
-  if (D == 64) return launch_chain_g<64, kChainCL>(p, st);
+  const bool small = chain_cl(p) == kChainCLSmall;
+  if (D == 128) return small ? launch_chain_g<128, kChainCLSmall>(p, st) : launch_chain_g<128, kChainCL>(p, st);
+  if (D == 64) return small ? launch_chain_g<64, kChainCLSmall>(p, st) : launch_chain_g<64, kChainCL>(p, st);
   return CTKV_ESHAPE;
 }
 

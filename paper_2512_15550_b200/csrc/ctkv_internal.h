@@ -70,6 +70,7 @@ struct DecodeParams {
   // v6 chain: the scan's last cosine CTA of a unit writes its top-C' slots
   int32_t* selg;    // [U][c'] top-C' slots (ties -> smaller slot)
   int* selctr;      // [U] cosine-chunk completion counters (reset by the last CTA)
+  int chain_cl;     // chain cluster size chosen by the caller (0: by this launch's units)
   int dbg;          // profiling builds only (-DCTKV_PROFILE): timestamp mark bits
                     // (1 scan2, 2 chain), a kernel parameter, so marks that are off
                     // cost no global load

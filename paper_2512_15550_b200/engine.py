@@ -66,6 +66,9 @@ class DecodeEngine:
             raise ValueError(f"lanes={lanes} must divide the batch {self.b}")
         self.nlanes = lanes
         self.bl = self.b // lanes
+        # chain cluster size from the whole batch (phase bits 32/64), the
+        # same for every lane (ctkv_decode_step_phase, include/ctkv.h)
+        self._cl_bits = 32 | (64 if self.b * self.g <= 16 else 0)
         self.dtype = st0.dtype
         dev = st0.keys.device
         nl = len(layers)
@@ -180,11 +183,11 @@ class DecodeEngine:
                 L = self.lane_layers[k][li]
                 ev = events[li * self.nlanes + k]
                 ev[0].record()
-                self._launch(L, 1)
+                self._launch(L, 1 | self._cl_bits)
                 ev[1].record()
-                self._launch(L, 2 | 8)
+                self._launch(L, 2 | 8 | self._cl_bits)
                 ev[2].record()
-                self._launch(L, 4)
+                self._launch(L, 4 | self._cl_bits)
                 if self.world > 1:
                     self._gather(k, li)
 
@@ -233,20 +236,20 @@ class DecodeEngine:
                 # previous layer's chain, before a chain this layer's scan).
                 # The previous layer's tail is released once this layer's scan
                 # is done, so it shares the GPU with this chain, not this scan.
-                self._launch(L, 1 | 16, ls)
+                self._launch(L, 1 | 16 | self._cl_bits, ls)
                 if li > 0:
                     es = self._evs[k][li]
                     es.record(ls)
                     ts.wait_event(self._ev[k][li - 1])
                     ts.wait_event(es)
-                    self._launch(self.lane_layers[k][li - 1], 4, ts)
+                    self._launch(self.lane_layers[k][li - 1], 4 | self._cl_bits, ts)
                     self._evt[k][li - 1].record(ts)
-                self._launch(L, 2 | 8 | 16, ls)
+                self._launch(L, 2 | 8 | 16 | self._cl_bits, ls)
                 ev = self._ev[k][li]
                 ev.record(ls)
                 if li == self.nl - 1:
                     ts.wait_event(ev)
-                    self._launch(L, 4, ts)
+                    self._launch(L, 4 | self._cl_bits, ts)
                     self._evt[k][li].record(ts)
                 if self._comm is not None:
                     self._comm.wait_event(ev)
