@@ -29,33 +29,34 @@ pytestmark = pytest.mark.gpu
 S, C, RHO, RP, CP, INIT, LOCAL = 98304, 2048, 1280, 512, 4, 128, 1024
 
 
-def _layers(b, h, g, nl, T):
-    lay = P.HeadLayout(b, h, g, S + T, 128)
+def _layers(b, h, g, nl, T, s=S):
+    lay = P.HeadLayout(b, h, g, s + T, 128)
     layers, inputs = [], []
     for li in range(nl):
-        q, k, v, _ = P.generate(P.DriftConfig(seed=42 + li, s=S, decode_steps=T), lay,
-                                dtype=torch.bfloat16, q_rows=(S - C, S + T))
-        st = KvStore(P.HeadLayout(b, h, g, S, 128), INIT, LOCAL, dtype=torch.bfloat16,
-                     capacity=S + T, host_api=False)
-        st.keys[:, :, :S].copy_(k[:, :, :S])
-        st.values[:, :, :S].copy_(v[:, :, :S])
-        st._set_total(S)
+        q, k, v, _ = P.generate(P.DriftConfig(seed=42 + li, s=s, decode_steps=T), lay,
+                                dtype=torch.bfloat16, q_rows=(s - C, s + T))
+        st = KvStore(P.HeadLayout(b, h, g, s, 128), INIT, LOCAL, dtype=torch.bfloat16,
+                     capacity=s + T, host_api=False)
+        st.keys[:, :, :s].copy_(k[:, :, :s])
+        st.values[:, :, :s].copy_(v[:, :, :s])
+        st._set_total(s)
         ix = QueryCentroidIndex.build(q[:, :, :C].contiguous(), st, C, RHO, mode=N.BUILD_FAST)
         layers.append((st, ix))
-        inputs.append((q[:, :, C:].contiguous(), k[:, :, S:].contiguous(), v[:, :, S:].contiguous()))
+        inputs.append((q[:, :, C:].contiguous(), k[:, :, s:].contiguous(), v[:, :, s:].contiguous()))
         del q, k, v
     return layers, inputs
 
 
-@pytest.mark.parametrize("b,h,g,units", [
-    (8, 32, 8, [(0, 0), (1, 7), (1, 3)]),        # cfg2 geometry (Llama-3-8B heads)
-    (16, 32, 4, [(0, 15), (1, 5)]),              # cfg3 geometry (Yi-9B heads, gs = 8)
+@pytest.mark.parametrize("b,h,g,units,s", [
+    (8, 32, 8, [(0, 0), (1, 7), (1, 3)], S),     # cfg2 geometry (Llama-3-8B heads)
+    (16, 32, 4, [(0, 15), (1, 5)], S),           # cfg3 geometry (Yi-9B heads, gs = 8)
+    (4, 4, 1, [(0, 0), (1, 3)], 131072),         # cfg5: one GPU's slice at 128K (8-CTA chains)
 ])
-def test_bench_path_matches_reference_at_96k(b, h, g, units):
+def test_bench_path_matches_reference_at_96k(b, h, g, units, s):
     torch.cuda.set_device(0)
     nl, warm, steps = 2, 4, 8
     T = warm + steps + 1
-    layers, inputs = _layers(b, h, g, nl, T)
+    layers, inputs = _layers(b, h, g, nl, T, s)
     eng = DecodeEngine(layers, P.DecodeConfig(CP, RP), lanes=4)
 
     def load(t):
