@@ -22,8 +22,8 @@ PARAMS = dict(init_len=32, local_len=256, capacity=256, rho=320)
 CP, RP = 4, 128
 
 
-def _inputs(li):
-    q, k, v = O.generate(O.Drift(seed=60 + li, s=S, decode_steps=T), B, H, G, D)
+def _inputs(li, b=B):
+    q, k, v = O.generate(O.Drift(seed=60 + li, s=S, decode_steps=T), b, H, G, D)
     return O.bf16_round(q), O.bf16_round(k), O.bf16_round(v)
 
 
@@ -33,13 +33,17 @@ def _prefill(q, k, v):
                      dtype=torch.bfloat16, reserve=T + 2, build_mode=0)
 
 
-@pytest.mark.parametrize("lanes,graph", [(1, False), (2, True), (4, True), (4, "host")])
-def test_engine_equals_per_layer_decode(lanes, graph):
+@pytest.mark.parametrize("lanes,graph,b", [(1, False, B), (2, True, B), (4, True, B), (4, "host", B),
+                                           (4, True, 12)])
+def test_engine_equals_per_layer_decode(lanes, graph, b):
     """graph="host": steps from t = 1 run through capture_host_io's two
     graph slots (q/k/v copied in from pinned host buffers per (layer, lane)
-    inside the step, outputs copied out as each layer finishes)."""
+    inside the step, outputs copied out as each layer finishes).  b = 12
+    (24 units, 6 per lane): the per-layer path takes 4-CTA chain clusters and
+    so must every lane, although a lane alone would qualify for 8 (the engine
+    passes the whole-batch choice, include/ctkv.h phase bits 32/64)."""
     torch.cuda.set_device(0)
-    data = [_inputs(li) for li in range(NL)]
+    data = [_inputs(li, b) for li in range(NL)]
     cfg = P.DecodeConfig(CP, RP)
     # per-layer drop-in path
     ref_out, ref_idx = [], []
@@ -54,7 +58,7 @@ def test_engine_equals_per_layer_decode(lanes, graph):
     built = [_prefill(q, k, v) for q, k, v in data]
     eng = DecodeEngine(built, cfg, lanes=lanes)
     dev = eng.q.device
-    got = np.zeros((NL, B, H, T, D), np.float32)
+    got = np.zeros((NL, b, H, T, D), np.float32)
     hbufs = None
     for t in range(T):
         if graph == "host" and t >= 1:
