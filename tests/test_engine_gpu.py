@@ -150,3 +150,23 @@ def test_engine_refuses_to_overrun_store_capacity():
     torch.cuda.synchronize()
     eng.check()
     assert st.total_tokens == S + 3 and int(st.total_dev.item()) == S + 3
+
+
+def test_stage_copy_moves_pinned_host_bytes_both_ways():
+    """ctkv_stage_copy (the engine's in-graph host I/O): host -> device and
+    device -> host through mapped pinned memory, byte-exact; misaligned or
+    non-16-byte sizes are refused (CTKV_ECONFIG)."""
+    from paper_2512_15550_b200 import _native as N
+    torch.cuda.set_device(0)
+    lib = N.lib()
+    src = torch.arange(4096 * 3, dtype=torch.int32).pin_memory()
+    dev = torch.empty(src.shape, dtype=torch.int32, device="cuda")
+    back = torch.zeros(src.shape, dtype=torch.int32).pin_memory()
+    st = torch.cuda.current_stream().cuda_stream
+    assert lib.ctkv_stage_copy(dev.data_ptr(), src.data_ptr(), src.nbytes, st) == N.OK
+    assert lib.ctkv_stage_copy(back.data_ptr(), dev.data_ptr(), dev.nbytes, st) == N.OK
+    torch.cuda.synchronize()
+    assert torch.equal(back, src) and torch.equal(dev.cpu(), src)
+    assert lib.ctkv_stage_copy(dev.data_ptr(), src.data_ptr(), 20, st) == N.ECONFIG
+    assert lib.ctkv_stage_copy(dev.data_ptr() + 4, src.data_ptr(), 32, st) == N.ECONFIG
+    assert lib.ctkv_stage_copy(dev.data_ptr(), src.data_ptr(), 0, st) == N.OK
