@@ -615,3 +615,27 @@ def test_multiturn_dcu_trace_matches_reference(use_dcu):
         assert row.sparse_digest == r["digest"], f"step {t}: sparse set differs"
         assert row.recall_len == r["recall_len"], f"step {t}: recall length differs"
         assert row.recall_at_k == pytest.approx(r["recall_at_k"], abs=1e-12), f"step {t}"
+
+
+def test_ac3_ac4_counters_and_index_size():
+    """SPEC acceptance criteria 3 and 4: the MAC counters of a real decode
+    step with and without rerank agree with acceleration_factor(L, R)
+    (ck/retrieval.py:287-292), and the index size formula gives 20,971,520
+    bytes at b=1, g=4, C=512, rho=2560 (footnote 5)."""
+    meta, p, flags, (q, k, v), store, index = _prefill("small_a")
+    s = meta["drift"]["s"]
+    qt = q[:, :, s]
+    macs = {}
+    lens = {}
+    for rr in (True, False):
+        st2, ix2 = _prefill("small_a")[4:]
+        _, row = P.decode_step(P.DecodeState(st2, ix2, P.DecodeConfig(4, 32, use_rerank=rr)), qt)
+        macs[rr] = row.macs_rerank_qk + row.macs_sparse_qk + row.macs_sparse_wv
+        lens[rr] = (row.recall_len, row.rerank_len)
+    L, R = lens[True]
+    assert L > R > 0 and lens[False][0] == L
+    assert macs[True] / macs[False] == pytest.approx(P.acceleration_factor(L, R), rel=0.05)
+    assert P.acceleration_factor(10000, 1000) == 0.6
+    ix_size = index.__class__.__new__(index.__class__)
+    ix_size.layout, ix_size.capacity, ix_size.rho = P.HeadLayout(1, 4, 4, 8, 8), 512, 2560
+    assert ix_size.size_bytes() == 20_971_520
