@@ -639,3 +639,21 @@ def test_ac3_ac4_counters_and_index_size():
     ix_size = index.__class__.__new__(index.__class__)
     ix_size.layout, ix_size.capacity, ix_size.rho = P.HeadLayout(1, 4, 4, 8, 8), 512, 2560
     assert ix_size.size_bytes() == 20_971_520
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_ac10_build_is_deterministic(tmp_path, mode):
+    """SPEC acceptance criterion 10: identical inputs give byte-identical
+    index files -- also for the tensor-core build, whose filter pass
+    collects candidates in whatever order the atomics land (the select
+    orders them by (score desc, id asc) before anything is written)."""
+    lay = P.HeadLayout(2, 32, 8, 8192, 128)
+    q, k, v, _ = P.generate(P.DriftConfig(seed=77, s=8192, decode_steps=0), lay, dtype=torch.bfloat16)
+    files = []
+    for rep in range(2):
+        store, index = P.prefill(q[:, :, -512:].contiguous(), k.contiguous(), v.contiguous(),
+                                 P.PrefillParams(128, 1024, 512, 1280), build_mode=mode)
+        path = tmp_path / f"idx{rep}.qivf"
+        index.save(path)
+        files.append(path.read_bytes())
+    assert files[0] == files[1]
