@@ -657,3 +657,30 @@ def test_ac10_build_is_deterministic(tmp_path, mode):
         index.save(path)
         files.append(path.read_bytes())
     assert files[0] == files[1]
+
+
+def test_store_appends_keep_the_partition_and_gathers_match():
+    """SPEC store invariants (ck/store.py:48-164): 100 sequential appends keep
+    the partition invariant after each and move ring tokens into the
+    offloaded range exactly like the reference store (restated in the
+    oracle); gather([]) is empty, a gather of a permutation of the offloaded
+    ids is that row permutation of the slice, out-of-range ids raise."""
+    rng = np.random.default_rng(9)
+    b, g, d, s = 2, 2, 32, 200
+    k = rng.standard_normal((b, g, s, d)).astype(np.float32)
+    v = rng.standard_normal((b, g, s, d)).astype(np.float32)
+    store = P.KvStore.partition(k, v, 8, 3, query_heads=4)
+    ost = O.partition(k, v, 8, 3, 4)
+    for t in range(100):
+        kn = rng.standard_normal((b, g, d)).astype(np.float32)
+        vn = rng.standard_normal((b, g, d)).astype(np.float32)
+        assert store.append(kn, vn) == ost.append(kn, vn) == s + t
+        store.check_partition()
+        np.testing.assert_array_equal(store.offloaded_ids(), ost.offloaded())
+        np.testing.assert_array_equal(store.static_ids(), ost.static())
+    assert store.gather(0, 0, []).shape[0] == 0
+    off = store.offloaded_ids()
+    perm = rng.permutation(off)
+    np.testing.assert_array_equal(np.asarray(store.gather(1, 1, perm)), ost.keys[1, 1, perm])
+    with pytest.raises(IndexError):
+        store.gather(0, 0, [s + 100])
