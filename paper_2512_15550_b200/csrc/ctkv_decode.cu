@@ -407,6 +407,7 @@ __device__ void cos_task(const DecodeParams& p, int task, unsigned char* smem, u
 }
 
 // attention partial over static tokens [i0, i0+ST) of the static index space
+// (f32, d < 64, or gs = 16; bf16 at d >= 64 and gs <= 8 takes static_task_tc)
 template <typename T, int D>
 __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t total,
                             unsigned char* smem, uint64_t* bar) {
@@ -476,83 +477,21 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
   s2mark(p, 1);
   const double scale = 1.0 / sqrt((double)D);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  __shared__ double wmax[kScanRowsV2 / 32][kMaxGroup];   // per-warp head maxima (tensor-core path)
-  bool mma_logits = false;
-  // (the m16n8 tile holds 8 heads: gs = 16 takes the SIMT logits below)
-  if constexpr (sizeof(T) == 2 && D >= 64) if (gs <= 8) {
-    // logits on the tensor cores: warp w takes tokens [16w, 16w+16) as the A
-    // operand of mma.m16n8k16 (f32 per 16-element k-step, f64 across), the
-    // gs heads as B columns; k permuted alike in K and q (as in the chain).
-    // The epilogue also reduces each warp's per-head maxima.
-    mma_logits = true;
-    const int g8 = lane >> 2, t4 = lane & 3;
-    double mloc[2] = {-INFINITY, -INFINITY};
-    for (int blk = warp; blk * 16 < nt; blk += nw) {
-      const int r0 = blk * 16 + g8, r1 = r0 + 8;
-      const T* ra = Ks + (size_t)r0 * D + 8 * t4;
-      const T* rb = ra + 8 * D;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int s2 = 0; s2 < D / 32; ++s2) {
-        const uint4 a = *reinterpret_cast<const uint4*>(ra + s2 * 32);
-        const uint4 b = *reinterpret_cast<const uint4*>(rb + s2 * 32);
-        const uint4 qv = g8 < gs ? *reinterpret_cast<const uint4*>(qs + g8 * D + s2 * 32 + 8 * t4)
-                                 : make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          float d0, d1, d2, d3;
-          asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-              "{%10,%10,%10,%10};"
-              : "=f"(d0), "=f"(d1), "=f"(d2), "=f"(d3)
-              : "r"(hf ? a.z : a.x), "r"(hf ? b.z : b.x), "r"(hf ? a.w : a.y), "r"(hf ? b.w : b.y),
-                "r"(hf ? qv.z : qv.x), "r"(hf ? qv.w : qv.y), "f"(0.f));
-          acc[0] += (double)d0;
-          acc[1] += (double)d1;
-          acc[2] += (double)d2;
-          acc[3] += (double)d3;
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int h = 2 * t4 + e;
-        if (h < gs) {
-          const double l0 = acc[e] * scale, l1 = acc[2 + e] * scale;
-          if (r0 < nt) { lg[h * ST + r0] = l0; mloc[e] = fmax(mloc[e], l0); }
-          if (r1 < nt) { lg[h * ST + r1] = l1; mloc[e] = fmax(mloc[e], l1); }
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 4; o < 32; o <<= 1) {
-      mloc[0] = fmax(mloc[0], __shfl_xor_sync(0xffffffffu, mloc[0], o));
-      mloc[1] = fmax(mloc[1], __shfl_xor_sync(0xffffffffu, mloc[1], o));
-    }
-    if (g8 == 0)
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        if (2 * t4 + e < gs) wmax[warp][2 * t4 + e] = mloc[e];
-  }
-  if (!mma_logits) {
-    // logits: pair (t, j), consecutive threads -> consecutive tokens
-    for (int pr = threadIdx.x; pr < nt * gs; pr += blockDim.x) {
-      const int t = pr % nt, j = pr / nt;
-      double dot, nrm;
-      row_dot<T, D, false>(qs + j * D, Ks + (size_t)t * D, t, dot, nrm);
-      lg[j * ST + t] = dot * scale;
-    }
+  // logits: pair (t, j), consecutive threads -> consecutive tokens
+  for (int pr = threadIdx.x; pr < nt * gs; pr += blockDim.x) {
+    const int t = pr % nt, j = pr / nt;
+    double dot, nrm;
+    row_dot<T, D, false>(qs + j * D, Ks + (size_t)t * D, t, dot, nrm);
+    lg[j * ST + t] = dot * scale;
   }
   __syncthreads();
   s2mark(p, 4);
   // per-head max / exp weights / denominators: one warp per head
   for (int j = warp; j < gs; j += nw) {
     double m = -INFINITY;
-    if (mma_logits) {
-      for (int w2 = 0; w2 * 16 < nt && w2 < nw; ++w2) m = fmax(m, wmax[w2][j]);
-    } else {
-      for (int t = lane; t < nt; t += 32) m = fmax(m, lg[j * ST + t]);
+    for (int t = lane; t < nt; t += 32) m = fmax(m, lg[j * ST + t]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     double l = 0.0;
     for (int t = lane; t < nt; t += 32) {
       const double e = sizeof(T) == 2 ? (double)expf((float)(lg[j * ST + t] - m)) : exp(lg[j * ST + t] - m);
@@ -617,6 +556,265 @@ __device__ void static_task(const DecodeParams& p, int task, int64_t t0, int64_t
   }
 }
 
+// bf16, d >= 64, gs <= 8: the static partition on the tensor cores, kept in
+// registers between its phases.  One 16-token block per warp (ST = 16 x 8
+// warps): logits by mma.m16n8k16 (f32 per 16-element k-step, f64 across, as
+// in static_task), the per-head maxima exchanged through shared memory, the
+// weights exp(l - m) computed by the lanes that hold the logits and split
+// into three bf16 terms hi + mid + lo (exactly the f32 weight), and P.V as
+// the GEMM O[gs x D] = W[gs x ST] V[ST x D] on the tensor cores (the bf16 V
+// rows are exact operands; products exact in f32, f32 accumulation).  V rows
+// land in groups of 16 tokens whose base moves 16 B per group, so an
+// ldmatrix.trans reading one row from each group (the MMA's k slots span
+// the groups) is conflict-free.  No logits or f32 weight arrays: the
+// partition needs 2 x ST x D x 2 B + 128 B of shared memory, which keeps
+// the scan at three CTAs per SM at gs = 8.
+constexpr int kStGroup = 16;                        // tokens per V row group
+template <int RB>
+__device__ __forceinline__ uint32_t vrow_off(int t) {
+  return (uint32_t)((t >> 4) * (kStGroup * RB + 16) + (t & 15) * RB);
+}
+constexpr int kWpStride = 128 + 8;                  // bf16 per weight row (bank shift)
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                               uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <typename T, int D>
+__device__ void static_task_tc(const DecodeParams& p, int task, int64_t t0, int64_t total,
+                               unsigned char* smem, uint64_t* bar) {
+  static_assert(sizeof(T) == 2 && D >= 64, "bf16, d >= 64");
+  constexpr int RB = D * int(sizeof(T));
+  constexpr int ST = static_tok<T>();
+  static_assert(ST == 16 * (kScanRowsV2 / 32), "one 16-token block per warp");
+  const int gs = p.gs;
+  const int u = task / p.ns, split = task % p.ns;
+  const int bi = u / p.g, gi = u % p.g;
+  const StaticSpan span(total, p.init_len, p.local_len);
+  const int64_t i0 = (int64_t)split * ST;
+  const int nt = (int)max((int64_t)0, min((int64_t)ST, span.n_static - i0));
+  T* Ks = reinterpret_cast<T*>(smem);                                      // [ST][D]
+  unsigned char* Vb = smem + (size_t)ST * RB;                              // grouped rows
+  T* qs = reinterpret_cast<T*>(Vb + (size_t)ST * RB + (ST / kStGroup) * 16);  // [gs][D]
+  __nv_bfloat16* Wp = reinterpret_cast<__nv_bfloat16*>(smem);   // [3][8][kWpStride], over Ks
+  // per-warp head maxima and partial denominators
+  double (*wmax)[8] = reinterpret_cast<double (*)[8]>(
+      (reinterpret_cast<uintptr_t>(qs + gs * D) + 15) & ~uintptr_t(15));   // [8 warps][8]
+  double (*wsum)[8] = wmax + kScanRowsV2 / 32;                              // [8 warps][8]
+  const int64_t slot = (int64_t)u * p.ns + split;
+  double* pm = p.pm + slot * gs;
+  double* pl = p.pl + slot * gs;
+  float* po = p.po + slot * gs * D;
+  if (nt == 0) {
+    for (int i = threadIdx.x; i < gs * D; i += blockDim.x) po[i] = 0.f;
+    if (threadIdx.x < gs) { pm[threadIdx.x] = -INFINITY; pl[threadIdx.x] = 0.0; }
+    return;
+  }
+  const T* keys = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
+  const T* vals = static_cast<const T*>(p.values) + (int64_t)u * p.cap * D;
+  const bool appending = p.k_new != nullptr;
+  uint64_t* barK = bar;
+  uint64_t* barV = bar + 1;
+  if (threadIdx.x == 0) {
+    bar_init(barK, 1);
+    bar_init(barV, 1);
+    bar_expect(barK, (uint32_t)(nt * RB));
+    bar_expect(barV, (uint32_t)(nt * RB));
+    // V rows [t, t + n) of the split from `src`, cut at the row groups
+    auto copy_v = [&](int t, const T* src, int n) {
+      while (n > 0) {
+        const int m = min(n, kStGroup - (t & (kStGroup - 1)));
+        bulk_g2s(Vb + vrow_off<RB>(t), src, (uint32_t)(m * RB), barV);
+        t += m;
+        src += (size_t)m * D;
+        n -= m;
+      }
+    };
+    // contiguous runs of ids: [i0, n_init) and the ring part
+    int64_t i = i0;
+    const int64_t i1 = i0 + nt;
+    while (i < i1) {
+      const int64_t id = span.id(i);
+      int64_t run_end = (i < span.n_init) ? min(i1, span.n_init) : i1;
+      int64_t n = run_end - i;
+      // the token appended by this step comes from the caller's buffer
+      const bool has_new = appending && id <= t0 && t0 < id + n;
+      if (has_new) n = t0 - id;  // rows before the new token
+      if (n > 0) {
+        bulk_g2s(Ks + (size_t)(i - i0) * D, keys + id * D, (uint32_t)(n * RB), barK);
+        copy_v((int)(i - i0), vals + id * D, (int)n);
+      }
+      if (has_new) {
+        const int64_t at = i + n - i0;
+        bulk_g2s(Ks + (size_t)at * D, static_cast<const T*>(p.k_new) + (int64_t)u * D, RB, barK);
+        copy_v((int)at, static_cast<const T*>(p.v_new) + (int64_t)u * D, 1);
+        n += 1;
+      }
+      i += n;
+    }
+  }
+  // V rows past the partition's tokens take part in the P.V MMAs with zero
+  // weights: make them finite zeros
+  for (int x = nt * (RB / 16) + threadIdx.x; x < ST * (RB / 16); x += blockDim.x)
+    *reinterpret_cast<uint4*>(Vb + vrow_off<RB>(x / (RB / 16)) + (x % (RB / 16)) * 16) = make_uint4(0, 0, 0, 0);
+  // K/V (and the appended token's rows, from the caller's k_new/v_new) are in
+  // flight; the query is read only after the wait (include/ctkv.h, phase bit 16)
+  pdl_wait();
+  const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
+  for (int k = threadIdx.x; k < gs * D; k += blockDim.x) qs[k] = q[k];
+  __syncthreads();
+  bar_wait(barK, 0);
+  s2mark(p, 1);
+  const double scale = 1.0 / sqrt((double)D);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  // ---- logits of tokens r0 = 16 warp + g8 and r1 = r0 + 8, heads 2 t4 + e
+  const int r0 = warp * 16 + g8, r1 = r0 + 8;
+  double lv[2][2];
+  {
+    const T* ra = Ks + (size_t)r0 * D + 8 * t4;
+    const T* rb = ra + 8 * D;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (warp * 16 < nt) {
+#pragma unroll
+      for (int s2 = 0; s2 < D / 32; ++s2) {
+        const uint4 a = *reinterpret_cast<const uint4*>(ra + s2 * 32);
+        const uint4 b = *reinterpret_cast<const uint4*>(rb + s2 * 32);
+        const uint4 qv = g8 < gs ? *reinterpret_cast<const uint4*>(qs + g8 * D + s2 * 32 + 8 * t4)
+                                 : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          float d[4] = {0.f, 0.f, 0.f, 0.f};
+          mma_bf16_16816(d, hf ? a.z : a.x, hf ? b.z : b.x, hf ? a.w : a.y, hf ? b.w : b.y,
+                         hf ? qv.z : qv.x, hf ? qv.w : qv.y);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[e] += (double)d[e];
+        }
+      }
+    }
+    double mloc[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const bool hv = 2 * t4 + e < gs;
+      lv[e][0] = (hv && r0 < nt) ? acc[e] * scale : -INFINITY;
+      lv[e][1] = (hv && r1 < nt) ? acc[2 + e] * scale : -INFINITY;
+      mloc[e] = fmax(lv[e][0], lv[e][1]);
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      mloc[0] = fmax(mloc[0], __shfl_xor_sync(0xffffffffu, mloc[0], o));
+      mloc[1] = fmax(mloc[1], __shfl_xor_sync(0xffffffffu, mloc[1], o));
+    }
+    if (g8 == 0) { wmax[warp][2 * t4] = mloc[0]; wmax[warp][2 * t4 + 1] = mloc[1]; }
+  }
+  __syncthreads();   // maxima exchanged; every warp is done with Ks
+  s2mark(p, 4);
+  // ---- weights: exp(l - m) as f32, split hi + mid + lo into Wp (over Ks),
+  // k slot of token t in k-step s = t%16 / 2: 8 (t%2) + t/16
+  {
+    double lsum[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int h = 2 * t4 + e;
+      double m = -INFINITY;
+      for (int w2 = 0; w2 < kScanRowsV2 / 32; ++w2) m = fmax(m, wmax[w2][h]);
+      lsum[e] = 0.0;
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) {
+        const int t = rr ? r1 : r0;
+        const float ef = lv[e][rr] == -INFINITY ? 0.f : expf((float)(lv[e][rr] - m));
+        lsum[e] += (double)ef;
+        const __nv_bfloat16 w0 = __float2bfloat16_rn(ef);
+        const float x1 = ef - __bfloat162float(w0);
+        const __nv_bfloat16 w1 = __float2bfloat16_rn(x1);
+        const __nv_bfloat16 w2 = __float2bfloat16_rn(x1 - __bfloat162float(w1));
+        if (h < 8) {
+          const int idx = ((t & 15) >> 1) * 16 + 8 * (t & 1) + (t >> 4);
+          Wp[(0 * 8 + h) * kWpStride + idx] = w0;
+          Wp[(1 * 8 + h) * kWpStride + idx] = w1;
+          Wp[(2 * 8 + h) * kWpStride + idx] = w2;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      lsum[0] += __shfl_xor_sync(0xffffffffu, lsum[0], o);
+      lsum[1] += __shfl_xor_sync(0xffffffffu, lsum[1], o);
+    }
+    if (g8 == 0) { wsum[warp][2 * t4] = lsum[0]; wsum[warp][2 * t4 + 1] = lsum[1]; }
+  }
+  __syncthreads();   // Wp and the partial denominators complete
+  s2mark(p, 5);
+  if (threadIdx.x < gs) {
+    double m = -INFINITY, l = 0.0;
+    for (int w2 = 0; w2 < kScanRowsV2 / 32; ++w2) {
+      m = fmax(m, wmax[w2][threadIdx.x]);
+      l += wsum[w2][threadIdx.x];
+    }
+    pm[threadIdx.x] = m;
+    pl[threadIdx.x] = l;
+  }
+  bar_wait(barV, 0);
+  s2mark(p, 6);
+  // ---- P.V: warp w owns output columns [w D/8, (w+1) D/8) = D/64 n-tiles
+  constexpr int NTW = D / 64;                 // n-tiles of 8 columns per warp
+  float c[NTW][4];
+#pragma unroll
+  for (int j = 0; j < NTW; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.f;
+  const int n0 = warp * (D / 8);
+  const bool arow = g8 < gs;
+  const uint32_t wbase = sa(Wp) + (uint32_t)(g8 * kWpStride + 2 * t4) * 2u;
+  const int mat = lane >> 3, li = lane & 7;
+#pragma unroll 1
+  for (int s = 0; s < ST / 16; ++s) {
+    uint32_t a[3][2];
+#pragma unroll
+    for (int tm = 0; tm < 3; ++tm) {
+      const uint32_t ad = wbase + (uint32_t)(tm * 8 * kWpStride + s * 16) * 2u;
+      a[tm][0] = arow ? ld_shared_u32(ad) : 0u;
+      a[tm][1] = arow ? ld_shared_u32(ad + 16u) : 0u;
+    }
+    // row li of matrix `mat`: token 16 li + 2 s + (mat & 1), columns
+    // n0 + 8 (mat >> 1) (+16 per further pair)
+    const uint32_t vrow = sa(Vb) + vrow_off<RB>(16 * li + 2 * s + (mat & 1));
+    if constexpr (NTW == 1) {
+      uint32_t b0, b1;
+      asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+                   : "=r"(b0), "=r"(b1)
+                   : "r"(vrow + (uint32_t)n0 * 2u));
+#pragma unroll
+      for (int tm = 0; tm < 3; ++tm) mma_bf16_16816(c[0], a[tm][0], 0u, a[tm][1], 0u, b0, b1);
+    } else {
+#pragma unroll
+      for (int jp = 0; jp < NTW / 2; ++jp) {
+        uint32_t b[4];
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+                     : "r"(vrow + (uint32_t)(n0 + 16 * jp + 8 * (mat >> 1)) * 2u));
+#pragma unroll
+        for (int tm = 0; tm < 3; ++tm) {
+          mma_bf16_16816(c[2 * jp], a[tm][0], 0u, a[tm][1], 0u, b[0], b[1]);
+          mma_bf16_16816(c[2 * jp + 1], a[tm][0], 0u, a[tm][1], 0u, b[2], b[3]);
+        }
+      }
+    }
+  }
+  if (arow)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j)
+      *reinterpret_cast<float2*>(po + g8 * D + n0 + 8 * j + 2 * t4) = make_float2(c[j][0], c[j][1]);
+}
+
 template <typename T, int D>
 __global__ void __launch_bounds__(kScanRowsV2, 4) scan2_kernel(DecodeParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -631,7 +829,15 @@ __global__ void __launch_bounds__(kScanRowsV2, 4) scan2_kernel(DecodeParams p) {
     cos_task<T, D>(p, blockIdx.x, smem, bars);
   } else {
     const int64_t t0 = p.total ? *p.total : p.id_bound;
-    static_task<T, D>(p, blockIdx.x - ncos, t0, t0 + (appending ? 1 : 0), smem, bars);
+    if constexpr (sizeof(T) == 2 && D >= 64) {
+      if (p.gs <= 8) {
+        static_task_tc<T, D>(p, blockIdx.x - ncos, t0, t0 + (appending ? 1 : 0), smem, bars);
+      } else {
+        static_task<T, D>(p, blockIdx.x - ncos, t0, t0 + (appending ? 1 : 0), smem, bars);
+      }
+    } else {
+      static_task<T, D>(p, blockIdx.x - ncos, t0, t0 + (appending ? 1 : 0), smem, bars);
+    }
   }
   s2mark(p, 2);
   if (appending && blockIdx.x == 0) {
@@ -664,10 +870,15 @@ template <typename T, int D>
 size_t scan2_smem(int gs) {
   constexpr int RB = D * int(sizeof(T));
   constexpr int ST = static_tok<T>();
-  const size_t cosb = (size_t)kScanRowsV2 * RB + sizeof(float) * gs * D + sizeof(double) * gs +
+  const size_t cosb = (size_t)kScanRowsV2 * RB + sizeof(T) * gs * D + sizeof(double) * gs +
                       sizeof(double) * 2 * kScanRowsV2 + sizeof(float) * kScanRowsV2 + 16;
-  const size_t stb = (size_t)2 * ST * RB + sizeof(float) * gs * D + sizeof(double) * gs * ST +
-                     sizeof(float) * gs * ST + sizeof(double) * 2 * gs;
+  // static partitions: static_task_tc (bf16, d >= 64, gs <= 8) keeps logits
+  // and weights in registers / over the K rows; static_task stages them
+  const bool tc = sizeof(T) == 2 && D >= 64 && gs <= 8;
+  const size_t stb = tc ? (size_t)2 * ST * RB + (ST / kStGroup) * 16 + sizeof(T) * gs * D + 16 +
+                             2 * sizeof(double) * (kScanRowsV2 / 32) * 8
+                        : (size_t)2 * ST * RB + sizeof(float) * gs * D + sizeof(double) * gs * ST +
+                              sizeof(float) * gs * ST + sizeof(double) * 2 * gs;
   return cosb > stb ? cosb : stb;
 }
 
