@@ -102,6 +102,7 @@ constexpr int kCMaxPer = 32;     // list entries per thread (keep mask bits)
 constexpr int kVUn = 8;          // V-row passes in flight per warp (2 rows each)
 constexpr int kCBins = 1024;     // top-rho' selection: histogram bins
 constexpr int kCBnd = 256;       // ... and keys ranked exactly in the boundary bin
+constexpr int kRedHeads = 4;     // heads per pass of the cross-warp V-sum reduction
 
 struct ChainSmem {
   uint32_t* bm;          // [words] OR of the lists before an owned one } area A; CTA 0
@@ -139,7 +140,9 @@ __host__ __device__ inline size_t chain_layout(const DecodeParams& p, int D, int
   const size_t a_lists = bm_b + align16((size_t)nlo * p.rho * 4);
   const size_t spo_b = align16((size_t)p.ns * p.gs * D * 4);
   const size_t a_static = spo_b + align16((size_t)2 * p.ns * p.gs * 8);
-  const size_t keys_b = (size_t)lmax * 4, red_b = (size_t)kCW * p.gs * D * 4;
+  // per-warp V sums of at most kRedHeads heads at a time (gs = 8 reduces in
+  // two passes, so the chain stays at two CTAs per SM)
+  const size_t keys_b = (size_t)lmax * 4, red_b = (size_t)kCW * min(p.gs, kRedHeads) * D * 4;
   ChainSmem t;
   unsigned char* a = take(a_lists > a_static ? a_lists : a_static);
   t.bm = reinterpret_cast<uint32_t*>(a);
@@ -684,22 +687,27 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     for (int e = 0; e < 8; ++e)
 #pragma unroll
       for (int o = VL; o < 32; o <<= 1) acc[hh][e] += __shfl_xor_sync(0xffffffffu, acc[hh][e], o);
-  __syncthreads();
-  if (vrw == 0)
-#pragma unroll
-    for (int hh = 0; hh < GS; ++hh)
-      if (hh < gs) {
-        float4* dst = reinterpret_cast<float4*>(S.red + ((size_t)warp * gs + hh) * D + 8 * vsub);
-        dst[0] = make_float4(acc[hh][0], acc[hh][1], acc[hh][2], acc[hh][3]);
-        dst[1] = make_float4(acc[hh][4], acc[hh][5], acc[hh][6], acc[hh][7]);
-      }
-  __syncthreads();
   float* cpo0 = cl.map_shared_rank(S.cpo, 0);
   double* cpml0 = cl.map_shared_rank(S.cpml, 0);
-  for (int i = tid; i < gs * D; i += kCT) {
-    float s = 0.f;
-    for (int w = 0; w < kCW; ++w) s += S.red[(size_t)w * gs * D + i];
-    cpo0[(size_t)r * gs * D + i] = s;
+  constexpr int RH = GS < kRedHeads ? GS : kRedHeads;   // heads per reduction pass
+#pragma unroll
+  for (int h0 = 0; h0 < GS; h0 += RH) {
+    __syncthreads();   // (previous pass's) sums consumed
+    if (vrw == 0)
+#pragma unroll
+      for (int hh = h0; hh < h0 + RH; ++hh)
+        if (hh < gs) {
+          float4* dst = reinterpret_cast<float4*>(S.red + ((size_t)warp * RH + (hh - h0)) * D + 8 * vsub);
+          dst[0] = make_float4(acc[hh][0], acc[hh][1], acc[hh][2], acc[hh][3]);
+          dst[1] = make_float4(acc[hh][4], acc[hh][5], acc[hh][6], acc[hh][7]);
+        }
+    __syncthreads();
+    const int nh = min(RH, gs - h0);
+    for (int i = tid; i < nh * D; i += kCT) {
+      float s = 0.f;
+      for (int w = 0; w < kCW; ++w) s += S.red[(size_t)w * RH * D + i];
+      cpo0[(size_t)r * gs * D + (size_t)h0 * D + i] = s;
+    }
   }
   if (tid < gs) {
     cpml0[r * gs + tid] = nmy > 0 ? hm[tid] : -INFINITY;

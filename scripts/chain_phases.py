@@ -1,5 +1,5 @@
 """Phase breakdown of the v6 chain kernel (4-CTA cluster per unit) on a
-cfg2-sized layer: one eager step with device phase timestamps on, printed
+cfg2-sized layer (or B x G units: chain_phases.py LANES B G): one eager step with device phase timestamps on, printed
 as per-phase medians over the units' CTAs."""
 import ctypes
 import os
@@ -17,7 +17,9 @@ from paper_2512_15550_b200.index import QueryCentroidIndex  # noqa: E402
 from paper_2512_15550_b200.store import KvStore  # noqa: E402
 
 lanes = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-b, h, g, d, s, C, T = 8, 32, 8, 128, 98304, 2048, 16
+b = int(sys.argv[2]) if len(sys.argv) > 2 else 8     # cfg3 geometry: LANES 16 4
+g = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+h, d, s, C, T = 32, 128, 98304, 2048, 16
 lay = P.HeadLayout(b, h, g, s + T, d)
 q, k, v, _ = P.generate(P.DriftConfig(seed=42, s=s, decode_steps=T), lay, dtype=torch.bfloat16,
                         q_rows=(s - C, s + T))
