@@ -461,8 +461,22 @@ def test_96k_tensor_core_build_matches_exact_within_tie_window():
     (32, 2, 128, 64, 64, 4, 32),    # gs = 16: unit2 (the chain takes gs <= 8)
 ])
 def test_bf16_fused_decode_geometries(h, g, d, C, rho, cp, rp):
-    rng = np.random.default_rng(1000 * h + 10 * d + C + rho + cp)
-    b, s, T, init, local = 2, 1024, 3, 16, 64
+    _bf16_decode_vs_oracle(h, g, d, C, rho, cp, rp, init=16, local=64, T=3)
+
+
+@pytest.mark.parametrize("h,g,d", [(32, 8, 128), (32, 4, 128), (16, 8, 64), (8, 8, 128)])
+def test_bf16_static_partitions_ragged(h, g, d):
+    """The tensor-core static partitions (scan2 static_task_tc) over a static
+    window of 40 + 300 tokens: two full 128-token partitions and a ragged one
+    (84 tokens: zero V rows and weights past the end), the appended token
+    walking across 16-token row groups for 20 steps while the ring advances;
+    gs = 4 / 8 / 2 / 1, d = 128 and 64."""
+    _bf16_decode_vs_oracle(h, g, d, 64, 64, 4, 48, init=40, local=300, T=20)
+
+
+def _bf16_decode_vs_oracle(h, g, d, C, rho, cp, rp, init, local, T):
+    rng = np.random.default_rng(1000 * h + 10 * d + C + rho + cp + init)
+    b, s = 2, 1024
     q = O.bf16_round(rng.standard_normal((b, h, s + T, d)).astype(np.float32))
     k = O.bf16_round(rng.standard_normal((b, g, s + T, d)).astype(np.float32))
     v = O.bf16_round(rng.standard_normal((b, g, s + T, d)).astype(np.float32))
