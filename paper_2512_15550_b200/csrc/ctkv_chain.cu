@@ -340,7 +340,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   ktl_mark(p.tl, 3, true);   // the last CTA start (slot 3 end = max start)
   pdl_wait();      // the scan's outputs (gcos / slots, static partials) are complete
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int i = tid; i < gs * D; i += kCT) qs[i] = q[i];
+  for (int i = tid; i < gs * D / 8; i += kCT)   // 16-byte pieces (q is 16-byte aligned: the scan bulk-copies it)
+    reinterpret_cast<uint4*>(qs)[i] = __ldg(reinterpret_cast<const uint4*>(q) + i);
   if (tid < p.c_prime) sel[tid] = __ldcg(p.selg + (int64_t)u * p.c_prime + tid);
   __syncthreads();
   cmark(p, 1);

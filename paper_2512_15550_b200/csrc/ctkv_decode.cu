@@ -671,7 +671,8 @@ __device__ void static_task_tc(const DecodeParams& p, int task, int64_t t0, int6
   // flight; the query is read only after the wait (include/ctkv.h, phase bit 16)
   pdl_wait();
   const T* q = static_cast<const T*>(p.q) + ((int64_t)bi * p.h + (int64_t)gi * gs) * D;
-  for (int k = threadIdx.x; k < gs * D; k += blockDim.x) qs[k] = q[k];
+  for (int k = threadIdx.x; k < gs * D / 8; k += blockDim.x)   // 16-byte pieces
+    reinterpret_cast<uint4*>(qs)[k] = __ldg(reinterpret_cast<const uint4*>(q) + k);
   __syncthreads();
   bar_wait(barK, 0);
   s2mark(p, 1);
