@@ -847,10 +847,19 @@ __global__ void __launch_bounds__(kScanRowsV2, 4) scan2_kernel(DecodeParams p) {
     T* vals = static_cast<T*>(const_cast<void*>(p.values));
     const T* kn = static_cast<const T*>(p.k_new);
     const T* vn = static_cast<const T*>(p.v_new);
-    for (int64_t i = threadIdx.x; i < (int64_t)p.U * D; i += blockDim.x) {
-      const int64_t uu = i / D, e = i % D;
-      keys[(uu * p.cap + t0) * D + e] = kn[i];
-      vals[(uu * p.cap + t0) * D + e] = vn[i];
+    if constexpr (D * sizeof(T) % 16 == 0) {   // 16-byte pieces of each unit's new row
+      constexpr int VPR = D * int(sizeof(T)) / 16;
+      for (int64_t i = threadIdx.x; i < (int64_t)p.U * VPR; i += blockDim.x) {
+        const int64_t uu = i / VPR, e = i % VPR;
+        reinterpret_cast<uint4*>(keys + (uu * p.cap + t0) * D)[e] = reinterpret_cast<const uint4*>(kn)[i];
+        reinterpret_cast<uint4*>(vals + (uu * p.cap + t0) * D)[e] = reinterpret_cast<const uint4*>(vn)[i];
+      }
+    } else {
+      for (int64_t i = threadIdx.x; i < (int64_t)p.U * D; i += blockDim.x) {
+        const int64_t uu = i / D, e = i % D;
+        keys[(uu * p.cap + t0) * D + e] = kn[i];
+        vals[(uu * p.cap + t0) * D + e] = vn[i];
+      }
     }
   }
   __syncthreads();

@@ -114,9 +114,11 @@ __global__ void __launch_bounds__(kTailT) tail_kernel(DecodeParams p) {
     const int keep = min(p.rho, L);
     for (int i = tid; i < p.rho; i += kTailT) row[i] = i < keep ? rec[pos_at(i)] : kEmpty;
     T* cent = static_cast<T*>(p.cent);
-    for (int i = tid; i < gs * D; i += kTailT) {
-      const int hh = i / D, e = i % D;
-      cent[(((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D + e] = q[i];
+    constexpr int VPR = D * int(sizeof(T)) / 16;   // 16-byte pieces per row
+    for (int i = tid; i < gs * VPR; i += kTailT) {
+      const int hh = i / VPR, e = i % VPR;
+      reinterpret_cast<uint4*>(cent + (((int64_t)bi * p.h + gi * gs + hh) * p.C + slot) * D)[e] =
+          reinterpret_cast<const uint4*>(q)[i];
     }
     write_slot_norms<T, D>(p, q, bi, gi, slot);
   }
