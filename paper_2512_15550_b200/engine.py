@@ -256,11 +256,14 @@ class DecodeEngine:
                     with torch.cuda.stream(self._comm):
                         self._gather(k, li)
                     self._gev[k][li].record(self._comm)
-                if hio is not None and self._comm is None:
-                    # a finished (layer, lane) output leaves while later layers run
-                    self._cout.wait_event(ev)
-                    b0, b1 = k * self.bl, (k + 1) * self.bl
-                    self._stage(hio[3][li, b0:b1], self.out[li, b0:b1], self._cout)
+            if hio is not None and self._comm is None and ((li + 1) % self._cout_chunk == 0
+                                                            or li == self.nl - 1):
+                # every _cout_chunk layers' outputs leave in one copy once all
+                # lanes have finished them, while later layers run
+                c0 = li - (li % self._cout_chunk)
+                for k in range(self.nlanes):
+                    self._cout.wait_event(self._ev[k][li])
+                self._stage(hio[3][c0:li + 1], self.out[c0:li + 1], self._cout)
             if hio is not None and self._comm is not None:
                 self._cout.wait_event(self._gev[self.nlanes - 1][li])   # all lanes gathered
                 self._stage(hio[3][li], self.gathered[li], self._cout)
@@ -338,6 +341,7 @@ class DecodeEngine:
         self._cout = torch.cuda.Stream(device=dev)
         self._cin_ev = [[torch.cuda.Event() for _ in range(self.nl)] for _ in range(self.nlanes)]
         self._cin_chunk = 4   # layers per input copy
+        self._cout_chunk = 4  # layers per output copy
         bufs, graphs = [], []
         torch.cuda.synchronize()
         for _ in range(slots):
