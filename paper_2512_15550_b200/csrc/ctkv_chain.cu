@@ -225,23 +225,11 @@ __device__ void chain_boundary(const uint32_t* key, int L, int R, int* hist, int
 // pass over [min, max] of the keys (1024 linear bins), then an exact rank
 // of the few keys in the boundary bin; degenerate distributions (more than
 // kCBnd keys in that bin) fall back to the 8-bit radix passes.
-__device__ void chain_select(const uint32_t* key, int L, int R, int* hist, uint64_t* bnd, int* st,
-                             uint32_t* red, uint32_t* vk_out, int* vpos_out) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  uint32_t mn = 0xffffffffu, mx = 0u;
-  for (int i = tid; i < L; i += blockDim.x) {
-    const uint32_t k = key[i];
-    mn = min(mn, k);
-    mx = max(mx, k);
-  }
-  mn = __reduce_min_sync(0xffffffffu, mn);
-  mx = __reduce_max_sync(0xffffffffu, mx);
-  for (int b = tid; b < kCBins; b += blockDim.x) hist[b] = 0;
-  if (lane == 0) { red[warp] = mn; red[32 + warp] = mx; }
-  __syncthreads();
-  mn = 0xffffffffu;
-  mx = 0u;
-  for (int w = 0; w < nw; ++w) { mn = min(mn, red[w]); mx = max(mx, red[32 + w]); }
+// `mn`/`mx` are the keys' min and max and `hist` is zeroed (the chain
+// gathers both while the keys are produced).
+__device__ void chain_select(const uint32_t* key, int L, int R, uint32_t mn, uint32_t mx, int* hist,
+                             uint64_t* bnd, int* st, uint32_t* red, uint32_t* vk_out, int* vpos_out) {
+  const int tid = threadIdx.x;
   if (mn == mx) {   // all scores equal: the first R positions
     *vk_out = mn;
     *vpos_out = R - 1;
@@ -331,6 +319,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   __shared__ int lcnt[kCMaxLists];
   __shared__ int sbase[kCMaxLists + 1];
   __shared__ int s_state[4];
+  __shared__ uint32_t s_kmm[2];   // min / max of all L score keys (every cluster CTA)
   __shared__ double hm[GS], hl[GS], hnew[GS], hresc[GS];
 
   cmark(p, 0);
@@ -407,6 +396,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     if (tid < CL) cl.map_shared_rank(lcnt, tid)[j] = tot;
   }
   cmark(p, 2);
+  if (tid == 0) { s_kmm[0] = 0xffffffffu; s_kmm[1] = 0u; }   // key min / max (filled remotely below)
+  for (int b = tid; b < kCBins; b += kCT) S.hist[b] = 0;
   cl.sync();   // #2: survivor counts everywhere, survivors compacted
   cmark(p, 3);
 
@@ -456,6 +447,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     constexpr int R1 = kCW * NB * 16;
     for (int i = tid; i < 2 * (n_sl - R1); i += kCT)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(keys_g + (int64_t)S.sid[R1 + (i >> 1)] * D + (i & 1) * (D / 2)));
+    uint32_t kmn = 0xffffffffu, kmx = 0u;   // this thread's key range
     for (int bk0 = warp * NB; bk0 * 16 < n_sl; bk0 += kCW * NB) {
       uint4 ra[NB][KS2], rb[NB][KS2];
 #pragma unroll
@@ -518,6 +510,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
           const float gm = t4 == 0 ? m0 : m1;
           if (rr < n_sl) {
             const uint32_t k32 = ~okey32(gm);
+            kmn = min(kmn, k32);
+            kmx = max(kmx, k32);
             S.keys[lo + rr] = k32;
 #pragma unroll
             for (int o = 0; o < CL - 1; ++o) st_cluster_u32(rkeys[o] + 4u * (uint32_t)(lo + rr), k32);
@@ -527,6 +521,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
       }
       if (bk0 == warp * NB) cmark(p, 14);
     }
+    // the slice's key range into every cluster CTA (the top-rho' histogram
+    // needs the min / max of all L keys; barrier #3 publishes them)
+    kmn = __reduce_min_sync(0xffffffffu, kmn);
+    kmx = __reduce_max_sync(0xffffffffu, kmx);
+    if (lane == 0 && kmn <= kmx)
+#pragma unroll
+      for (int o = 0; o < CL; ++o) {
+        uint32_t* rm = cl.map_shared_rank(s_kmm, o);
+        atomicMin(rm, kmn);
+        atomicMax(rm + 1, kmx);
+      }
   }
   cmark(p, 5);
   cl.sync();   // #3: every slice's keys are complete (and its logits/ids in L2)
@@ -549,8 +554,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
   uint32_t vk = 0xffffffffu;
   int vpos = L;
   if (Rn > 0 && Rn < L)
-    chain_select(S.keys, L, Rn, S.hist, reinterpret_cast<uint64_t*>(S.spos), s_state,
-                 reinterpret_cast<uint32_t*>(S.scratch), &vk, &vpos);
+    chain_select(S.keys, L, Rn, s_kmm[0], s_kmm[1], S.hist, reinterpret_cast<uint64_t*>(S.spos),
+                 s_state, reinterpret_cast<uint32_t*>(S.scratch), &vk, &vpos);
   cmark(p, 8);
   // this CTA's share of the selected positions: ranks [Rn*r/CL, Rn*(r+1)/CL)
   // in position order (ordered compaction)
