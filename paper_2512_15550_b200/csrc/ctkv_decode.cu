@@ -597,6 +597,8 @@ __device__ void static_task_tc(const DecodeParams& p, int task, int64_t t0, int6
   constexpr int RB = D * int(sizeof(T));
   constexpr int ST = static_tok<T>();
   static_assert(ST == 16 * (kScanRowsV2 / 32), "one 16-token block per warp");
+  static_assert(kWpStride == ST + 8, "weight rows: ST slots + 16 B bank shift");
+  static_assert(3 * 8 * kWpStride * 2 <= ST * RB, "the weight terms fit over the K rows");
   const int gs = p.gs;
   const int u = task / p.ns, split = task % p.ns;
   const int bi = u / p.g, gi = u % p.g;
