@@ -99,7 +99,7 @@ constexpr int kCW = kCT / 32;
 constexpr int kCB = 128;         // selected rows per attention batch
 constexpr int kCMaxLists = 8;    // c' <= 8
 constexpr int kCMaxPer = 32;     // list entries per thread (keep mask bits)
-constexpr int kVUn = 8;          // V-row passes in flight per warp (2 rows each)
+constexpr int kVUn = 8;          // V-row passes in flight per warp (2 rows each; gs <= 4)
 constexpr int kCBins = 1024;     // top-rho' selection: histogram bins
 constexpr int kCBnd = 256;       // ... and keys ranked exactly in the boundary bin
 constexpr int kRedHeads = 4;     // heads per pass of the cross-warp V-sum reduction
@@ -616,10 +616,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     }
     __syncthreads();
     // the first round of V rows is in flight while the weights are computed
-    uint4 rawv[kVUn];
+    // V-row passes in flight per warp: at gs = 8 the 64 accumulators leave
+    // room for 4 (8 there cost 3 %: cfg3 3,607 vs 3,709 tok/s; 2 also lost)
+    constexpr int VUN = GS >= 8 ? 4 : kVUn;
+    uint4 rawv[VUN];
     const int t00 = warp * VR;
 #pragma unroll
-    for (int x = 0; x < kVUn; ++x) {
+    for (int x = 0; x < VUN; ++x) {
       const int t = t00 + x * kCW * VR + vrw;
       rawv[x] = t < n ? ldg16(reinterpret_cast<const uint4*>(vals_g + (int64_t)S.vid[t] * D) + vsub)
                       : make_uint4(0, 0, 0, 0);
@@ -660,18 +663,18 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     for (int hh = 0; hh < GS; ++hh)
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[hh][e] *= resc[hh];
-    // weighted V rows: VL lanes per row, kVUn passes in flight
-    for (int t0 = t00; t0 < n; t0 += kCW * VR * kVUn) {
+    // weighted V rows: VL lanes per row, VUN passes in flight
+    for (int t0 = t00; t0 < n; t0 += kCW * VR * VUN) {
       if (t0 != t00) {
 #pragma unroll
-        for (int x = 0; x < kVUn; ++x) {
+        for (int x = 0; x < VUN; ++x) {
           const int t = t0 + x * kCW * VR + vrw;
           rawv[x] = t < n ? ldg16(reinterpret_cast<const uint4*>(vals_g + (int64_t)S.vid[t] * D) + vsub)
                           : make_uint4(0, 0, 0, 0);
         }
       }
 #pragma unroll
-      for (int x = 0; x < kVUn; ++x) {
+      for (int x = 0; x < VUN; ++x) {
         const int t = t0 + x * kCW * VR + vrw;
         if (t >= n) continue;
         float f[8];
