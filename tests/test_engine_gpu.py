@@ -33,16 +33,18 @@ def _prefill(q, k, v):
                      dtype=torch.bfloat16, reserve=T + 2, build_mode=0)
 
 
-@pytest.mark.parametrize("lanes,graph,b", [(1, False, B), (2, True, B), (4, True, B), (4, "host", B),
-                                           (4, True, 12)])
-def test_engine_equals_per_layer_decode(lanes, graph, b):
+@pytest.mark.parametrize("lanes,graph,b,nl", [(1, False, B, NL), (2, True, B, NL), (4, True, B, NL),
+                                              (4, "host", B, NL), (2, "host", B, 6), (4, True, 12, NL)])
+def test_engine_equals_per_layer_decode(lanes, graph, b, nl):
     """graph="host": steps from t = 1 run through capture_host_io's two
     graph slots (q/k/v copied in from pinned host buffers per (layer, lane)
-    inside the step, outputs copied out as each layer finishes).  b = 12
+    inside the step, outputs copied out 4 layers at a time).  b = 12
     (24 units, 6 per lane): the per-layer path takes 4-CTA chain clusters and
     so must every lane, although a lane alone would qualify for 8 (the engine
-    passes the whole-batch choice, include/ctkv.h phase bits 32/64)."""
+    passes the whole-batch choice, include/ctkv.h phase bits 32/64).  nl = 6
+    with host I/O: outputs leave in a 4-layer copy and a 2-layer remainder."""
     torch.cuda.set_device(0)
+    NL = nl
     data = [_inputs(li, b) for li in range(NL)]
     cfg = P.DecodeConfig(CP, RP)
     # per-layer drop-in path
