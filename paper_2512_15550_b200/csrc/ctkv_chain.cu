@@ -436,7 +436,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(kCT, 2) chain_kerne
     const double scale = 1.0 / sqrt((double)D);
     const T* keys_g = static_cast<const T*>(p.keys) + (int64_t)u * p.cap * D;
     constexpr int KS2 = D / 32;            // 32-element k pairs per row
-    constexpr int NB = 2;                  // 16-row blocks in flight per warp
+    constexpr int NB = GS >= 8 ? 1 : 2;    // 16-row blocks in flight per warp (1 at gs = 8: registers)
     const int g8 = lane >> 2, t4 = lane & 3;
     const T* qf_base = qs + (g8 < GS ? g8 : 0) * D + 8 * t4;   // B fragments re-read from smem per k-step
     uint32_t rkeys[CL > 1 ? CL - 1 : 1];   // shared::cluster addresses of the other CTAs' keys
